@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 wave-propagation step (contract: see DESIGN.md §7).
+
+Default workload = BASELINE.json configs[1] (C2): 2D shallow water, Roe +
+Harten entropy fix, 1024x1024 cells on [-1,1]^2, MC limiter, second order,
+CFL 0.9, extrapolation BCs, seeded dam-break input.  One bench "step" is one
+time step of that simulation.
+
+Metric: cell-updates/s = nx*ny*steps / time (reference bench.py:194-203).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+  python bench.py --impl reference ...      # reference-path CPU arm
+
+N > 1 (torchrun): weak scaling, row strips of nx x ny per rank stacked along
+y, halo rows + the CFL max exchanged with NCCL every step (parallel.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/sec per step (fp64)"
+UNIT = "cell-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--precision", default=None, choices=[None, "f64", "f32"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def build_case(name: str, n_ranks: int = 1, precision: str | None = None):
+    from paper_1308_1464_b200 import configs
+    if name == "c5":
+        c = configs.c5_bumps(dtype=precision or "f64")
+    else:
+        c = configs.BUILDERS[name]()
+    if precision:
+        c.dtype = precision
+    return c
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md "clocks line")
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port, numpy + threads; the reference itself is numpy)
+
+def cpu_rate(case, seconds: float, threads: int, max_steps: int = 10**9):
+    """Time the oracle port on a bounded sample: whole steps of the same
+    workload until `seconds` of CPU work; returns (cell-updates/s, steps)."""
+    from oracle import wavestep_oracle as O
+    solver = O.make_solver(case.kernel, **case.kernel_params)
+    spec = O.Spec(case.nx, case.ny, case.dx, case.dy)
+    q = np.asfortranarray(case.q.copy())
+    aux = np.asfortranarray(case.aux.copy()) if case.aux is not None else None
+    kw = dict(bc_x=case.bc, bc_y=case.bc, order=case.order, limiter=case.limiter,
+              threads=threads)
+    ctl = O.Controller(case.cfl)
+    O.step(q, aux, spec, solver, ctl, **kw)      # warm-up step (pool start, caches)
+    n, t0 = 0, time.perf_counter()
+    while n < max_steps:
+        O.step(q, aux, spec, solver, ctl, **kw)
+        n += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    return case.nx * case.ny * n / el, n, el
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    case = build_case(args.config, precision=args.precision)
+    threads = os.cpu_count() or 1
+    from oracle import wavestep_oracle as O
+    solver = O.make_solver(case.kernel, **case.kernel_params)
+    spec = O.Spec(case.nx, case.ny, case.dx, case.dy)
+    q = np.asfortranarray(case.q.copy())
+    aux = np.asfortranarray(case.aux.copy()) if case.aux is not None else None
+    kw = dict(bc_x=case.bc, bc_y=case.bc, order=case.order, limiter=case.limiter,
+              threads=threads)
+    ctl = O.Controller(case.cfl)
+    for _ in range(args.warmup):
+        O.step(q, aux, spec, solver, ctl, **kw)
+    # each timed step is one full time step of the workload; K is capped so the
+    # run stays within a few minutes
+    k = args.steps
+    t0 = time.perf_counter()
+    done = 0
+    for _ in range(k):
+        O.step(q, aux, spec, solver, ctl, **kw)
+        done += 1
+        if time.perf_counter() - t0 > 120.0:
+            break
+    el = time.perf_counter() - t0
+    v = case.nx * case.ny * done / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": done, "warmup": args.warmup, "ms_per_step": el * 1e3 / done,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": case.name, "nx": case.nx, "ny": case.ny,
+                   "limiter": case.limiter, "order": case.order, "cfl": case.cfl,
+                   "parallelism": "cpu-threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{done} full time steps of {case.name} "
+                                   f"({case.nx}x{case.ny}) after {args.warmup} warm-up"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def gpu_arm(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        return gpu_arm_sharded(args, rank, world, local)
+
+    from paper_1308_1464_b200 import DeviceGrid, _abi, make_kernel, configs
+    case = build_case(args.config, precision=args.precision)
+    prec = case.dtype
+    kernel = make_kernel(case.kernel, **case.kernel_params)
+    g = DeviceGrid(case.nx, case.ny, case.dx, case.dy, kernel, order=case.order,
+                   limiter=case.limiter, bc_x=case.bc, bc_y=case.bc, precision=prec,
+                   device=local)
+    npdt = np.float64 if prec == "f64" else np.float32
+    host_q = np.asfortranarray(case.q, dtype=npdt)
+    host_aux = np.asfortranarray(case.aux, dtype=npdt) if case.aux is not None else None
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+    ctl = _abi.make_ctl(case.cfl)
+    cells = case.nx * case.ny
+    bpc = configs.bytes_per_cell(case.kernel, prec)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
+
+    g.upload(host_q, host_aux, stream=sp)
+    for _ in range(args.warmup):
+        g.step(ctl, stream=sp)
+    res = g.poll()
+    g.raise_for(res.error)
+
+    dyn = not (case.kernel.startswith("acoustics"))
+    k = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(k)]
+    l0 = g.launches()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        with torch.cuda.stream(stream):
+            # keep the GPU busy while the host enqueues the whole timed loop, so
+            # event gaps are device time, not Python/ctypes launch latency
+            torch.cuda._sleep(int(2e6 + 4e5 * k))
+            for i in range(k):
+                flush.zero_()                     # L2 flush between timed steps
+                ev[i][0].record(stream)
+                if dyn:
+                    g.phase_speeds(stream=sp)
+                ev[i][1].record(stream)
+                if dyn:
+                    g.phase_update(ctl, stream=sp)
+                else:
+                    g.step(ctl, stream=sp)
+                ev[i][2].record(stream)
+        torch.cuda.synchronize()
+    launches = g.launches() - l0
+    res = g.poll()
+    g.raise_for(res.error)
+    t_spd = [ev[i][0].elapsed_time(ev[i][1]) for i in range(k)]
+    t_upd = [ev[i][1].elapsed_time(ev[i][2]) for i in range(k)]
+    total_ms = sum(t_spd) + sum(t_upd)
+    ms_per_step = total_ms / k
+    value = cells * k / (total_ms / 1e3)
+
+    # dominant kernel: the fused update; algorithmic bytes = q read + aux read + q write
+    upd_ms = statistics.mean(t_upd)
+    peak, peak_kind = measured_peak_hbm()
+    achieved = cells * bpc / (upd_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "kernel": "k_update",
+                "peak_kind": peak_kind, "kernel_ms": upd_ms,
+                "speeds_kernel_ms": statistics.mean(t_spd) if dyn else 0.0,
+                "algorithmic_bytes_per_cell": bpc}
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                roofline["traffic"] = json.load(f).get(args.config, {}).get("bytes_per_launch")
+        except Exception:
+            pass
+
+    # whole simulation, device resident: the configured number of steps via graphs
+    g.upload(host_q, host_aux, stream=sp)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    g.run(case.steps, ctl, stream=sp)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    res_run = g.poll()
+    g.raise_for(res_run.error)
+    sim_ms = e0.elapsed_time(e1)
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(g, case, host_q, host_aux, ctl, stream, k)
+    cpu = None
+    if not args.no_cpu:
+        v, n, el = cpu_rate(case, args.cpu_seconds, os.cpu_count() or 1)
+        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+               "sample": f"{n} full time steps of {case.name} ({case.nx}x{case.ny}) "
+                         f"in {el:.1f} s, numpy oracle with {os.cpu_count()} threads"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": k,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+        "config": {"workload": case.name, "kernel": case.kernel, "nx": case.nx,
+                   "ny": case.ny, "limiter": case.limiter, "order": case.order,
+                   "cfl": case.cfl, "bc": case.bc, "parallelism": "single-gpu",
+                   "l2": "flushed between timed steps (512 MiB write)",
+                   "timed_step": "one time step = CFL pre-pass + fused update"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "simulation": {"steps": case.steps, "ms": sim_ms,
+                       "cell_updates_per_s": cells * res_run.steps_done / (sim_ms / 1e3),
+                       "l2": "not flushed (whole run, graph replay)"},
+    }
+    print(json.dumps(line), flush=True)
+    g.close()
+    return 0
+
+
+def e2e_leg(g, case, host_q, host_aux, ctl, stream, k):
+    """Through the public API with host buffers: per step, pinned H2D of the
+    state, one step, D2H of the resulting state (driver.step's contract)."""
+    import torch
+    sp = stream.cuda_stream
+    pin_q = torch.empty(host_q.size, dtype=torch.float64 if host_q.dtype == np.float64
+                        else torch.float32, pin_memory=True).numpy()
+    pin_q = pin_q.reshape(host_q.shape, order="F")
+    pin_q[...] = host_q
+    pin_out = torch.empty_like(torch.from_numpy(np.ascontiguousarray(pin_q.ravel(order="F"))),
+                               pin_memory=True).numpy().reshape(host_q.shape, order="F")
+    pin_aux = None
+    if host_aux is not None:
+        pin_aux = torch.empty(host_aux.size, dtype=torch.from_numpy(host_aux.ravel()).dtype,
+                              pin_memory=True).numpy().reshape(host_aux.shape, order="F")
+        pin_aux[...] = host_aux
+    n = max(3, min(k, 20))
+    for _ in range(2):
+        g.upload(pin_q, pin_aux, stream=sp)
+        g.step(ctl, stream=sp)
+        g.download(pin_out, stream=sp)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        g.upload(pin_q, pin_aux, stream=sp)
+        g.step(ctl, stream=sp)
+        g.download(pin_out, stream=sp)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    res = g.poll()
+    g.raise_for(res.error)
+    hb = pin_q.nbytes + (pin_aux.nbytes if pin_aux is not None else 0)
+    # whole-run variant: one upload, the configured steps, one download
+    t1 = time.perf_counter()
+    g.upload(pin_q, pin_aux, stream=sp)
+    g.run(case.steps, ctl, stream=sp)
+    g.download(pin_out, stream=sp)
+    el2 = time.perf_counter() - t1
+    cells = case.nx * case.ny
+    return {"value": cells * n / el, "unit": UNIT, "h2d_bytes_per_step": hb,
+            "d2h_bytes_per_step": pin_out.nbytes,
+            "api": "DeviceGrid.upload/step/download per step (pinned host, C ABI ws_upload/"
+                   "ws_step/ws_download)",
+            "run_value": cells * case.steps / el2,
+            "run_api": f"upload once, ws_run({case.steps}) graph replay, download once"}
+
+
+def gpu_arm_sharded(args, rank, world, local):
+    from paper_1308_1464_b200 import parallel
+    return parallel.bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate,
+                                  measured_peak_hbm, METRIC, UNIT)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,177 @@
+/*
+ * wavestep.h — C ABI of the B200-native 2D wave-propagation step.
+ *
+ * Drop-in boundary for the hot path of the reference package `wavesweep`
+ * (/root/reference/pkg/src/wavesweep).  The reference is pure Python, so
+ * its "FFI" is the Python call surface; each entry point below states the
+ * reference interface it replaces.  The Python host layer
+ * (paper_1308_1464_b200/_abi.py) binds exactly these symbols with ctypes;
+ * INTEGRATION.md shows the binding.
+ *
+ * Types are plain C: no torch or CUDA types appear in the signatures
+ * (streams are passed as `void*` holding a cudaStream_t, NULL = the
+ * handle's own stream).  All reals on the host side are float64 in the
+ * reference's layout: arrays of shape (ncomp, nx+4, ny+4), Fortran order
+ * (component fastest, then i, then j), two ghost layers
+ * (reference grid.py:76-95).  Device storage is the handle's own
+ * structure-of-arrays layout.
+ *
+ * Return codes (every int-returning function):
+ *   WS_OK (0), WS_ERR_KERNEL (1: inadmissible state, see ws_error_info),
+ *   WS_ERR_CONFIG (2: bad descriptor / argument, message in ws_last_error),
+ *   WS_ERR_CUDA (3), WS_ERR_STATIONARY (4: all wave speeds zero and no
+ *   fixed_dt — reference driver.py:330-331 raises ValueError).
+ */
+#ifndef WAVESTEP_H
+#define WAVESTEP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WS_ABI_VERSION 1
+
+enum ws_status { WS_OK = 0, WS_ERR_KERNEL = 1, WS_ERR_CONFIG = 2, WS_ERR_CUDA = 3,
+                 WS_ERR_STATIONARY = 4 };
+
+/* Riemann solvers: reference kernels.py:282-287 (DESCRIPTORS) plus the two
+ * north-star solvers the reference lacks. */
+enum ws_solver { WS_ACOUSTICS_CONST = 0,   /* kernels.py:374-406, params rho, bulk      */
+                 WS_ACOUSTICS_VAR = 1,     /* kernels.py:409-454, aux (rho, c)          */
+                 WS_EULER_ROE = 2,         /* kernels.py:457-533, params gamma          */
+                 WS_EULER_HLLE = 3,        /* extension, params gamma                   */
+                 WS_SHALLOW_ROE = 4 };     /* extension (Roe + Harten fix), params grav */
+
+enum ws_limiter { WS_LIM_NONE = 0, WS_LIM_MINMOD = 1, WS_LIM_SUPERBEE = 2, WS_LIM_MC = 3 };
+enum ws_bc { WS_BC_PERIODIC = 0, WS_BC_EXTRAPOLATE = 1 };  /* grid.py:12-16 */
+enum ws_precision { WS_FP64 = 0, WS_FP32 = 1 };
+/* how the rows below j = 0 / above j = ny of THIS shard are obtained */
+enum ws_rowmode { WS_ROWS_MEMORY = 0,   /* ghost rows in memory (halo exchange) */
+                  WS_ROWS_BC = 1 };     /* physical boundary: apply bc_y         */
+
+/* Replaces GridSpec (grid.py:19-50) + SimulationConfig (driver.py:340-363)
+ * + make_kernel (kernels.py:589-633) for one shard. */
+typedef struct ws_desc {
+  int32_t nx, ny;            /* interior cells of this shard (ny = local rows)      */
+  double dx, dy;             /* cell widths                                         */
+  int32_t num_ghost;         /* must be 2 (reference default grid.py:36)            */
+  int32_t solver;            /* enum ws_solver                                      */
+  double params[4];          /* acoustics-const: rho, bulk; euler*: gamma; sw: grav */
+  int32_t order;             /* 1 = reference donor cell, 2 = + limited correction */
+  int32_t limiter;           /* enum ws_limiter (ignored for order 1)               */
+  int32_t bc_x, bc_y;        /* enum ws_bc                                          */
+  int32_t precision;         /* enum ws_precision                                   */
+  int32_t device;            /* CUDA ordinal                                        */
+  /* row-strip decomposition (reference has none: SPEC.md:89 non-goal) */
+  int32_t ny_global;         /* rows of the whole domain (== ny for one shard)      */
+  int32_t j_offset;          /* global row of local row 0                            */
+  int32_t rows_lo, rows_hi;  /* enum ws_rowmode for the bottom / top ghost rows     */
+  /* optional borrowed device buffers (NULL = the handle allocates).  Sizes
+   * from ws_buffer_bytes().  q0 receives uploads; steps ping-pong q0 <-> q1. */
+  void *ext_q0, *ext_q1, *ext_aux, *ext_slots;
+} ws_desc;
+
+/* Replaces TimestepController (driver.py:297-311) + the `remaining`
+ * argument of step() (driver.py:479-481).  NaN = "None". */
+typedef struct ws_ctl {
+  double cfl;        /* cfl_target in (0,1)                   */
+  double dt_max;     /* NaN = None                            */
+  double fixed_dt;   /* NaN = None                            */
+  double remaining;  /* NaN = None (per-step clamp)           */
+  double t_final;    /* NaN = None; device-side run() target  */
+} ws_ctl;
+
+/* Replaces StepReport (driver.py:366-375), minus the wall-clock fields. */
+typedef struct ws_report {
+  double dt, cfl, max_speed_x, max_speed_y;
+} ws_report;
+
+/* Replaces SweepError (sweep.py:68-75) / KernelError (kernels.py:237-248). */
+typedef struct ws_error_info {
+  int32_t code;        /* 0 none, else enum ws_status                          */
+  int32_t direction;   /* 0 = x-interface, 1 = y-interface                     */
+  int32_t i, j;        /* global interface indices                              */
+  int32_t stage;       /* index of the failed admissibility test, solver order  */
+  int32_t component;   /* component for non-finite tests                        */
+  int64_t step;        /* step index (since upload) that failed                */
+} ws_error_info;
+
+typedef struct ws_handle ws_handle;
+
+int ws_abi_version(void);
+
+/* Layout of the borrowed buffers a caller may provide in ws_desc. */
+int ws_buffer_bytes(const ws_desc* d, uint64_t* q_bytes, uint64_t* aux_bytes,
+                    uint64_t* slots_bytes);
+
+int ws_create(const ws_desc* d, ws_handle** out);
+void ws_destroy(ws_handle* h);
+/* last message; h may be NULL for ws_create failures */
+const char* ws_last_error(const ws_handle* h);
+
+/* Host <-> device.  Host arrays use the reference layout (ncomp, nx+4, ny+4)
+ * Fortran order.  Pinned host memory makes the copies asynchronous.
+ * Replaces the StateField/AuxField data hand-off (grid.py:86-95). */
+int ws_upload(ws_handle* h, const double* q_host, const double* aux_host, void* stream);
+int ws_download(ws_handle* h, double* q_host, void* stream);
+/* fp32 handles: same calls with float arrays */
+int ws_upload_f32(ws_handle* h, const float* q_host, const float* aux_host, void* stream);
+int ws_download_f32(ws_handle* h, float* q_host, void* stream);
+
+/* One step, enqueued only (no host sync): fill ghosts (implicit, by index
+ * mapping) -> sweep -> choose_dt on device -> update.
+ * Replaces driver.step (driver.py:479-505). */
+int ws_step(ws_handle* h, const ws_ctl* c, void* stream);
+/* nsteps steps through a captured CUDA graph; stops early on error or when
+ * t_final is reached.  Replaces driver.run's loop (driver.py:508-530). */
+int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* stream);
+
+/* Split step for multi-shard runs: the caller all-reduces the 3 x uint64
+ * slot (MAX) between the two phases and exchanges halo rows before phase 1.
+ * ws_step == ws_phase_speeds + ws_phase_update on one shard. */
+int ws_phase_speeds(ws_handle* h, void* stream);
+int ws_phase_update(ws_handle* h, const ws_ctl* c, void* stream);
+/* device pointer of the current step's 3 x uint64 reduction slot */
+void* ws_slot_ptr(ws_handle* h);
+/* device pointers of the current state's halo rows (2 rows x all components,
+ * contiguous): send_lo = rows 0,1; send_hi = rows ny-2,ny-1; recv_lo = rows
+ * -2,-1; recv_hi = rows ny,ny+1.  bytes = size of each block. */
+int ws_halo_ptrs(ws_handle* h, void** send_lo, void** send_hi, void** recv_lo,
+                 void** recv_hi, uint64_t* bytes);
+/* device pointer of the current state buffer and its row geometry */
+int ws_state_ptr(ws_handle* h, void** q, int64_t* pitch_elems, int64_t* row_elems);
+
+/* Synchronise and read what the device recorded: number of committed steps
+ * since upload, their reports (the last min(n, max) of them), time t, and
+ * the error record.  Reports are consumed (cleared) by this call. */
+int ws_poll(ws_handle* h, int64_t* steps_done, ws_report* reports, int32_t max_reports,
+            int32_t* n_reports, double* t_now, ws_error_info* err);
+int ws_sync(ws_handle* h);
+
+/* Pointwise plugin call, batched: replaces Kernel.solve(direction, ql, qr,
+ * auxl, auxr) -> RiemannResult (kernels.py:567-586) for one solver on n
+ * interfaces.  Host arrays, C order: ql/qr (num_eqn, n), aux (num_aux, n)
+ * or NULL, waves (num_waves, num_eqn, n), speeds (num_waves, n),
+ * amdq/apdq (num_eqn, n), codes (n): 0 admissible, else
+ * (stage + 1) | (component << 8) of the first failed test in the
+ * reference's order.  direction 0 = x, 1 = y.  fp64 only. */
+int ws_riemann(int32_t solver, const double* params, int32_t direction, int64_t n,
+               const double* ql, const double* qr, const double* auxl, const double* auxr,
+               double* waves, double* speeds, double* amdq, double* apdq, int32_t* codes,
+               int32_t device);
+
+/* In-place ghost fill of a host field (ncomp, nx+4, ny+4) F-order on the
+ * device: replaces fill_ghost (grid.py:179-193; x pass then y pass). */
+int ws_fill_ghost(double* data, int32_t ncomp, int32_t nx, int32_t ny, int32_t bc_x,
+                  int32_t bc_y, int32_t device);
+
+/* number of kernel launches this handle has issued (bench evidence) */
+int64_t ws_launch_count(const ws_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WAVESTEP_H */

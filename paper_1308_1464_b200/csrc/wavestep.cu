@@ -1,0 +1,813 @@
+// wavestep.cu — C-ABI implementation (include/wavestep.h).
+//
+// One handle = one shard of the grid on one GPU: ping-pong state buffers,
+// aux, the device step state (reductions, reports, errors) and a stream.
+// ws_step enqueues the CFL pre-pass (dynamic-speed solvers) and the fused
+// update kernel without any host synchronisation; ws_run replays a captured
+// two-step CUDA graph.  The translation unit is compiled with --fmad=false
+// (bitwise parity with the numpy oracle, see ws_solvers.cuh).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/wavestep.h"
+#include "ws_kernels.cuh"
+
+using namespace ws;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+template <class S, class R, int ORDER> struct TileCfg {
+  static constexpr int TX = 32, TY = 16, NT = 256;
+};
+// Euler-Roe's 15-value wave record would cap residency at 1 CTA/SM at 32x16
+template <class R> struct TileCfg<EulerRoe, R, 2> {
+  static constexpr int TX = 32, TY = 8, NT = 256;
+};
+constexpr int SPD_TX = 32, SPD_TY = 8;
+
+struct Ops {
+  void (*speeds)(ws_handle*, const void* q, int cur, cudaStream_t);
+  void (*update)(ws_handle*, const void* q, void* qn, const StepArgs&, cudaStream_t);
+  void (*to_soa)(ws_handle*, const void* stage, void* dst, int ncomp, cudaStream_t);
+  void (*to_aos)(ws_handle*, const void* cur, const void* gsrc, void* stage, cudaStream_t);
+  void (*static_speed)(ws_handle*, cudaStream_t);
+  void (*prepare)();   // one-time kernel attributes (never inside a capture)
+  int static_speeds;   // solver has q-independent speeds
+};
+
+}  // namespace
+
+struct ws_handle {
+  ws_desc d{};
+  int neq = 0, naux = 0;
+  size_t esz = 8;
+  Layout L{};
+  void* q[2] = {nullptr, nullptr};
+  void* aux = nullptr;
+  DevState* ds = nullptr;
+  bool own_q[2] = {false, false}, own_aux = false, own_ds = false;
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t last_stream = nullptr;
+  long long enq = 0;            // steps enqueued since upload (== committed after a poll)
+  long long nrep_seen = 0;
+  bool multi = false;           // row-strip shard with memory ghost rows
+  bool uploaded = false;
+  double host_static[2] = {0, 0};
+  Ops ops{};
+  std::vector<char> params;     // typed Params<R> blob
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  ws_ctl gctl{};
+  cudaStream_t gstream = nullptr;
+  long long launches = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(ws_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg; else g_create_error = msg;
+  return code;
+}
+
+int cuda_fail(ws_handle* h, cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  return fail(h, WS_ERR_CUDA, m);
+}
+
+#define WS_CUDA(h, call)                                   \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_fail((h), e_, #call); \
+  } while (0)
+
+cudaStream_t pick(ws_handle* h, void* s) {
+  cudaStream_t st = s ? reinterpret_cast<cudaStream_t>(s) : h->stream;
+  h->last_stream = st;
+  return st;
+}
+
+// ---- typed launchers -----------------------------------------------------
+template <class S, class R, int ORDER, int LIM> struct Impl {
+  using P = typename S::template Params<R>;
+  using C = TileCfg<S, R, ORDER>;
+  using G = TileGeom<S, ORDER, C::TX, C::TY>;
+
+  static const P& prm(ws_handle* h) { return *reinterpret_cast<const P*>(h->params.data()); }
+
+  static void speeds(ws_handle* h, const void* q, int cur, cudaStream_t st) {
+    dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + SPD_TY - 1) / SPD_TY);
+    k_speeds<S, R, SPD_TX, SPD_TY><<<grid, SPD_TX * SPD_TY, 0, st>>>(
+        static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
+    h->launches++;
+  }
+
+  static void prepare() {
+    const int smem = (int)G::template smem_bytes<R>();
+    cudaFuncSetAttribute(k_update<S, R, ORDER, LIM, C::TX, C::TY, C::NT, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_update<S, R, ORDER, LIM, C::TX, C::TY, C::NT, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+
+  template <bool CHECKS> static void update_t(ws_handle* h, const void* q, void* qn,
+                                              const StepArgs& a, cudaStream_t st) {
+    auto k = k_update<S, R, ORDER, LIM, C::TX, C::TY, C::NT, CHECKS>;
+    const size_t smem = G::template smem_bytes<R>();
+    dim3 grid((h->L.nx + C::TX - 1) / C::TX, (h->L.ny + C::TY - 1) / C::TY);
+    k<<<grid, C::NT, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
+                                 static_cast<R*>(qn), h->L, prm(h), a, h->ds);
+    h->launches++;
+  }
+
+  static void update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
+    if (S::STATIC_SPEEDS && !h->multi) update_t<true>(h, q, qn, a, st);
+    else update_t<false>(h, q, qn, a, st);
+  }
+
+  static void to_soa(ws_handle* h, const void* stage, void* dst, int ncomp, cudaStream_t st) {
+    int blocks = 148 * 8;
+    k_to_soa<R, R><<<blocks, 256, 0, st>>>(static_cast<const R*>(stage), static_cast<R*>(dst),
+                                           ncomp, h->L.nx, h->L.ny, h->L.pitch);
+    h->launches++;
+  }
+
+  static void to_aos(ws_handle* h, const void* cur, const void* gsrc, void* stage,
+                     cudaStream_t st) {
+    int blocks = 148 * 8;
+    k_to_aos<R, R><<<blocks, 256, 0, st>>>(static_cast<const R*>(cur),
+                                           static_cast<const R*>(gsrc), static_cast<R*>(stage),
+                                           h->L, h->neq);
+    h->launches++;
+  }
+
+  static void static_speed(ws_handle* h, cudaStream_t st) {
+    if (S::NAUX > 0) {
+      k_static_speed<R><<<148 * 4, 256, 0, st>>>(static_cast<const R*>(h->aux), h->L, h->ds);
+      h->launches++;
+    }
+  }
+
+  static Ops ops() {
+    Ops o;
+    o.speeds = &speeds;
+    o.update = &update;
+    o.to_soa = &to_soa;
+    o.to_aos = &to_aos;
+    o.static_speed = &static_speed;
+    o.prepare = &prepare;
+    o.static_speeds = S::STATIC_SPEEDS ? 1 : 0;
+    return o;
+  }
+};
+
+template <class S, class R> Ops pick_lim(int order, int lim) {
+  if (order == 1 || lim == LIM_NONE) return Impl<S, R, 1, LIM_NONE>::ops();
+  switch (lim) {
+    case LIM_MINMOD: return Impl<S, R, 2, LIM_MINMOD>::ops();
+    case LIM_SUPERBEE: return Impl<S, R, 2, LIM_SUPERBEE>::ops();
+    default: return Impl<S, R, 2, LIM_MC>::ops();
+  }
+}
+
+template <class R> bool bind(ws_handle* h, std::string& msg) {
+  const ws_desc& d = h->d;
+  const double* p = d.params;
+  switch (d.solver) {
+    case WS_ACOUSTICS_CONST: {
+      // reference kernels.py:299-311: both positive; c = sqrt(K/rho), Z = rho*c
+      if (!(p[0] > 0 && p[1] > 0)) {
+        char b[160];
+        snprintf(b, sizeof b, "density and bulk modulus must be positive, got %.17g, %.17g",
+                 p[0], p[1]);
+        msg = b;
+        return false;
+      }
+      double c = std::sqrt(p[1] / p[0]);
+      double z = p[0] * c;
+      AcousticsConst::Params<R> pr{(R)z, (R)(2.0 * z), (R)c};
+      h->params.assign((char*)&pr, (char*)&pr + sizeof pr);
+      h->host_static[0] = h->host_static[1] = (double)(R)c;
+      h->ops = pick_lim<AcousticsConst, R>(d.order, d.limiter);
+      h->neq = 3; h->naux = 0;
+      return true;
+    }
+    case WS_ACOUSTICS_VAR: {
+      AcousticsVar::Params<R> pr{(R)0};
+      h->params.assign((char*)&pr, (char*)&pr + sizeof pr);
+      h->ops = pick_lim<AcousticsVar, R>(d.order, d.limiter);
+      h->neq = 3; h->naux = 2;
+      return true;
+    }
+    case WS_EULER_ROE:
+    case WS_EULER_HLLE: {
+      if (!(p[0] > 1.0)) {
+        char b[96];
+        snprintf(b, sizeof b, "gamma must exceed 1, got %.17g", p[0]);
+        msg = b;
+        return false;
+      }
+      if (d.solver == WS_EULER_ROE) {
+        EulerRoe::Params<R> pr{(R)(p[0] - 1.0)};
+        h->params.assign((char*)&pr, (char*)&pr + sizeof pr);
+        h->ops = pick_lim<EulerRoe, R>(d.order, d.limiter);
+      } else {
+        EulerHLLE::Params<R> pr{(R)(p[0] - 1.0), (R)p[0]};
+        h->params.assign((char*)&pr, (char*)&pr + sizeof pr);
+        h->ops = pick_lim<EulerHLLE, R>(d.order, d.limiter);
+      }
+      h->neq = 4; h->naux = 0;
+      return true;
+    }
+    case WS_SHALLOW_ROE: {
+      if (!(p[0] > 0)) {
+        char b[96];
+        snprintf(b, sizeof b, "gravity must be positive, got %.17g", p[0]);
+        msg = b;
+        return false;
+      }
+      ShallowRoe::Params<R> pr{(R)p[0], (R)std::sqrt(p[0])};
+      h->params.assign((char*)&pr, (char*)&pr + sizeof pr);
+      h->ops = pick_lim<ShallowRoe, R>(d.order, d.limiter);
+      h->neq = 3; h->naux = 0;
+      return true;
+    }
+  }
+  msg = "unknown solver id " + std::to_string(d.solver);
+  return false;
+}
+
+long long pitch_for(int nx, size_t esz) {
+  // 256-byte aligned component rows (coalescing; TMA-compatible strides)
+  long long per = 256 / (long long)esz;
+  return ((long long)nx + per - 1) / per * per;
+}
+
+int validate(const ws_desc* d, std::string& m) {
+  char b[200];
+  if (d->nx < 1 || d->ny < 1) {
+    snprintf(b, sizeof b, "cell counts must be >= 1, got nx=%d, ny=%d", d->nx, d->ny);
+    m = b; return WS_ERR_CONFIG;
+  }
+  if (!(d->dx > 0 && d->dy > 0)) {
+    snprintf(b, sizeof b, "cell widths must be > 0, got dx=%.17g, dy=%.17g", d->dx, d->dy);
+    m = b; return WS_ERR_CONFIG;
+  }
+  if (d->num_ghost != 2) {
+    snprintf(b, sizeof b, "the device layout uses num_ghost=2, got %d", d->num_ghost);
+    m = b; return WS_ERR_CONFIG;
+  }
+  if (d->order != 1 && d->order != 2) {
+    snprintf(b, sizeof b, "order must be 1 or 2, got %d", d->order);
+    m = b; return WS_ERR_CONFIG;
+  }
+  if (d->limiter < 0 || d->limiter > 3) { m = "unknown limiter"; return WS_ERR_CONFIG; }
+  if ((d->bc_x != 0 && d->bc_x != 1) || (d->bc_y != 0 && d->bc_y != 1)) {
+    m = "unknown boundary condition"; return WS_ERR_CONFIG;
+  }
+  if (d->precision != WS_FP64 && d->precision != WS_FP32) {
+    m = "unknown precision"; return WS_ERR_CONFIG;
+  }
+  // reference grid.py:165-169
+  if (d->bc_x == WS_BC_PERIODIC && d->nx < 2) {
+    snprintf(b, sizeof b, "periodic boundary needs at least num_ghost=2 interior cells, got %d",
+             d->nx);
+    m = b; return WS_ERR_CONFIG;
+  }
+  bool multi = d->rows_lo == WS_ROWS_MEMORY || d->rows_hi == WS_ROWS_MEMORY;
+  if (!multi && d->bc_y == WS_BC_PERIODIC && d->ny < 2) {
+    snprintf(b, sizeof b, "periodic boundary needs at least num_ghost=2 interior cells, got %d",
+             d->ny);
+    m = b; return WS_ERR_CONFIG;
+  }
+  if (multi && d->ny < 2) { m = "a row-strip shard needs at least 2 rows"; return WS_ERR_CONFIG; }
+  if (d->ny_global < d->ny || d->j_offset < 0 || d->j_offset + d->ny > d->ny_global) {
+    m = "inconsistent row-strip geometry (ny_global / j_offset)"; return WS_ERR_CONFIG;
+  }
+  if (d->nx >= (1 << 19) || d->ny_global >= (1 << 19)) {
+    m = "grid too large for the 19-bit interface indices of the error key"; return WS_ERR_CONFIG;
+  }
+  return WS_OK;
+}
+
+void compute_layout(ws_handle* h) {
+  const ws_desc& d = h->d;
+  Layout& L = h->L;
+  L.nx = d.nx; L.ny = d.ny;
+  bool top = d.j_offset + d.ny == d.ny_global;
+  L.ny_edges_y = d.ny + (top ? 1 : 0);
+  L.bcx = d.bc_x; L.bcy = d.bc_y;
+  L.lo = d.rows_lo == WS_ROWS_MEMORY ? ROWS_MEMORY : ROWS_BC;
+  L.hi = d.rows_hi == WS_ROWS_MEMORY ? ROWS_MEMORY : ROWS_BC;
+  L.j_off = d.j_offset;
+  L.nx_glob = d.nx;
+  L.pitch = pitch_for(d.nx, h->esz);
+  L.rstride = (long long)h->neq * L.pitch;
+  L.astride = (long long)h->naux * L.pitch;
+}
+
+StepArgs make_args(ws_handle* h, const ws_ctl* c, int cur) {
+  StepArgs a{};
+  a.dx = h->d.dx; a.dy = h->d.dy;
+  a.cfl = c->cfl;
+  a.has_dt_max = !std::isnan(c->dt_max); a.dt_max = c->dt_max;
+  a.has_fixed = !std::isnan(c->fixed_dt); a.fixed_dt = c->fixed_dt;
+  a.has_remaining = !std::isnan(c->remaining); a.remaining = c->remaining;
+  a.has_t_final = !std::isnan(c->t_final); a.t_final = c->t_final;
+  a.tol = a.has_t_final ? 1e-14 * std::fmax(1.0, c->t_final) : 0.0;   // driver.py:525
+  a.cur = cur;
+  a.static_speeds = (h->ops.static_speeds && !h->multi) ? 1 : 0;
+  return a;
+}
+
+int check_ctl(ws_handle* h, const ws_ctl* c) {
+  // reference driver.py:305-311
+  char b[128];
+  if (!(c->cfl > 0.0 && c->cfl < 1.0)) {
+    snprintf(b, sizeof b, "cfl_target must lie in (0, 1), got %.17g", c->cfl);
+    return fail(h, WS_ERR_CONFIG, b);
+  }
+  if (!std::isnan(c->dt_max) && !(c->dt_max > 0)) return fail(h, WS_ERR_CONFIG, "dt_max must be positive");
+  if (!std::isnan(c->fixed_dt) && !(c->fixed_dt > 0)) return fail(h, WS_ERR_CONFIG, "fixed_dt must be positive");
+  return WS_OK;
+}
+
+// enqueue one step of parity `cur` from q[cur] into q[cur^1]
+void enqueue_step(ws_handle* h, const ws_ctl* c, int cur, cudaStream_t st) {
+  StepArgs a = make_args(h, c, cur);
+  if (!a.static_speeds) h->ops.speeds(h, h->q[cur], cur, st);
+  h->ops.update(h, h->q[cur], h->q[cur ^ 1], a, st);
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int ws_abi_version(void) { return WS_ABI_VERSION; }
+
+int ws_buffer_bytes(const ws_desc* d, uint64_t* q_bytes, uint64_t* aux_bytes,
+                    uint64_t* slots_bytes) {
+  std::string m;
+  int rc = validate(d, m);
+  if (rc) return fail(nullptr, rc, m);
+  size_t esz = d->precision == WS_FP32 ? 4 : 8;
+  int neq = (d->solver == WS_EULER_ROE || d->solver == WS_EULER_HLLE) ? 4 : 3;
+  int naux = d->solver == WS_ACOUSTICS_VAR ? 2 : 0;
+  long long pitch = pitch_for(d->nx, esz);
+  if (q_bytes) *q_bytes = (uint64_t)(d->ny + 4) * neq * pitch * esz;
+  if (aux_bytes) *aux_bytes = (uint64_t)(d->ny + 4) * naux * pitch * esz;
+  if (slots_bytes) *slots_bytes = sizeof(DevState);
+  return WS_OK;
+}
+
+int ws_create(const ws_desc* d, ws_handle** out) {
+  if (!d || !out) return fail(nullptr, WS_ERR_CONFIG, "null argument");
+  *out = nullptr;
+  std::string m;
+  int rc = validate(d, m);
+  if (rc) return fail(nullptr, rc, m);
+  ws_handle* h = new ws_handle();
+  h->d = *d;
+  h->esz = d->precision == WS_FP32 ? 4 : 8;
+  h->multi = d->rows_lo == WS_ROWS_MEMORY || d->rows_hi == WS_ROWS_MEMORY;
+  bool ok = d->precision == WS_FP32 ? bind<float>(h, m) : bind<double>(h, m);
+  if (!ok) { delete h; return fail(nullptr, WS_ERR_CONFIG, m); }
+  compute_layout(h);
+  cudaError_t e = cudaSetDevice(d->device);
+  if (e != cudaSuccess) { delete h; return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e)); }
+  uint64_t qb, ab, sb;
+  ws_buffer_bytes(d, &qb, &ab, &sb);
+  auto get = [&](void* ext, size_t bytes, void** dst, bool* own) -> cudaError_t {
+    if (bytes == 0) { *dst = nullptr; *own = false; return cudaSuccess; }
+    if (ext) { *dst = ext; *own = false; return cudaSuccess; }
+    *own = true;
+    return cudaMalloc(dst, bytes);
+  };
+  void* dsp = nullptr;
+  if ((e = get(d->ext_q0, qb, &h->q[0], &h->own_q[0])) != cudaSuccess ||
+      (e = get(d->ext_q1, qb, &h->q[1], &h->own_q[1])) != cudaSuccess ||
+      (e = get(d->ext_aux, ab, &h->aux, &h->own_aux)) != cudaSuccess ||
+      (e = get(d->ext_slots, sb, &dsp, &h->own_ds)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    ws_destroy(h);
+    return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+  }
+  h->ds = static_cast<DevState*>(dsp);
+  h->ops.prepare();
+  // zero everything once so ghost rows / padding are defined
+  cudaMemsetAsync(h->q[0], 0, qb, h->stream);
+  cudaMemsetAsync(h->q[1], 0, qb, h->stream);
+  if (h->aux) cudaMemsetAsync(h->aux, 0, ab, h->stream);
+  cudaMemsetAsync(h->ds, 0, sb, h->stream);
+  e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) { ws_destroy(h); return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e)); }
+  *out = h;
+  return WS_OK;
+}
+
+void ws_destroy(ws_handle* h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (int k = 0; k < 2; ++k) if (h->own_q[k] && h->q[k]) cudaFree(h->q[k]);
+  if (h->own_aux && h->aux) cudaFree(h->aux);
+  if (h->own_ds && h->ds) cudaFree(h->ds);
+  if (h->stage) cudaFree(h->stage);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+const char* ws_last_error(const ws_handle* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+static int ensure_stage(ws_handle* h, size_t bytes) {
+  if (h->stage_bytes >= bytes) return WS_OK;
+  if (h->stage) { cudaStreamSynchronize(h->stream); cudaFree(h->stage); h->stage = nullptr; }
+  WS_CUDA(h, cudaMalloc(&h->stage, bytes));
+  h->stage_bytes = bytes;
+  return WS_OK;
+}
+
+static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz, void* s) {
+  if (!h || !qh) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (hesz != h->esz) return fail(h, WS_ERR_CONFIG, "host precision does not match the handle");
+  if (h->naux > 0 && !ah) return fail(h, WS_ERR_CONFIG, "this solver needs aux data");
+  cudaStream_t st = pick(h, s);
+  const size_t cells = (size_t)(h->d.nx + 4) * (h->d.ny + 4);
+  int ncmax = h->neq > h->naux ? h->neq : h->naux;
+  int rc = ensure_stage(h, cells * ncmax * h->esz);
+  if (rc) return rc;
+  WS_CUDA(h, cudaMemcpyAsync(h->stage, qh, cells * h->neq * h->esz, cudaMemcpyHostToDevice, st));
+  h->ops.to_soa(h, h->stage, h->q[0], h->neq, st);
+  if (h->naux > 0) {
+    WS_CUDA(h, cudaMemcpyAsync(h->stage, ah, cells * h->naux * h->esz, cudaMemcpyHostToDevice, st));
+    h->ops.to_soa(h, h->stage, h->aux, h->naux, st);
+  }
+  WS_CUDA(h, cudaMemsetAsync(h->ds, 0, offsetof(DevState, rep), st));
+  if (h->ops.static_speeds) {
+    if (h->naux > 0) {
+      h->ops.static_speed(h, st);
+    } else {
+      unsigned long long b[2];
+      if (h->esz == 8) { std::memcpy(&b[0], &h->host_static[0], 8); }
+      else { float f = (float)h->host_static[0]; unsigned u; std::memcpy(&u, &f, 4); b[0] = u; }
+      b[1] = b[0];
+      // pageable source: synchronous w.r.t. the host, ordered on st
+      WS_CUDA(h, cudaMemcpyAsync(&h->ds->static_bits[0], b, sizeof b, cudaMemcpyHostToDevice, st));
+      WS_CUDA(h, cudaStreamSynchronize(st));
+    }
+  }
+  WS_CUDA(h, cudaGetLastError());
+  h->enq = 0;
+  h->nrep_seen = 0;
+  h->uploaded = true;
+  return WS_OK;
+}
+
+int ws_upload(ws_handle* h, const double* q, const double* a, void* s) {
+  return upload_impl(h, q, a, 8, s);
+}
+int ws_upload_f32(ws_handle* h, const float* q, const float* a, void* s) {
+  return upload_impl(h, q, a, 4, s);
+}
+
+// host view of the DevState header
+struct HostState {
+  long long steps, err_step, nrep;
+  unsigned long long err_key;
+  int err, finished;
+  double t;
+};
+
+static int read_state(ws_handle* h, HostState* hs, cudaStream_t st) {
+  DevState tmp;
+  WS_CUDA(h, cudaStreamSynchronize(st));
+  if (h->stream != st) WS_CUDA(h, cudaStreamSynchronize(h->stream));
+  WS_CUDA(h, cudaMemcpy(&tmp, h->ds, offsetof(DevState, rep), cudaMemcpyDeviceToHost));
+  hs->steps = tmp.steps; hs->err_step = tmp.err_step; hs->nrep = tmp.nrep;
+  hs->err_key = tmp.err_key; hs->err = tmp.err; hs->finished = tmp.finished; hs->t = tmp.t;
+  return WS_OK;
+}
+
+// after a sync: re-align the enqueue counter with what the device committed
+static int resync(ws_handle* h, const HostState& hs, cudaStream_t st) {
+  if (h->enq != hs.steps) {
+    h->enq = hs.steps;
+    WS_CUDA(h, cudaMemsetAsync(&h->ds->slot[0][0], 0, sizeof(h->ds->slot), st));
+  }
+  return WS_OK;
+}
+
+static int download_impl(ws_handle* h, void* qh, size_t hesz, void* s) {
+  if (!h || !qh) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (hesz != h->esz) return fail(h, WS_ERR_CONFIG, "host precision does not match the handle");
+  cudaStream_t st = pick(h, s);
+  HostState hs;
+  int rc = read_state(h, &hs, st);
+  if (rc) return rc;
+  if ((rc = resync(h, hs, st))) return rc;
+  const int cur = (int)(hs.steps & 1);
+  // ghosts hold the BC fill of the state the last (attempted) step started from
+  const void* gsrc = (hs.steps == 0 || hs.err) ? h->q[cur] : h->q[cur ^ 1];
+  const size_t bytes = (size_t)(h->d.nx + 4) * (h->d.ny + 4) * h->neq * h->esz;
+  if ((rc = ensure_stage(h, bytes))) return rc;
+  h->ops.to_aos(h, h->q[cur], gsrc, h->stage, st);
+  WS_CUDA(h, cudaMemcpyAsync(qh, h->stage, bytes, cudaMemcpyDeviceToHost, st));
+  WS_CUDA(h, cudaStreamSynchronize(st));
+  return WS_OK;
+}
+
+int ws_download(ws_handle* h, double* q, void* s) { return download_impl(h, q, 8, s); }
+int ws_download_f32(ws_handle* h, float* q, void* s) { return download_impl(h, q, 4, s); }
+
+int ws_step(ws_handle* h, const ws_ctl* c, void* s) {
+  if (!h || !c) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (!h->uploaded) return fail(h, WS_ERR_CONFIG, "no state uploaded");
+  int rc = check_ctl(h, c);
+  if (rc) return rc;
+  cudaStream_t st = pick(h, s);
+  if (!std::isnan(c->t_final)) WS_CUDA(h, cudaMemsetAsync(&h->ds->finished, 0, sizeof(int), st));
+  enqueue_step(h, c, (int)(h->enq & 1), st);
+  h->enq++;
+  WS_CUDA(h, cudaGetLastError());
+  return WS_OK;
+}
+
+int ws_phase_speeds(ws_handle* h, void* s) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  cudaStream_t st = pick(h, s);
+  h->ops.speeds(h, h->q[h->enq & 1], (int)(h->enq & 1), st);
+  WS_CUDA(h, cudaGetLastError());
+  return WS_OK;
+}
+
+int ws_phase_update(ws_handle* h, const ws_ctl* c, void* s) {
+  if (!h || !c) return fail(h, WS_ERR_CONFIG, "null argument");
+  int rc = check_ctl(h, c);
+  if (rc) return rc;
+  cudaStream_t st = pick(h, s);
+  const int cur = (int)(h->enq & 1);
+  StepArgs a = make_args(h, c, cur);
+  h->ops.update(h, h->q[cur], h->q[cur ^ 1], a, st);
+  h->enq++;
+  WS_CUDA(h, cudaGetLastError());
+  return WS_OK;
+}
+
+void* ws_slot_ptr(ws_handle* h) { return h ? (void*)&h->ds->slot[h->enq & 1][0] : nullptr; }
+
+int ws_halo_ptrs(ws_handle* h, void** slo, void** shi, void** rlo, void** rhi, uint64_t* bytes) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  char* b = static_cast<char*>(h->q[h->enq & 1]);
+  const long long rs = h->L.rstride * (long long)h->esz;
+  if (slo) *slo = b + 2 * rs;
+  if (shi) *shi = b + (long long)h->L.ny * rs;
+  if (rlo) *rlo = b;
+  if (rhi) *rhi = b + (long long)(h->L.ny + 2) * rs;
+  if (bytes) *bytes = (uint64_t)(2 * rs);
+  return WS_OK;
+}
+
+int ws_state_ptr(ws_handle* h, void** q, int64_t* pitch, int64_t* row) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (q) *q = h->q[h->enq & 1];
+  if (pitch) *pitch = h->L.pitch;
+  if (row) *row = h->L.rstride;
+  return WS_OK;
+}
+
+int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
+  if (!h || !c) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (!h->uploaded) return fail(h, WS_ERR_CONFIG, "no state uploaded");
+  if (nsteps < 0) return fail(h, WS_ERR_CONFIG, "nsteps must be >= 0");
+  int rc = check_ctl(h, c);
+  if (rc) return rc;
+  cudaStream_t st = pick(h, s);
+  WS_CUDA(h, cudaMemsetAsync(&h->ds->finished, 0, sizeof(int), st));
+  long long left = nsteps;
+  if (left > 0 && (h->enq & 1)) { enqueue_step(h, c, 1, st); h->enq++; left--; }
+  if (left >= 4 && st != nullptr) {
+    // two-step graph (parity 0 then 1), cached per (ctl, stream)
+    if (!h->gexec || std::memcmp(&h->gctl, c, sizeof(ws_ctl)) != 0 || h->gstream != st) {
+      if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+      cudaGraph_t g;
+      long long l0 = h->launches;
+      WS_CUDA(h, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      enqueue_step(h, c, 0, st);
+      enqueue_step(h, c, 1, st);
+      WS_CUDA(h, cudaStreamEndCapture(st, &g));
+      h->launches = l0;
+      WS_CUDA(h, cudaGraphInstantiate(&h->gexec, g, 0));
+      cudaGraphDestroy(g);
+      h->gctl = *c;
+      h->gstream = st;
+    }
+    const int per_pair = (h->ops.static_speeds && !h->multi) ? 2 : 4;
+    while (left >= 2) {
+      WS_CUDA(h, cudaGraphLaunch(h->gexec, st));
+      h->launches += per_pair;
+      h->enq += 2;
+      left -= 2;
+    }
+  }
+  while (left > 0) { enqueue_step(h, c, (int)(h->enq & 1), st); h->enq++; left--; }
+  WS_CUDA(h, cudaGetLastError());
+  return WS_OK;
+}
+
+int ws_poll(ws_handle* h, int64_t* steps_done, ws_report* reports, int32_t max_reports,
+            int32_t* n_reports, double* t_now, ws_error_info* err) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  cudaStream_t st = h->last_stream ? h->last_stream : h->stream;
+  HostState hs;
+  int rc = read_state(h, &hs, st);
+  if (rc) return rc;
+  if ((rc = resync(h, hs, st))) return rc;
+  WS_CUDA(h, cudaStreamSynchronize(st));
+  if (steps_done) *steps_done = hs.steps;
+  if (t_now) *t_now = hs.t;
+  long long avail = hs.nrep - h->nrep_seen;
+  if (avail > REPCAP) avail = REPCAP;
+  long long want = avail < max_reports ? avail : max_reports;
+  if (n_reports) *n_reports = (int32_t)want;
+  if (reports && want > 0) {
+    std::vector<Report> tmp((size_t)want);
+    long long first = hs.nrep - want;
+    long long k = 0;
+    while (k < want) {
+      long long idx = (first + k) % REPCAP;
+      long long n = want - k;
+      if (idx + n > REPCAP) n = REPCAP - idx;
+      WS_CUDA(h, cudaMemcpy(&tmp[(size_t)k], &h->ds->rep[idx], sizeof(Report) * n,
+                            cudaMemcpyDeviceToHost));
+      k += n;
+    }
+    for (long long m = 0; m < want; ++m) {
+      reports[m].dt = tmp[m].dt; reports[m].cfl = tmp[m].cfl;
+      reports[m].max_speed_x = tmp[m].msx; reports[m].max_speed_y = tmp[m].msy;
+    }
+  }
+  h->nrep_seen = hs.nrep;
+  if (err) {
+    std::memset(err, 0, sizeof *err);
+    err->code = hs.err;
+    err->step = hs.err_step;
+    if (hs.err == ERR_KERNEL) {
+      unsigned long long k = hs.err_key;
+      err->direction = (int)(k >> 63);
+      err->stage = (int)((k >> 41) & 0xf);
+      err->component = (int)((k >> 38) & 0x7);
+      err->i = (int)((k >> 19) & 0x7ffff);
+      err->j = (int)(k & 0x7ffff);
+    }
+  }
+  return hs.err ? hs.err : WS_OK;
+}
+
+int ws_sync(ws_handle* h) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  cudaStream_t st = h->last_stream ? h->last_stream : h->stream;
+  WS_CUDA(h, cudaStreamSynchronize(st));
+  return WS_OK;
+}
+
+int64_t ws_launch_count(const ws_handle* h) { return h ? h->launches : 0; }
+
+}  // extern "C"
+
+namespace {
+
+template <class S>
+int riemann_t(const typename S::template Params<double>& P, int dir, long long n,
+              const double* ql, const double* qr, const double* al, const double* ar,
+              double* waves, double* speeds, double* amdq, double* apdq, int* codes) {
+  constexpr int NEQ = S::NEQ, NW = S::NW, NAUX = S::NAUX;
+  if (NAUX > 0 && (!al || !ar)) return fail(nullptr, WS_ERR_CONFIG, "this solver needs aux data");
+  const size_t b = sizeof(double) * (size_t)n;
+  double *dql, *dqr, *dal = nullptr, *dar = nullptr, *dw, *ds, *dm, *dp;
+  int* dc;
+  cudaError_t e;
+  std::vector<void*> bufs;
+  auto alloc = [&](void** p, size_t bytes) {
+    e = cudaMalloc(p, bytes > 0 ? bytes : 8);
+    if (e == cudaSuccess) bufs.push_back(*p);
+    return e == cudaSuccess;
+  };
+  auto cleanup = [&]() { for (void* p : bufs) cudaFree(p); };
+  bool ok = alloc((void**)&dql, b * NEQ) && alloc((void**)&dqr, b * NEQ) &&
+            alloc((void**)&dw, b * NW * NEQ) && alloc((void**)&ds, b * NW) &&
+            alloc((void**)&dm, b * NEQ) && alloc((void**)&dp, b * NEQ) &&
+            alloc((void**)&dc, sizeof(int) * (size_t)(n > 0 ? n : 1));
+  if (ok && NAUX > 0) ok = alloc((void**)&dal, b * NAUX) && alloc((void**)&dar, b * NAUX);
+  if (!ok) { cleanup(); return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e)); }
+  cudaMemcpy(dql, ql, b * NEQ, cudaMemcpyHostToDevice);
+  cudaMemcpy(dqr, qr, b * NEQ, cudaMemcpyHostToDevice);
+  if (NAUX > 0) {
+    cudaMemcpy(dal, al, b * NAUX, cudaMemcpyHostToDevice);
+    cudaMemcpy(dar, ar, b * NAUX, cudaMemcpyHostToDevice);
+  }
+  if (n > 0) {
+    const int blocks = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+    if (dir == 0)
+      k_riemann<S, double, 1><<<blocks, 256>>>(P, n, dql, dqr, dal, dar, dw, ds, dm, dp, dc);
+    else
+      k_riemann<S, double, 2><<<blocks, 256>>>(P, n, dql, dqr, dal, dar, dw, ds, dm, dp, dc);
+  }
+  e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(waves, dw, b * NW * NEQ, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(speeds, ds, b * NW, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(amdq, dm, b * NEQ, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(apdq, dp, b * NEQ, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(codes, dc, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e != cudaSuccess) return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+  return WS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ws_riemann(int32_t solver, const double* p, int32_t direction, int64_t n, const double* ql,
+               const double* qr, const double* al, const double* ar, double* waves,
+               double* speeds, double* amdq, double* apdq, int32_t* codes, int32_t device) {
+  if (n < 0 || !ql || !qr || !waves || !speeds || !amdq || !apdq || !codes || !p)
+    return fail(nullptr, WS_ERR_CONFIG, "bad argument");
+  if (direction != 0 && direction != 1) return fail(nullptr, WS_ERR_CONFIG, "direction must be 0 or 1");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+  switch (solver) {
+    case WS_ACOUSTICS_CONST: {
+      if (!(p[0] > 0 && p[1] > 0))
+        return fail(nullptr, WS_ERR_CONFIG, "density and bulk modulus must be positive");
+      double c = std::sqrt(p[1] / p[0]), z = p[0] * c;
+      AcousticsConst::Params<double> P{z, 2.0 * z, c};
+      return riemann_t<AcousticsConst>(P, direction, n, ql, qr, al, ar, waves, speeds, amdq,
+                                       apdq, codes);
+    }
+    case WS_ACOUSTICS_VAR: {
+      AcousticsVar::Params<double> P{0.0};
+      return riemann_t<AcousticsVar>(P, direction, n, ql, qr, al, ar, waves, speeds, amdq,
+                                     apdq, codes);
+    }
+    case WS_EULER_ROE: {
+      if (!(p[0] > 1.0)) return fail(nullptr, WS_ERR_CONFIG, "gamma must exceed 1");
+      EulerRoe::Params<double> P{p[0] - 1.0};
+      return riemann_t<EulerRoe>(P, direction, n, ql, qr, al, ar, waves, speeds, amdq, apdq,
+                                 codes);
+    }
+    case WS_EULER_HLLE: {
+      if (!(p[0] > 1.0)) return fail(nullptr, WS_ERR_CONFIG, "gamma must exceed 1");
+      EulerHLLE::Params<double> P{p[0] - 1.0, p[0]};
+      return riemann_t<EulerHLLE>(P, direction, n, ql, qr, al, ar, waves, speeds, amdq, apdq,
+                                  codes);
+    }
+    case WS_SHALLOW_ROE: {
+      if (!(p[0] > 0)) return fail(nullptr, WS_ERR_CONFIG, "gravity must be positive");
+      ShallowRoe::Params<double> P{p[0], std::sqrt(p[0])};
+      return riemann_t<ShallowRoe>(P, direction, n, ql, qr, al, ar, waves, speeds, amdq, apdq,
+                                   codes);
+    }
+  }
+  return fail(nullptr, WS_ERR_CONFIG, "unknown solver id");
+}
+
+int ws_fill_ghost(double* data, int32_t ncomp, int32_t nx, int32_t ny, int32_t bcx, int32_t bcy,
+                  int32_t device) {
+  if (!data || ncomp < 0 || nx < 1 || ny < 1) return fail(nullptr, WS_ERR_CONFIG, "bad argument");
+  if (ncomp == 0) return WS_OK;
+  char b[128];
+  if (bcx == WS_BC_PERIODIC && nx < 2) {
+    snprintf(b, sizeof b, "periodic boundary needs at least num_ghost=2 interior cells, got %d", nx);
+    return fail(nullptr, WS_ERR_CONFIG, b);
+  }
+  if (bcy == WS_BC_PERIODIC && ny < 2) {
+    snprintf(b, sizeof b, "periodic boundary needs at least num_ghost=2 interior cells, got %d", ny);
+    return fail(nullptr, WS_ERR_CONFIG, b);
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+  const size_t bytes = sizeof(double) * (size_t)ncomp * (nx + 4) * (ny + 4);
+  double* d = nullptr;
+  if ((e = cudaMalloc(&d, bytes)) != cudaSuccess) return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+  e = cudaMemcpy(d, data, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_fill_ghost<<<148 * 4, 256>>>(d, ncomp, nx, ny, bcx, bcy);
+    e = cudaMemcpy(data, d, bytes, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+  return WS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,170 @@
+// ws_common.cuh — device layout, boundary index mapping and step control
+// shared by every kernel of the B200 wave-propagation step.
+//
+// Device storage: one buffer per state, rows j in [-2, ny+2)
+// of the shard, each row holding the num_eqn component rows of `pitch`
+// elements (x fastest).  Address of (component c, cell i, row j):
+//     base + (j + 2) * rstride + c * pitch + i,   rstride = num_eqn * pitch.
+// Only the interior columns are stored; x ghost cells and physical-boundary
+// y ghost rows are produced by index mapping on load, which is exactly the
+// reference fill_ghost (grid.py:156-193: extrapolate copies the nearest
+// interior cell, periodic wraps).  The two ghost rows per side exist in
+// memory for the row-strip halo exchange.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ws {
+
+enum : int { BC_PERIODIC = 0, BC_EXTRAPOLATE = 1 };
+enum : int { ROWS_MEMORY = 0, ROWS_BC = 1 };
+enum : int { LIM_NONE = 0, LIM_MINMOD = 1, LIM_SUPERBEE = 2, LIM_MC = 3 };
+
+constexpr int REPCAP = 4096;          // device report ring (steps between polls)
+constexpr int ERR_KERNEL = 1;
+constexpr int ERR_STATIONARY = 4;
+
+struct Layout {
+  int nx, ny;             // local interior
+  int ny_edges_y;         // y-edge rows this shard reports (ny, +1 on the top shard)
+  int bcx, bcy;           // BC_*
+  int lo, hi;             // ROWS_* for the bottom / top ghost rows
+  int j_off;              // global index of local row 0
+  int nx_glob;            // == nx (x is never split)
+  long long pitch;        // elements per component row
+  long long rstride;      // elements per grid row of q   (num_eqn * pitch)
+  long long astride;      // elements per grid row of aux (num_aux * pitch)
+};
+
+struct Report { double dt, cfl, msx, msy; };
+
+// Device-resident step state.  slot[k&1] = {max|s| x bits, max|s| y bits,
+// ~first-error-key}: reduced with MAX (so the smallest key wins), which is
+// also what a multi-shard all-reduce of the 3 x u64 does.
+struct DevState {
+  unsigned long long slot[2][3];
+  unsigned long long static_bits[2];  // acoustics: precomputed max speeds
+  int err;                            // sticky status (ERR_*), 0 = fine
+  int done;                           // last-block counter of the update kernel
+  long long steps;                    // committed steps since upload
+  long long err_step;
+  unsigned long long err_key;
+  double t;                           // simulated time since upload
+  int finished;                       // t_final reached
+  int pad_;
+  long long nrep;                     // reports written (ring index)
+  Report rep[REPCAP];
+};
+
+struct StepArgs {
+  double dx, dy;
+  double cfl, dt_max, fixed_dt, remaining, t_final, tol;
+  int has_dt_max, has_fixed, has_remaining, has_t_final;
+  int cur;              // slot parity of this step
+  int static_speeds;    // 1: max speeds come from DevState::static_bits
+};
+
+__device__ __forceinline__ int map_i(int i, const Layout& L) {
+  if (i < 0) i = (L.bcx == BC_PERIODIC) ? i + L.nx : 0;
+  else if (i >= L.nx) i = (L.bcx == BC_PERIODIC) ? i - L.nx : L.nx - 1;
+  // cells past the periodic image only feed discarded (out-of-domain) cells
+  return i < 0 ? 0 : (i >= L.nx ? L.nx - 1 : i);
+}
+
+__device__ __forceinline__ int map_j(int j, const Layout& L) {
+  if (j < 0) {
+    if (L.lo == ROWS_MEMORY) return j < -2 ? -2 : j;
+    j = (L.bcy == BC_PERIODIC) ? j + L.ny : 0;
+  } else if (j >= L.ny) {
+    if (L.hi == ROWS_MEMORY) return j > L.ny + 1 ? L.ny + 1 : j;
+    j = (L.bcy == BC_PERIODIC) ? j - L.ny : L.ny - 1;
+  }
+  return j < 0 ? 0 : (j >= L.ny ? L.ny - 1 : j);
+}
+
+__device__ __forceinline__ long long row_off(int j, const Layout& L) {
+  return (long long)(j + 2) * L.rstride;
+}
+
+// Error key: ordering of reference CellWise/Serial sweeps (sweep.py:203-218):
+// all x chunks, then y; chunk = MAX_BLOCK // width rows (sweep.py:117-119);
+// inside a chunk the kernel's admissibility stage, then the first bad element
+// in C order over (component, i, j) (kernels.py:325-328).
+__device__ __forceinline__ unsigned long long err_key(int dir, int i, int jg, int stage,
+                                                      int comp, int nx) {
+  int width = dir == 0 ? nx + 1 : nx;
+  int rows_per = 32768 / width;
+  if (rows_per < 1) rows_per = 1;
+  unsigned long long chunk = (unsigned long long)(jg / rows_per);
+  return ((unsigned long long)dir << 63) | (chunk << 45) |
+         ((unsigned long long)stage << 41) | ((unsigned long long)comp << 38) |
+         ((unsigned long long)i << 19) | (unsigned long long)jg;
+}
+
+template <class R> struct Bits;
+template <> struct Bits<double> {
+  static __device__ __forceinline__ unsigned long long to(double v) {
+    return (unsigned long long)__double_as_longlong(v);
+  }
+  static __device__ __forceinline__ double from(unsigned long long b) {
+    return __longlong_as_double((long long)b);
+  }
+};
+template <> struct Bits<float> {
+  static __device__ __forceinline__ unsigned long long to(float v) {
+    return (unsigned long long)__float_as_uint(v);
+  }
+  static __device__ __forceinline__ float from(unsigned long long b) {
+    return __uint_as_float((unsigned)b);
+  }
+};
+
+// numpy.minimum / maximum for non-NaN operands
+template <class R> __device__ __forceinline__ R nmin(R a, R b) { return (a <= b) ? a : b; }
+template <class R> __device__ __forceinline__ R nmax(R a, R b) { return (a >= b) ? a : b; }
+
+// Step control computed identically by every CTA: dt from this step's max
+// speeds exactly as reference choose_dt (driver.py:314-337), all in fp64.
+struct Ctl {
+  double dt, msx, msy;
+  int skip;        // 1: do nothing (sticky error, pending error, or t_final reached)
+  int stationary;  // rate == 0 without fixed_dt
+  int finished;
+};
+
+template <class R>
+__device__ __forceinline__ Ctl step_control(const StepArgs& A, const DevState* ds,
+                                            bool pending_error_blocks) {
+  Ctl c;
+  c.skip = 0; c.stationary = 0; c.finished = 0; c.dt = 0.0;
+  volatile const DevState* vds = ds;
+  if (vds->err) { c.skip = 1; c.msx = c.msy = 0.0; return c; }
+  unsigned long long bx, by;
+  if (A.static_speeds) { bx = vds->static_bits[0]; by = vds->static_bits[1]; }
+  else { bx = vds->slot[A.cur][0]; by = vds->slot[A.cur][1]; }
+  c.msx = (double)Bits<R>::from(bx);
+  c.msy = (double)Bits<R>::from(by);
+  if (pending_error_blocks && vds->slot[A.cur][2] != 0ull) c.skip = 1;
+  double remaining = A.remaining;
+  int has_rem = A.has_remaining;
+  if (A.has_t_final) {
+    double t = vds->t;
+    if (!(A.t_final - t > A.tol)) { c.skip = 1; c.finished = 1; return c; }
+    remaining = A.t_final - t;
+    has_rem = 1;
+  }
+  double dt;
+  if (A.has_fixed) {
+    dt = A.fixed_dt;
+  } else {
+    double rate = c.msx / A.dx + c.msy / A.dy;
+    if (rate == 0.0) { c.stationary = 1; c.skip = 1; return c; }
+    dt = A.cfl / rate;
+  }
+  if (A.has_dt_max) dt = (A.dt_max < dt) ? A.dt_max : dt;   // Python min(dt, dt_max)
+  if (has_rem) dt = (remaining < dt) ? remaining : dt;
+  c.dt = dt;
+  return c;
+}
+
+}  // namespace ws

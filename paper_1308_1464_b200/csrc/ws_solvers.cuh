@@ -1,0 +1,369 @@
+// ws_solvers.cuh — pointwise Riemann solvers as parallelism-unaware device
+// plugins (the paper's decoupling goal; reference plugin
+// contract kernels.py:567-586).
+//
+// A solver is a struct with
+//   NEQ, NW, NAUX, NPR           components, waves, aux fields, per-cell primitives
+//   STATIC_SPEEDS                speeds independent of q (acoustics)
+//   Params<R>                    bound parameters (reference make_kernel, kernels.py:589-633)
+//   prims(q, aux, P, pr)         per-cell quantities shared by the 4 edges of a cell
+//   solve<NI>(ql,qr,pl,pr,al,ar,P,W,s,amdq,apdq)   one edge, NI = normal slot (1=x, 2=y)
+//   probe<NI>(...,smax) -> code  admissibility tests in the reference order and
+//                                the edge's max |s| (for the CFL reduction)
+// Every expression keeps the association of the numpy oracle
+// (oracle/wavestep_oracle.py) and of the reference for the solvers it has;
+// the translation unit is compiled with --fmad=false, IEEE div/sqrt, so
+// fp64 results are bitwise identical to numpy.
+#pragma once
+#include "ws_common.cuh"
+
+namespace ws {
+
+constexpr double FLOOR = 1e-300;  // reference kernels.py:227
+
+// code = (stage + 1) | (component << 8); 0 = admissible
+template <class R, int N>
+__device__ __forceinline__ int finite_code(const R* ql, const R* qr) {
+#pragma unroll
+  for (int m = 0; m < N; ++m)
+    if (!isfinite(ql[m])) return 1 | (m << 8);
+#pragma unroll
+  for (int m = 0; m < N; ++m)
+    if (!isfinite(qr[m])) return 2 | (m << 8);
+  return 0;
+}
+
+// float32: every positive float exceeds 1e-300, so the floor is 0 (numpy's
+// float32 comparison against 1e-300 behaves the same way)
+template <class R> __device__ __forceinline__ R floor_v() { return (R)0; }
+template <> __device__ __forceinline__ double floor_v<double>() { return FLOOR; }
+template <class R> __device__ __forceinline__ bool bad_pos(R v) { return !(v > floor_v<R>()); }
+
+// ---------------------------------------------------------------------------
+// constant-coefficient acoustics — reference kernels.py:374-406
+struct AcousticsConst {
+  static constexpr int NEQ = 3, NW = 2, NAUX = 0, NPR = 0;
+  static constexpr bool STATIC_SPEEDS = true;
+  template <class R> struct Params { R z, twoz, c; };
+
+  template <class R, class P>
+  __device__ static __forceinline__ void prims(const R*, const R*, const P&, R*) {}
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R*, const R*,
+                                               const R*, const R*, const P& p, R (&W)[NW][NEQ],
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+    constexpr int TI = 3 - NI;
+    R dp = qr[0] - ql[0];
+    R dn = qr[NI] - ql[NI];
+    R a1 = (-dp + p.z * dn) / p.twoz;
+    R a2 = (dp + p.z * dn) / p.twoz;
+    W[0][0] = (-p.z) * a1; W[0][NI] = a1; W[0][TI] = (R)0;
+    W[1][0] = p.z * a2;    W[1][NI] = a2; W[1][TI] = (R)0;
+    s[0] = -p.c; s[1] = p.c;
+#pragma unroll
+    for (int m = 0; m < NEQ; ++m) { am[m] = (-p.c) * W[0][m]; ap[m] = p.c * W[1][m]; }
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R*, const R*,
+                                              const R*, const R*, const P& p, R& smax) {
+    smax = p.c;
+    return finite_code<R, NEQ>(ql, qr);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// variable-coefficient acoustics, aux = (rho, c) — reference kernels.py:409-454
+struct AcousticsVar {
+  static constexpr int NEQ = 3, NW = 2, NAUX = 2, NPR = 1;  // pr[0] = Z = rho*c
+  static constexpr bool STATIC_SPEEDS = true;
+  template <class R> struct Params { R unused; };
+
+  template <class R, class P>
+  __device__ static __forceinline__ void prims(const R*, const R* a, const P&, R* pr) {
+    pr[0] = a[0] * a[1];
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R* pl, const R* pr,
+                                               const R* al, const R* ar, const P&, R (&W)[NW][NEQ],
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+    constexpr int TI = 3 - NI;
+    R zl = pl[0], zr = pr[0];
+    R cl = al[1], cr = ar[1];
+    R dp = qr[0] - ql[0];
+    R dn = qr[NI] - ql[NI];
+    R den = zl + zr;
+    R a1 = (-dp + zr * dn) / den;
+    R a2 = (dp + zl * dn) / den;
+    W[0][0] = (-zl) * a1; W[0][NI] = a1; W[0][TI] = (R)0;
+    W[1][0] = zr * a2;    W[1][NI] = a2; W[1][TI] = (R)0;
+    s[0] = -cl; s[1] = cr;
+#pragma unroll
+    for (int m = 0; m < NEQ; ++m) { am[m] = (-cl) * W[0][m]; ap[m] = cr * W[1][m]; }
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R*, const R*,
+                                              const R* al, const R* ar, const P&, R& smax) {
+    smax = nmax(al[1], ar[1]);
+    int c = finite_code<R, NEQ>(ql, qr);
+    if (c) return c;
+    // kernels.py:428-430: per side density then sound speed, left first
+    if (bad_pos(al[0])) return 3;
+    if (bad_pos(al[1])) return 4;
+    if (bad_pos(ar[0])) return 5;
+    if (bad_pos(ar[1])) return 6;
+    return 0;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// ideal gas, shared per-cell primitives (reference kernels.py:475-478, 482, 487)
+//   pr = {u = q1/rho, v = q2/rho, p, sqrt(rho), sqrt(rho)*(E+p)/rho [, c]}
+// p uses (u*u + v*v); the y sweep's (v*v + u*u) is the same IEEE sum.
+template <class R, class P>
+__device__ __forceinline__ void gas_prims(const R* q, const P& p, R* pr) {
+  R rho = q[0];
+  R u = q[1] / rho;
+  R v = q[2] / rho;
+  R pp = p.gm1 * (q[3] - (R)0.5 * rho * (u * u + v * v));
+  R sq = sqrt(rho);
+  pr[0] = u; pr[1] = v; pr[2] = pp; pr[3] = sq; pr[4] = sq * (q[3] + pp) / rho;
+}
+
+// Euler, Roe linearisation, no entropy fix — reference kernels.py:457-533
+struct EulerRoe {
+  static constexpr int NEQ = 4, NW = 3, NAUX = 0, NPR = 5;
+  static constexpr bool STATIC_SPEEDS = false;
+  template <class R> struct Params { R gm1; };
+
+  template <class R, class P>
+  __device__ static __forceinline__ void prims(const R* q, const R*, const P& p, R* pr) {
+    gas_prims(q, p, pr);
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void roe(const R* pl, const R* pr, const P& p, R& uh, R& vh,
+                                             R& hh, R& kin, R& c2) {
+    constexpr int UN = NI - 1, UT = 2 - NI;
+    R ws = pl[3] + pr[3];
+    uh = (pl[3] * pl[UN] + pr[3] * pr[UN]) / ws;
+    vh = (pl[3] * pl[UT] + pr[3] * pr[UT]) / ws;
+    hh = (pl[4] + pr[4]) / ws;
+    kin = (R)0.5 * (uh * uh + vh * vh);
+    c2 = p.gm1 * (hh - kin);
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R* pl, const R* pr,
+                                               const R*, const R*, const P& p, R (&W)[NW][NEQ],
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+    constexpr int TI = 3 - NI;
+    R uh, vh, hh, kin, c2;
+    roe<NI>(pl, pr, p, uh, vh, hh, kin, c2);
+    R ch = sqrt(c2);
+    R d0 = qr[0] - ql[0];
+    R dm = qr[NI] - ql[NI];
+    R dt = qr[TI] - ql[TI];
+    R de = qr[3] - ql[3];
+    R ash = dt - vh * d0;
+    R amid = p.gm1 / c2 * ((hh - uh * uh) * d0 + uh * dm - (de - ash * vh));
+    R span = (dm - uh * d0) / ch;
+    R apl = (R)0.5 * (span + d0 - amid);
+    R ami = d0 - amid - apl;
+    W[0][0] = ami;  W[0][NI] = ami * (uh - ch);  W[0][TI] = ami * vh;       W[0][3] = ami * (hh - uh * ch);
+    W[1][0] = amid; W[1][NI] = amid * uh;        W[1][TI] = amid * vh + ash; W[1][3] = amid * kin + ash * vh;
+    W[2][0] = apl;  W[2][NI] = apl * (uh + ch);  W[2][TI] = apl * vh;       W[2][3] = apl * (hh + uh * ch);
+    s[0] = uh - ch; s[1] = uh; s[2] = uh + ch;
+    R n0 = nmin(s[0], (R)0), n1 = nmin(s[1], (R)0), n2 = nmin(s[2], (R)0);
+    R p0 = nmax(s[0], (R)0), p1 = nmax(s[1], (R)0), p2 = nmax(s[2], (R)0);
+#pragma unroll
+    for (int m = 0; m < NEQ; ++m) {
+      am[m] = n0 * W[0][m] + n1 * W[1][m] + n2 * W[2][m];
+      ap[m] = p0 * W[0][m] + p1 * W[1][m] + p2 * W[2][m];
+    }
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R* pl, const R* pr,
+                                              const R*, const R*, const P& p, R& smax) {
+    int c = finite_code<R, NEQ>(ql, qr);
+    if (c) { smax = (R)0; return c; }
+    if (bad_pos(ql[0])) { smax = (R)0; return 3; }
+    if (bad_pos(qr[0])) { smax = (R)0; return 4; }
+    if (bad_pos(pl[2])) { smax = (R)0; return 5; }
+    if (bad_pos(pr[2])) { smax = (R)0; return 6; }
+    R uh, vh, hh, kin, c2;
+    roe<NI>(pl, pr, p, uh, vh, hh, kin, c2);
+    if (!(c2 > (R)0)) { smax = (R)0; return 7; }
+    R ch = sqrt(c2);
+    smax = nmax(nmax(fabs(uh - ch), fabs(uh)), fabs(uh + ch));
+    return 0;
+  }
+};
+
+// Euler HLLE (builder-owned formula; oracle rp_euler_hlle)
+struct EulerHLLE {
+  static constexpr int NEQ = 4, NW = 2, NAUX = 0, NPR = 6;  // gas prims + c
+  static constexpr bool STATIC_SPEEDS = false;
+  template <class R> struct Params { R gm1, gam; };
+
+  template <class R, class P>
+  __device__ static __forceinline__ void prims(const R* q, const R*, const P& p, R* pr) {
+    gas_prims(q, p, pr);
+    pr[5] = sqrt(p.gam * pr[2] / q[0]);
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void roe(const R* pl, const R* pr, const P& p, R& uh, R& vh,
+                                             R& c2) {
+    constexpr int UN = NI - 1, UT = 2 - NI;
+    R iws = (R)1 / (pl[3] + pr[3]);
+    uh = (pl[3] * pl[UN] + pr[3] * pr[UN]) * iws;
+    vh = (pl[3] * pl[UT] + pr[3] * pr[UT]) * iws;
+    R hh = (pl[4] + pr[4]) * iws;
+    c2 = p.gm1 * (hh - (R)0.5 * (uh * uh + vh * vh));
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void speeds(const R* pl, const R* pr, const P& p, R& s1,
+                                                R& s2, R& c2) {
+    constexpr int UN = NI - 1;
+    R uh, vh;
+    roe<NI>(pl, pr, p, uh, vh, c2);
+    R ch = sqrt(c2);
+    s1 = nmin(pl[UN] - pl[5], uh - ch);
+    s2 = nmax(pr[UN] + pr[5], uh + ch);
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R* pl, const R* pr,
+                                               const R*, const R*, const P& p, R (&W)[NW][NEQ],
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+    constexpr int TI = 3 - NI, UN = NI - 1;
+    R s1, s2, c2;
+    speeds<NI>(pl, pr, p, s1, s2, c2);
+    R ul = pl[UN], ur = pr[UN];
+    R fl[NEQ], fr[NEQ];
+    fl[0] = ql[NI]; fl[NI] = ql[NI] * ul + pl[2]; fl[TI] = ql[TI] * ul; fl[3] = ul * (ql[3] + pl[2]);
+    fr[0] = qr[NI]; fr[NI] = qr[NI] * ur + pr[2]; fr[TI] = qr[TI] * ur; fr[3] = ur * (qr[3] + pr[2]);
+    R inv = (R)1 / (s1 - s2);
+    R n0 = nmin(s1, (R)0), n1 = nmin(s2, (R)0);
+    R p0 = nmax(s1, (R)0), p1 = nmax(s2, (R)0);
+#pragma unroll
+    for (int m = 0; m < NEQ; ++m) {
+      R qm = (fr[m] - fl[m] - s2 * qr[m] + s1 * ql[m]) * inv;
+      W[0][m] = qm - ql[m];
+      W[1][m] = qr[m] - qm;
+      am[m] = n0 * W[0][m] + n1 * W[1][m];
+      ap[m] = p0 * W[0][m] + p1 * W[1][m];
+    }
+    s[0] = s1; s[1] = s2;
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R* pl, const R* pr,
+                                              const R*, const R*, const P& p, R& smax) {
+    int c = finite_code<R, NEQ>(ql, qr);
+    if (c) { smax = (R)0; return c; }
+    if (bad_pos(ql[0])) { smax = (R)0; return 3; }
+    if (bad_pos(qr[0])) { smax = (R)0; return 4; }
+    if (bad_pos(pl[2])) { smax = (R)0; return 5; }
+    if (bad_pos(pr[2])) { smax = (R)0; return 6; }
+    R s1, s2, c2;
+    speeds<NI>(pl, pr, p, s1, s2, c2);
+    if (!(c2 > (R)0)) { smax = (R)0; return 7; }
+    smax = nmax(fabs(s1), fabs(s2));
+    return 0;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// shallow water, Roe + Harten entropy fix (builder-owned; oracle rp_shallow_roe)
+//   prims: {u = hu*(1/h), v = hv*(1/h), sqrt(h)}
+struct ShallowRoe {
+  static constexpr int NEQ = 3, NW = 3, NAUX = 0, NPR = 3;
+  static constexpr bool STATIC_SPEEDS = false;
+  template <class R> struct Params { R grav, sqg; };
+
+  template <class R, class P>
+  __device__ static __forceinline__ void prims(const R* q, const R*, const P&, R* pr) {
+    R rh = (R)1 / q[0];
+    pr[0] = q[1] * rh;
+    pr[1] = q[2] * rh;
+    pr[2] = sqrt(q[0]);
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void roe(const R* ql, const R* qr, const R* pl, const R* pr,
+                                             const P& p, R& uh, R& vh, R& ch) {
+    constexpr int UN = NI - 1, UT = 2 - NI;
+    R iws = (R)1 / (pl[2] + pr[2]);
+    uh = (pl[2] * pl[UN] + pr[2] * pr[UN]) * iws;
+    vh = (pl[2] * pl[UT] + pr[2] * pr[UT]) * iws;
+    ch = sqrt(p.grav * ((R)0.5 * (ql[0] + qr[0])));
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R* pl, const R* pr,
+                                               const R*, const R*, const P& p, R (&W)[NW][NEQ],
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+    constexpr int TI = 3 - NI, UN = NI - 1;
+    R uh, vh, ch;
+    roe<NI>(ql, qr, pl, pr, p, uh, vh, ch);
+    R d0 = qr[0] - ql[0];
+    R d1 = qr[NI] - ql[NI];
+    R d2 = qr[TI] - ql[TI];
+    R i2c = (R)0.5 / ch;
+    R s1 = uh - ch, s3 = uh + ch;
+    R a1 = (s3 * d0 - d1) * i2c;
+    R a2 = d2 - vh * d0;
+    R a3 = (d1 - s1 * d0) * i2c;
+    W[0][0] = a1;   W[0][NI] = a1 * s1;  W[0][TI] = a1 * vh;
+    W[1][0] = (R)0; W[1][NI] = (R)0;     W[1][TI] = a2;
+    W[2][0] = a3;   W[2][NI] = a3 * s3;  W[2][TI] = a3 * vh;
+    s[0] = s1; s[1] = uh; s[2] = s3;
+    // Harten entropy fix on families 1 and 3 (LeVeque 2002 §15.3.5)
+    R cl = p.sqg * pl[2], cr = p.sqg * pr[2];
+    R ul = pl[UN], ur = pr[UN];
+    R del1 = nmax((R)0, (ur - cr) - (ul - cl));
+    R del3 = nmax((R)0, (ur + cr) - (ul + cl));
+    R f1 = fabs(s1), f2 = fabs(uh), f3 = fabs(s3);
+    if (f1 < del1) f1 = (s1 * s1 + del1 * del1) / ((R)2 * del1);
+    if (f3 < del3) f3 = (s3 * s3 + del3 * del3) / ((R)2 * del3);
+    R am1 = (R)0.5 * (s1 - f1), am2 = (R)0.5 * (uh - f2), am3 = (R)0.5 * (s3 - f3);
+    R ap1 = (R)0.5 * (s1 + f1), ap2 = (R)0.5 * (uh + f2), ap3 = (R)0.5 * (s3 + f3);
+    am[0] = am1 * W[0][0] + am3 * W[2][0];
+    am[NI] = am1 * W[0][NI] + am3 * W[2][NI];
+    am[TI] = am1 * W[0][TI] + am2 * a2 + am3 * W[2][TI];
+    ap[0] = ap1 * W[0][0] + ap3 * W[2][0];
+    ap[NI] = ap1 * W[0][NI] + ap3 * W[2][NI];
+    ap[TI] = ap1 * W[0][TI] + ap2 * a2 + ap3 * W[2][TI];
+  }
+
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R* pl, const R* pr,
+                                              const R*, const R*, const P& p, R& smax) {
+    int c = finite_code<R, NEQ>(ql, qr);
+    if (c) { smax = (R)0; return c; }
+    if (bad_pos(ql[0])) { smax = (R)0; return 3; }
+    if (bad_pos(qr[0])) { smax = (R)0; return 4; }
+    R uh, vh, ch;
+    roe<NI>(ql, qr, pl, pr, p, uh, vh, ch);
+    smax = nmax(nmax(fabs(uh - ch), fabs(uh)), fabs(uh + ch));
+    return 0;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// wave limiters (oracle phi(); LeVeque 2002 §6.9)
+template <int LIM, class R> __device__ __forceinline__ R limiter_phi(R th) {
+  if (LIM == LIM_MINMOD) return nmax((R)0, nmin((R)1, th));
+  if (LIM == LIM_SUPERBEE) return nmax((R)0, nmax(nmin((R)1, (R)2 * th), nmin((R)2, th)));
+  if (LIM == LIM_MC) return nmax((R)0, nmin(nmin((R)0.5 * ((R)1 + th), (R)2), (R)2 * th));
+  return (R)1;
+}
+
+}  // namespace ws

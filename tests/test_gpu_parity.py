@@ -1,0 +1,176 @@
+"""GPU parity: the CUDA step against the numpy oracle, through the C ABI.
+
+Bar (north_star): fp64 results identical to the oracle — bitwise, checked
+with np.array_equal like the reference's own guard (bench.py:181) — and
+every dt identical.  Sizes are deliberately not multiples of the 32x16
+CUDA tile so partial tiles and the boundary index mapping are exercised.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import PARAMS, device_run, oracle_run, random_state, same_bits
+from oracle import wavestep_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SOLVERS = ["acoustics-const", "acoustics-var", "euler", "euler-hlle", "shallow-water-roe"]
+BCS = [("extrapolate", "extrapolate"), ("periodic", "periodic"), ("periodic", "extrapolate")]
+
+
+def _compare(name, nx, ny, steps, order, limiter, bc, seed=0, use_run=False, cfl=0.9):
+    dx, dy = 1.0 / nx, 1.3 / ny
+    q, aux = random_state(name, nx, ny, seed)
+    oq, oreps = oracle_run(name, q, aux, nx, ny, dx, dy, steps=steps, order=order,
+                           limiter=limiter, bc_x=bc[0], bc_y=bc[1], cfl=cfl)
+    dq, res, _ = device_run(name, q, aux, nx, ny, dx, dy, steps=steps, order=order,
+                            limiter=limiter, bc_x=bc[0], bc_y=bc[1], cfl=cfl, use_run=use_run)
+    assert res.error.code == 0
+    assert res.steps_done == steps
+    for k, (r, (dt, cfl_r, msx, msy)) in enumerate(zip(oreps, res.reports)):
+        assert (r.dt, r.max_speed_x, r.max_speed_y) == (dt, msx, msy), f"step {k}"
+        assert r.cfl == cfl_r
+    assert same_bits(oq, dq), f"max |diff| = {np.abs(oq - dq).max():.3e}"
+
+
+@pytest.mark.parametrize("bc", BCS)
+@pytest.mark.parametrize("name", SOLVERS)
+def test_first_order_bitwise(name, bc):
+    _compare(name, 37, 29, 4, 1, "none", bc)
+
+
+@pytest.mark.parametrize("limiter", ["minmod", "superbee", "mc"])
+@pytest.mark.parametrize("name", SOLVERS)
+def test_second_order_bitwise(name, limiter):
+    _compare(name, 45, 35, 4, 2, limiter, ("extrapolate", "extrapolate"), seed=1)
+
+
+@pytest.mark.parametrize("name", ["shallow-water-roe", "euler-hlle", "acoustics-var"])
+def test_second_order_periodic_bitwise(name):
+    _compare(name, 40, 33, 4, 2, "mc", ("periodic", "periodic"), seed=2)
+
+
+@pytest.mark.parametrize("name", ["shallow-water-roe", "acoustics-const"])
+def test_graph_run_equals_steps(name):
+    _compare(name, 64, 48, 9, 2, "mc", ("extrapolate", "extrapolate"), seed=3, use_run=True)
+
+
+def test_tiny_grids():
+    for nx, ny in ((1, 1), (2, 3), (5, 1), (33, 17)):
+        _compare("shallow-water-roe", nx, ny, 3, 2, "mc", ("extrapolate", "extrapolate"), seed=4)
+        _compare("acoustics-const", nx, ny, 3, 1, "none", ("extrapolate", "extrapolate"), seed=4)
+    _compare("euler-hlle", 2, 2, 3, 2, "minmod", ("periodic", "periodic"), seed=5)
+
+
+def test_fp32_bitwise_vs_fp32_oracle():
+    name, nx, ny = "shallow-water-roe", 50, 42
+    dx = dy = 1.0 / 50
+    q, aux = random_state(name, nx, ny, 6, dtype=np.float32)
+    oq, oreps = oracle_run(name, q, aux, nx, ny, dx, dy, steps=5, order=2, limiter="mc")
+    assert oq.dtype == np.float32
+    dq, res, _ = device_run(name, q, aux, nx, ny, dx, dy, steps=5, order=2, limiter="mc",
+                            precision="f32")
+    assert [r.dt for r in oreps] == [r[0] for r in res.reports]
+    assert same_bits(oq, dq)
+
+
+def test_fp32_close_to_fp64():
+    name, nx, ny = "shallow-water-roe", 64, 64
+    dx = dy = 1.0 / 64
+    q, _ = random_state(name, nx, ny, 7)
+    q64, _ = oracle_run(name, q, None, nx, ny, dx, dy, steps=20, order=2, limiter="mc")
+    q32, _, _ = device_run(name, np.asfortranarray(q, dtype=np.float32), None, nx, ny, dx, dy,
+                           steps=20, order=2, limiter="mc", precision="f32")
+    h64, h32 = q64[0, 2:-2, 2:-2], q32[0, 2:-2, 2:-2].astype(np.float64)
+    rel = np.abs(h32 - h64).max() / np.abs(h64).max()
+    assert rel <= 1e-5, rel   # stated fp32 bound
+
+
+@pytest.mark.parametrize("name", SOLVERS)
+def test_inadmissible_cell_reports_reference_location(name):
+    from paper_1308_1464_b200 import SweepError
+    from helpers import device_grid
+    from paper_1308_1464_b200 import _abi
+    nx, ny = 12, 9
+    q, aux = random_state(name, nx, ny, 8)
+    if name.startswith("acoustics"):
+        q[1, 2 + 5, 2 + 3] = np.nan
+    else:
+        q[0, 2 + 5, 2 + 3] = -1.0
+    with pytest.raises(O.OracleError) as oe:
+        oracle_run(name, q, aux, nx, ny, 1.0 / nx, 1.0 / ny, steps=1)
+    g = device_grid(name, nx, ny, 1.0 / nx, 1.0 / ny)
+    g.upload(q, aux)
+    g.step(_abi.make_ctl(0.9))
+    res = g.poll()
+    with pytest.raises(SweepError) as de:
+        g.raise_for(res.error)
+    assert str(de.value) == str(oe.value)
+    # state untouched: the download is the uploaded state with its ghosts filled
+    out = g.download()
+    assert np.array_equal(out[:, 2:-2, 2:-2], q[:, 2:-2, 2:-2], equal_nan=True)
+    g.close()
+
+
+def test_error_in_later_step_keeps_last_good_state():
+    """A run that turns inadmissible mid-way stops at the last good state."""
+    from helpers import device_grid
+    from paper_1308_1464_b200 import _abi
+    name, nx, ny = "euler", 24, 16
+    rng = np.random.default_rng(11)
+    q = np.zeros((4, nx + 4, ny + 4), order="F")
+    rho = rng.uniform(0.1, 10, (nx, ny))
+    u = rng.uniform(-3, 3, (nx, ny))
+    v = rng.uniform(-3, 3, (nx, ny))
+    p = rng.uniform(0.1, 10, (nx, ny))
+    q[:, 2:-2, 2:-2] = np.stack([rho, rho * u, rho * v, p / 0.4 + 0.5 * rho * (u * u + v * v)])
+    oq = np.asfortranarray(q.copy())
+    solver = O.make_solver(name, gamma=1.4)
+    good = 0
+    err = None
+    for _ in range(6):
+        try:
+            O.step(oq, None, O.Spec(nx, ny, 1 / nx, 1 / ny), solver, O.Controller(0.9),
+                   bc_x="periodic", bc_y="periodic")
+            good += 1
+        except O.OracleError as e:
+            err = e
+            break
+    assert err is not None, "input should turn inadmissible within 6 steps"
+    g = device_grid(name, nx, ny, 1 / nx, 1 / ny, bc_x="periodic", bc_y="periodic")
+    g.upload(q, None)
+    g.run(6, _abi.make_ctl(0.9))
+    res = g.poll()
+    assert res.steps_done == good
+    assert res.error.step == good
+    out = g.download()
+    assert same_bits(out[:, 2:-2, 2:-2], oq[:, 2:-2, 2:-2])
+    g.close()
+
+
+def test_fixed_dt_bypasses_the_cfl_formula():
+    from helpers import device_grid
+    from paper_1308_1464_b200 import _abi
+    nx = ny = 8
+    qa = np.zeros((3, nx + 4, ny + 4), order="F")
+    aux = np.ones((2, nx + 4, ny + 4), order="F")
+    g = device_grid("acoustics-var", nx, ny, 0.1, 0.1)
+    g.upload(qa, aux)
+    g.step(_abi.make_ctl(0.9, fixed_dt=1e-3))
+    res = g.poll()
+    assert res.error.code == 0 and res.reports[-1][0] == 1e-3
+    # reference cfl = dt * (max_sx/dx + max_sy/dy) with max speeds c = 1
+    assert res.reports[-1][1] == 1e-3 * (1.0 / 0.1 + 1.0 / 0.1)
+    g.close()
+
+
+def test_dt_max_remaining_and_fixed_dt_match_oracle():
+    name, nx, ny = "shallow-water-roe", 30, 20
+    q, _ = random_state(name, nx, ny, 12)
+    for kw in ({"dt_max": 1e-4}, {"fixed_dt": 2.5e-4}):
+        oq, oreps = oracle_run(name, q, None, nx, ny, 1 / nx, 1 / ny, steps=3, order=2,
+                               limiter="superbee", **kw)
+        dq, res, _ = device_run(name, q, None, nx, ny, 1 / nx, 1 / ny, steps=3, order=2,
+                                limiter="superbee", **kw)
+        assert [r.dt for r in oreps] == [r[0] for r in res.reports]
+        assert same_bits(oq, dq)
