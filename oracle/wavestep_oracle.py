@@ -289,8 +289,11 @@ def rp_euler_hlle(ni, ql, qr, auxl, auxr, p):
       per side: u_n, u_t, p as reference kernels.py:475-478, c = sqrt(g p/rho)
       Roe averages u^, c^ as reference kernels.py:482-495
       s1 = min(u_l - c_l, u^ - c^),  s2 = max(u_r + c_r, u^ + c^)
-      q_m = ((f(q_r) - f(q_l)) - s2 q_r + s1 q_l) * (1 / (s1 - s2))
-      W1 = q_m - q_l at s1,  W2 = q_r - q_m at s2
+      with df = f(q_r) - f(q_l), dq = q_r - q_l and the middle state
+      q_m = (df - s2 q_r + s1 q_l) / (s1 - s2):
+      W1 = q_m - q_l = (df - s2 dq) * (1/(s1 - s2))  at s1
+      W2 = q_r - q_m = (s1 dq - df) * (1/(s1 - s2))  at s2
+      (written on the jumps so a zero jump gives exactly zero waves)
     amdq/apdq = sum of min/max(s,0) W in wave order.
     """
     gam = p["gamma"]
@@ -319,10 +322,11 @@ def rp_euler_hlle(ni, ql, qr, auxl, auxr, p):
         f[ti] = q[ti] * u
         f[3] = u * (q[3] + pp)
     inv = 1.0 / (s1 - s2)
-    qm = (fr - fl - s2 * qr + s1 * ql) * inv
+    df = fr - fl
+    dq = qr - ql
     w = np.empty((2, 4) + s1.shape, dtype=s1.dtype)
-    w[0] = qm - ql
-    w[1] = qr - qm
+    w[0] = (df - s2 * dq) * inv     # = q_m - q_l
+    w[1] = (s1 * dq - df) * inv     # = q_r - q_m
     s = np.stack([s1, s2])
     neg = np.minimum(s, 0.0)
     pos = np.maximum(s, 0.0)

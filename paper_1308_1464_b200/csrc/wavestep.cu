@@ -11,6 +11,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/wavestep.h"
@@ -68,6 +70,12 @@ struct ws_handle {
   ws_ctl gctl{};
   cudaStream_t gstream = nullptr;
   long long launches = 0;
+  int variant = 0;              // WS_TILE experiment selector (0 = default tiles)
+  bool fused = false;           // next-step CFL maxima computed in the update epilogue
+  bool need_prepass = true;     // fused mode: slot of the current state not yet filled
+  int* borders = nullptr;       // tile-border counters of the fused epilogue
+  int exp = 0;                  // WS_EXP timing-study switches
+  size_t border_bytes = 0;
   std::string err;
 };
 
@@ -95,6 +103,70 @@ cudaStream_t pick(ws_handle* h, void* s) {
   return st;
 }
 
+// persistent grid: resident CTAs (occupancy query, cached per kernel), capped
+// by the tile count
+template <class K>
+int persistent_grid(K kernel, int nt, size_t smem, int nx, int ny, int tx, int ty) {
+  static std::unordered_map<const void*, int> cache;   // resident CTAs per SM, per kernel
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  auto it = cache.find((const void*)kernel);
+  int per_sm;
+  if (it == cache.end()) {
+    per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem);
+    if (per_sm < 1) per_sm = 1;
+    cache[(const void*)kernel] = per_sm;
+  } else {
+    per_sm = it->second;
+  }
+  const long long tiles = (long long)((nx + tx - 1) / tx) * ((ny + ty - 1) / ty);
+  const long long g = (long long)per_sm * sms;
+  return (int)(tiles < g ? tiles : g);
+}
+
+// ---- tile-shape experiments (WS_TILE=k selects variant k; SW fp64 order 2 MC)
+template <class S, class R, int ORDER, int LIM, int TX, int TY, int NT>
+void launch_variant(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
+  using G = TileGeom<S, ORDER, TX, TY>;
+  const size_t smem = G::template smem_bytes<R>();
+  auto go = [&](auto k) {
+    static bool done = false;
+    if (!done) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); done = true; }
+    dim3 grid(persistent_grid(k, NT, smem, h->L.nx, h->L.ny, TX, TY));
+    k<<<grid, NT, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
+                              static_cast<R*>(qn), h->L,
+                              *reinterpret_cast<const typename S::template Params<R>*>(h->params.data()),
+                              a, h->ds);
+  };
+  if (h->fused) go(k_update<S, R, ORDER, LIM, TX, TY, NT, false, true>);
+  else go(k_update<S, R, ORDER, LIM, TX, TY, NT, false, false>);
+  h->launches++;
+}
+
+template <class S, class R, int ORDER, int LIM>
+bool variant_update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
+  if constexpr (std::is_same<S, ShallowRoe>::value && std::is_same<R, double>::value &&
+                ORDER == 2 && LIM == LIM_MC) {
+    switch (h->variant) {
+      case 1: launch_variant<S, R, 2, LIM_MC, 32, 8, 256>(h, q, qn, a, st); return true;
+      case 2: launch_variant<S, R, 2, LIM_MC, 32, 13, 256>(h, q, qn, a, st); return true;
+      case 3: launch_variant<S, R, 2, LIM_MC, 64, 8, 256>(h, q, qn, a, st); return true;
+      case 4: launch_variant<S, R, 2, LIM_MC, 32, 16, 128>(h, q, qn, a, st); return true;
+      case 5: launch_variant<S, R, 2, LIM_MC, 16, 16, 256>(h, q, qn, a, st); return true;
+      case 6: launch_variant<S, R, 2, LIM_MC, 32, 8, 128>(h, q, qn, a, st); return true;
+      case 7: launch_variant<S, R, 2, LIM_MC, 64, 6, 256>(h, q, qn, a, st); return true;
+      case 8: launch_variant<S, R, 2, LIM_MC, 32, 12, 192>(h, q, qn, a, st); return true;
+      default: return false;
+    }
+  }
+  return false;
+}
+
 // ---- typed launchers -----------------------------------------------------
 template <class S, class R, int ORDER, int LIM> struct Impl {
   using P = typename S::template Params<R>;
@@ -110,27 +182,32 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     h->launches++;
   }
 
-  static void prepare() {
-    const int smem = (int)G::template smem_bytes<R>();
-    cudaFuncSetAttribute(k_update<S, R, ORDER, LIM, C::TX, C::TY, C::NT, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_update<S, R, ORDER, LIM, C::TX, C::TY, C::NT, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  template <bool CHECKS, bool FUSED> static auto kern() {
+    return k_update<S, R, ORDER, LIM, C::TX, C::TY, C::NT, CHECKS, FUSED>;
   }
 
-  template <bool CHECKS> static void update_t(ws_handle* h, const void* q, void* qn,
-                                              const StepArgs& a, cudaStream_t st) {
-    auto k = k_update<S, R, ORDER, LIM, C::TX, C::TY, C::NT, CHECKS>;
+  static void prepare() {
+    const int smem = (int)G::template smem_bytes<R>();
+    cudaFuncSetAttribute(kern<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern<false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+
+  template <bool CHECKS, bool FUSED> static void update_t(ws_handle* h, const void* q, void* qn,
+                                                          const StepArgs& a, cudaStream_t st) {
+    auto k = kern<CHECKS, FUSED>();
     const size_t smem = G::template smem_bytes<R>();
-    dim3 grid((h->L.nx + C::TX - 1) / C::TX, (h->L.ny + C::TY - 1) / C::TY);
+    dim3 grid(persistent_grid(k, C::NT, smem, h->L.nx, h->L.ny, C::TX, C::TY));
     k<<<grid, C::NT, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
                                  static_cast<R*>(qn), h->L, prm(h), a, h->ds);
     h->launches++;
   }
 
   static void update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
-    if (S::STATIC_SPEEDS && !h->multi) update_t<true>(h, q, qn, a, st);
-    else update_t<false>(h, q, qn, a, st);
+    if (h->variant > 0 && variant_update<S, R, ORDER, LIM>(h, q, qn, a, st)) return;
+    if (S::STATIC_SPEEDS && !h->multi) update_t<true, false>(h, q, qn, a, st);
+    else if (h->fused) update_t<false, true>(h, q, qn, a, st);
+    else update_t<false, false>(h, q, qn, a, st);
   }
 
   static void to_soa(ws_handle* h, const void* stage, void* dst, int ncomp, cudaStream_t st) {
@@ -292,8 +369,9 @@ int validate(const ws_desc* d, std::string& m) {
   if (d->ny_global < d->ny || d->j_offset < 0 || d->j_offset + d->ny > d->ny_global) {
     m = "inconsistent row-strip geometry (ny_global / j_offset)"; return WS_ERR_CONFIG;
   }
-  if (d->nx >= (1 << 19) || d->ny_global >= (1 << 19)) {
-    m = "grid too large for the 19-bit interface indices of the error key"; return WS_ERR_CONFIG;
+  if (d->nx >= (1 << 19) || d->ny_global >= (1 << 18)) {
+    m = "grid too large for the interface indices of the error key (nx < 2^19, ny < 2^18)";
+    return WS_ERR_CONFIG;
   }
   return WS_OK;
 }
@@ -325,6 +403,8 @@ StepArgs make_args(ws_handle* h, const ws_ctl* c, int cur) {
   a.tol = a.has_t_final ? 1e-14 * std::fmax(1.0, c->t_final) : 0.0;   // driver.py:525
   a.cur = cur;
   a.static_speeds = (h->ops.static_speeds && !h->multi) ? 1 : 0;
+  a.borders = h->borders;
+  a.exp = h->exp;
   return a;
 }
 
@@ -343,7 +423,11 @@ int check_ctl(ws_handle* h, const ws_ctl* c) {
 // enqueue one step of parity `cur` from q[cur] into q[cur^1]
 void enqueue_step(ws_handle* h, const ws_ctl* c, int cur, cudaStream_t st) {
   StepArgs a = make_args(h, c, cur);
-  if (!a.static_speeds) h->ops.speeds(h, h->q[cur], cur, st);
+  if (!a.static_speeds) {
+    // fused mode: the pre-pass only for a state the epilogue has not probed
+    if (!h->fused || h->need_prepass) h->ops.speeds(h, h->q[cur], cur, st);
+    h->need_prepass = false;
+  }
   h->ops.update(h, h->q[cur], h->q[cur ^ 1], a, st);
 }
 
@@ -402,7 +486,18 @@ int ws_create(const ws_desc* d, ws_handle** out) {
     return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
   }
   h->ds = static_cast<DevState*>(dsp);
+  h->fused = !h->ops.static_speeds && !h->multi;
+  if (const char* v = std::getenv("WS_NOFUSE")) h->fused = h->fused && std::atoi(v) == 0;
+  if (const char* v = std::getenv("WS_EXP")) h->exp = std::atoi(v);
+  // generous for every tile shape (TX >= 16, TY >= 4): vertical + horizontal borders
+  h->border_bytes = sizeof(int) * 2 * (size_t)((d->nx + 15) / 16 + 1) * ((d->ny + 3) / 4 + 1);
+  if ((e = cudaMalloc(&h->borders, h->border_bytes)) != cudaSuccess) {
+    ws_destroy(h);
+    return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaMemsetAsync(h->borders, 0, h->border_bytes, h->stream);
   h->ops.prepare();
+  if (const char* v = std::getenv("WS_TILE")) h->variant = std::atoi(v);
   // zero everything once so ghost rows / padding are defined
   cudaMemsetAsync(h->q[0], 0, qb, h->stream);
   cudaMemsetAsync(h->q[1], 0, qb, h->stream);
@@ -422,6 +517,7 @@ void ws_destroy(ws_handle* h) {
   if (h->own_aux && h->aux) cudaFree(h->aux);
   if (h->own_ds && h->ds) cudaFree(h->ds);
   if (h->stage) cudaFree(h->stage);
+  if (h->borders) cudaFree(h->borders);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -454,6 +550,8 @@ static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz
     h->ops.to_soa(h, h->stage, h->aux, h->naux, st);
   }
   WS_CUDA(h, cudaMemsetAsync(h->ds, 0, offsetof(DevState, rep), st));
+  WS_CUDA(h, cudaMemsetAsync(h->borders, 0, h->border_bytes, st));
+  h->need_prepass = true;
   if (h->ops.static_speeds) {
     if (h->naux > 0) {
       h->ops.static_speed(h, st);
@@ -504,6 +602,7 @@ static int resync(ws_handle* h, const HostState& hs, cudaStream_t st) {
   if (h->enq != hs.steps) {
     h->enq = hs.steps;
     WS_CUDA(h, cudaMemsetAsync(&h->ds->slot[0][0], 0, sizeof(h->ds->slot), st));
+    h->need_prepass = true;
   }
   return WS_OK;
 }
@@ -546,7 +645,9 @@ int ws_step(ws_handle* h, const ws_ctl* c, void* s) {
 int ws_phase_speeds(ws_handle* h, void* s) {
   if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
   cudaStream_t st = pick(h, s);
-  h->ops.speeds(h, h->q[h->enq & 1], (int)(h->enq & 1), st);
+  // single-shard dynamic solvers probe the next state in the update epilogue
+  if (!h->fused || h->need_prepass) h->ops.speeds(h, h->q[h->enq & 1], (int)(h->enq & 1), st);
+  h->need_prepass = false;
   WS_CUDA(h, cudaGetLastError());
   return WS_OK;
 }
@@ -596,6 +697,11 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
   WS_CUDA(h, cudaMemsetAsync(&h->ds->finished, 0, sizeof(int), st));
   long long left = nsteps;
   if (left > 0 && (h->enq & 1)) { enqueue_step(h, c, 1, st); h->enq++; left--; }
+  if (left >= 4 && h->need_prepass && !h->ops.static_speeds) {
+    // keep the one-off pre-pass out of the captured graph
+    enqueue_step(h, c, 0, st); h->enq++; left--;
+    enqueue_step(h, c, 1, st); h->enq++; left--;
+  }
   if (left >= 4 && st != nullptr) {
     // two-step graph (parity 0 then 1), cached per (ctl, stream)
     if (!h->gexec || std::memcmp(&h->gctl, c, sizeof(ws_ctl)) != 0 || h->gstream != st) {
@@ -612,7 +718,7 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
       h->gctl = *c;
       h->gstream = st;
     }
-    const int per_pair = (h->ops.static_speeds && !h->multi) ? 2 : 4;
+    const int per_pair = (h->ops.static_speeds && !h->multi) || h->fused ? 2 : 4;
     while (left >= 2) {
       WS_CUDA(h, cudaGraphLaunch(h->gexec, st));
       h->launches += per_pair;
@@ -664,11 +770,11 @@ int ws_poll(ws_handle* h, int64_t* steps_done, ws_report* reports, int32_t max_r
     err->step = hs.err_step;
     if (hs.err == ERR_KERNEL) {
       unsigned long long k = hs.err_key;
-      err->direction = (int)(k >> 63);
-      err->stage = (int)((k >> 41) & 0xf);
-      err->component = (int)((k >> 38) & 0x7);
-      err->i = (int)((k >> 19) & 0x7ffff);
-      err->j = (int)(k & 0x7ffff);
+      err->direction = (int)(k >> 62);
+      err->stage = (int)((k >> 40) & 0xf);
+      err->component = (int)((k >> 37) & 0x7);
+      err->i = (int)((k >> 18) & 0x7ffff);
+      err->j = (int)(k & 0x3ffff);
     }
   }
   return hs.err ? hs.err : WS_OK;

@@ -39,8 +39,9 @@ struct Layout {
 struct Report { double dt, cfl, msx, msy; };
 
 // Device-resident step state.  slot[k&1] = {max|s| x bits, max|s| y bits,
-// ~first-error-key}: reduced with MAX (so the smallest key wins), which is
-// also what a multi-shard all-reduce of the 3 x u64 does.
+// NKEY_MAX - first error key}: every entry is reduced with MAX (non-negative
+// IEEE values order like their bit patterns; the smallest key wins), which is
+// also what a multi-shard all-reduce (int64 MAX) of the 3 words does.
 struct DevState {
   unsigned long long slot[2][3];
   unsigned long long static_bits[2];  // acoustics: precomputed max speeds
@@ -62,6 +63,8 @@ struct StepArgs {
   int has_dt_max, has_fixed, has_remaining, has_t_final;
   int cur;              // slot parity of this step
   int static_speeds;    // 1: max speeds come from DevState::static_bits
+  int* borders;         // tile-border counters of the fused CFL epilogue
+  int exp;              // experiment switches (WS_EXP, timing studies only)
 };
 
 __device__ __forceinline__ int map_i(int i, const Layout& L) {
@@ -89,16 +92,19 @@ __device__ __forceinline__ long long row_off(int j, const Layout& L) {
 // Error key: ordering of reference CellWise/Serial sweeps (sweep.py:203-218):
 // all x chunks, then y; chunk = MAX_BLOCK // width rows (sweep.py:117-119);
 // inside a chunk the kernel's admissibility stage, then the first bad element
-// in C order over (component, i, j) (kernels.py:325-328).
+// in C order over (component, i, j) (kernels.py:325-328).  63 bits, so the
+// reduction slot stores NKEY_MAX - key >= 0 and one int64/u64 MAX all-reduce
+// across shards picks the smallest key.
+constexpr unsigned long long NKEY_MAX = 0x7fffffffffffffffull;
 __device__ __forceinline__ unsigned long long err_key(int dir, int i, int jg, int stage,
                                                       int comp, int nx) {
   int width = dir == 0 ? nx + 1 : nx;
   int rows_per = 32768 / width;
   if (rows_per < 1) rows_per = 1;
   unsigned long long chunk = (unsigned long long)(jg / rows_per);
-  return ((unsigned long long)dir << 63) | (chunk << 45) |
-         ((unsigned long long)stage << 41) | ((unsigned long long)comp << 38) |
-         ((unsigned long long)i << 19) | (unsigned long long)jg;
+  return ((unsigned long long)dir << 62) | (chunk << 44) |
+         ((unsigned long long)stage << 40) | ((unsigned long long)comp << 37) |
+         ((unsigned long long)i << 18) | (unsigned long long)jg;
 }
 
 template <class R> struct Bits;
@@ -137,18 +143,19 @@ __device__ __forceinline__ Ctl step_control(const StepArgs& A, const DevState* d
                                             bool pending_error_blocks) {
   Ctl c;
   c.skip = 0; c.stationary = 0; c.finished = 0; c.dt = 0.0;
-  volatile const DevState* vds = ds;
-  if (vds->err) { c.skip = 1; c.msx = c.msy = 0.0; return c; }
+  // plain L2 reads: everything read here was written by an earlier kernel
+  // (the commit of the previous step / the speeds pre-pass)
+  if (__ldcg(&ds->err)) { c.skip = 1; c.msx = c.msy = 0.0; return c; }
   unsigned long long bx, by;
-  if (A.static_speeds) { bx = vds->static_bits[0]; by = vds->static_bits[1]; }
-  else { bx = vds->slot[A.cur][0]; by = vds->slot[A.cur][1]; }
+  if (A.static_speeds) { bx = __ldcg(&ds->static_bits[0]); by = __ldcg(&ds->static_bits[1]); }
+  else { bx = __ldcg(&ds->slot[A.cur][0]); by = __ldcg(&ds->slot[A.cur][1]); }
   c.msx = (double)Bits<R>::from(bx);
   c.msy = (double)Bits<R>::from(by);
-  if (pending_error_blocks && vds->slot[A.cur][2] != 0ull) c.skip = 1;
+  if (pending_error_blocks && __ldcg(&ds->slot[A.cur][2]) != 0ull) c.skip = 1;
   double remaining = A.remaining;
   int has_rem = A.has_remaining;
   if (A.has_t_final) {
-    double t = vds->t;
+    double t = __ldcg(&ds->t);
     if (!(A.t_final - t > A.tol)) { c.skip = 1; c.finished = 1; return c; }
     remaining = A.t_final - t;
     has_rem = 1;

@@ -57,11 +57,13 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   __shared__ R sA[NAUX > 0 ? NAUX : 1][HC];
   __shared__ R sP[NPR > 0 ? NPR : 1][HC];
   __shared__ unsigned long long sred[NT / 32];
-  {
-    volatile const DevState* vds = ds;
-    if (vds->err || vds->finished) return;   // stable for the whole kernel
-  }
+  __shared__ int s_skip;
   const int tid = threadIdx.x;
+  // one L2 read per CTA (the flags cannot change during this kernel: only the
+  // update kernel's commit writes them); broadcast through shared memory
+  if (tid == 0) s_skip = __ldcg(&ds->err) | __ldcg(&ds->finished);
+  __syncthreads();
+  if (s_skip) return;
   const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
   // tile cell (lx, ly) = cell (i0 - 1 + lx, j0 - 1 + ly)
   for (int idx = tid; idx < HC; idx += NT) {
@@ -116,7 +118,7 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
     R s = edge(NY{}, lj * HX + li + 1, (lj + 1) * HX + li + 1, 1, i, j);
     my = nmax(my, s);
   }
-  if (key != ~0ull) atomicMax(&ds->slot[cur][2], ~key);
+  if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
   unsigned long long bx = block_max_u64<NT>(Bits<R>::to(mx), sred);
   __syncthreads();
   unsigned long long by = block_max_u64<NT>(Bits<R>::to(my), sred);
@@ -137,7 +139,7 @@ __device__ __forceinline__ void commit_step(DevState* ds, const StepArgs& A, con
     if (c.finished) {
       v->finished = 1;
     } else if (nkey != 0ull) {
-      v->err = ERR_KERNEL; v->err_key = ~nkey; v->err_step = v->steps;
+      v->err = ERR_KERNEL; v->err_key = NKEY_MAX - nkey; v->err_step = v->steps;
     } else if (c.stationary) {
       v->err = ERR_STATIONARY; v->err_step = v->steps;
     } else {
@@ -152,8 +154,8 @@ __device__ __forceinline__ void commit_step(DevState* ds, const StepArgs& A, con
       v->t = v->t + c.dt;
     }
   }
-  // the next step's speeds kernel accumulates into the other slot
-  v->slot[A.cur ^ 1][0] = 0ull; v->slot[A.cur ^ 1][1] = 0ull; v->slot[A.cur ^ 1][2] = 0ull;
+  // this step's slot is consumed; it is the accumulator of the step after next
+  v->slot[A.cur][0] = 0ull; v->slot[A.cur][1] = 0ull; v->slot[A.cur][2] = 0ull;
   __threadfence();
   v->done = 0;
 }
@@ -176,13 +178,184 @@ struct TileGeom {
   static constexpr int NFL = (ORDER == 2 ? 3 : 2) * NEQ;  // amdq, apdq [, F~]
   static constexpr int EBUF = (ORDER == 2) ? (NEST * NWS > NIST * NFL ? NEST * NWS : NIST * NFL)
                                            : NIST * NFL;
+  // double-buffered q and aux tiles + primitives + edge records
   template <class R> static constexpr size_t smem_bytes() {
-    return sizeof(R) * (size_t)((NEQ + NAUX + NPR) * HC + EBUF);
+    return sizeof(R) * (size_t)((2 * NEQ + 2 * NAUX + NPR) * HC + EBUF);
   }
 };
 
-template <class S, class R, int ORDER, int LIM, int TX, int TY, int NT, bool CHECKS>
-__global__ void __launch_bounds__(NT)
+// --------------------------------------------------------------------------
+// FUSED CFL epilogue: max |s| and admissibility of the NEXT step's state,
+// computed while q_new is still in shared memory.  Every reference edge is
+// probed exactly once: edges inside a tile by that tile; extrapolated
+// domain-boundary edges (ghost == boundary cell) by the boundary tile; an
+// edge on a border shared by two tiles (or the periodic wrap) by whichever
+// of the two finishes SECOND — it sees the other's q_new through a per-border
+// counter (+1 per side per step; odd previous value = the other side is
+// done), so nothing ever waits.  Single-shard only (shard borders need the
+// exchanged halo, the multi-shard path keeps the k_speeds pre-pass).
+template <class S, class R, int TX, int TY, int NT, int H>
+__device__ __forceinline__ void next_step_speeds(
+    R* sQ, const R* sA, R* sP, const R* __restrict__ qn, const R* __restrict__ aux,
+    const Layout& L, const typename S::template Params<R>& P, const StepArgs& A, int i0, int j0,
+    int tc, int tr, int ntx, int nty, int* s_second, R& nmx, R& nmy, unsigned long long& nkey) {
+  constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int HX = TX + 2 * H, HC = HX * (TY + 2 * H);
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  static_assert(2 * TX + 2 * TY <= NT, "one thread per border edge");
+  const int tid = threadIdx.x;
+  const int nxv = min(TX, L.nx - i0), nyv = min(TY, L.ny - j0);
+  const bool perx = L.bcx == BC_PERIODIC, pery = L.bcy == BC_PERIODIC;
+  __syncthreads();   // q_new of the whole tile is in sQ
+
+  // primitives of the tile's new cells
+  for (int c2 = tid; c2 < TX * TY; c2 += NT) {
+    const int idx = (c2 / TX + H) * HX + c2 % TX + H;
+    R qc[NEQ], ac[NA1], pc[NP1];
+#pragma unroll
+    for (int c = 0; c < NEQ; ++c) qc[c] = sQ[c * HC + idx];
+#pragma unroll
+    for (int c = 0; c < NAUX; ++c) ac[c] = sA[c * HC + idx];
+    S::prims(qc, ac, P, pc);
+#pragma unroll
+    for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
+  }
+  __syncthreads();
+
+  auto probe_smem = [&](auto ni_tag, int cl, int cr, int dir, int gi, int gj, R& mx) {
+    constexpr int NI = decltype(ni_tag)::value;
+    R ql[NEQ], qr[NEQ], al[NA1], ar[NA1], pl[NP1], pr[NP1];
+#pragma unroll
+    for (int c = 0; c < NEQ; ++c) { ql[c] = sQ[c * HC + cl]; qr[c] = sQ[c * HC + cr]; }
+#pragma unroll
+    for (int c = 0; c < NAUX; ++c) { al[c] = sA[c * HC + cl]; ar[c] = sA[c * HC + cr]; }
+#pragma unroll
+    for (int c = 0; c < NPR; ++c) { pl[c] = sP[c * HC + cl]; pr[c] = sP[c * HC + cr]; }
+    R sm;
+    int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+    if (code) {
+      unsigned long long k = err_key(dir, gi, L.j_off + gj, (code & 0xff) - 1, code >> 8, L.nx);
+      nkey = k < nkey ? k : nkey;
+    } else {
+      mx = nmax(mx, sm);
+    }
+  };
+  using NX = std::integral_constant<int, 1>;
+  using NY = std::integral_constant<int, 2>;
+  auto cidx = [&](int li, int lr) { return (lr + H) * HX + li + H; };
+
+  // x-edges owned by the tile itself
+  for (int e = tid; e < (TX + 1) * TY; e += NT) {
+    const int le = e % (TX + 1), lr = e / (TX + 1);
+    if (lr >= nyv || le > nxv) continue;
+    const int gi = i0 + le;
+    if (le > 0 && le < nxv) probe_smem(NX{}, cidx(le - 1, lr), cidx(le, lr), 0, gi, j0 + lr, nmx);
+    else if (!perx && gi == 0) probe_smem(NX{}, cidx(0, lr), cidx(0, lr), 0, 0, j0 + lr, nmx);
+    else if (!perx && gi == L.nx)
+      probe_smem(NX{}, cidx(nxv - 1, lr), cidx(nxv - 1, lr), 0, gi, j0 + lr, nmx);
+  }
+  // y-edges owned by the tile itself
+  for (int e = tid; e < TX * (TY + 1); e += NT) {
+    const int li = e % TX, le = e / TX;
+    if (li >= nxv || le > nyv) continue;
+    const int gj = j0 + le;
+    if (le > 0 && le < nyv) probe_smem(NY{}, cidx(li, le - 1), cidx(li, le), 1, i0 + li, gj, nmy);
+    else if (!pery && gj == 0) probe_smem(NY{}, cidx(li, 0), cidx(li, 0), 1, i0 + li, 0, nmy);
+    else if (!pery && gj == L.ny)
+      probe_smem(NY{}, cidx(li, nyv - 1), cidx(li, nyv - 1), 1, i0 + li, gj, nmy);
+  }
+
+  // shared borders: left/right = vertical border ids, bottom/top = horizontal
+  if (A.exp & 1) return;   // timing study: interior edges only (NOT a valid CFL max)
+  __syncthreads();
+  if (tid == 0) {
+    if (A.exp & 2) __threadfence();
+    int* vb = A.borders;                 // [nty][ntx]: left border of tile column c
+    int* hb = A.borders + ntx * nty;     // [nty][ntx]: bottom border of tile row r
+    int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    if (tc > 0 || perx) s0 = atomicAdd(&vb[tr * ntx + tc], 1) & 1;
+    if (tc + 1 < ntx) s1 = atomicAdd(&vb[tr * ntx + tc + 1], 1) & 1;
+    else if (perx) s1 = atomicAdd(&vb[tr * ntx + 0], 1) & 1;
+    if (tr > 0 || pery) s2 = atomicAdd(&hb[tr * ntx + tc], 1) & 1;
+    if (tr + 1 < nty) s3 = atomicAdd(&hb[(tr + 1) * ntx + tc], 1) & 1;
+    else if (pery) s3 = atomicAdd(&hb[0 * ntx + tc], 1) & 1;
+    __threadfence();
+    s_second[0] = s0; s_second[1] = s1; s_second[2] = s2; s_second[3] = s3;
+  }
+  __syncthreads();
+
+  auto probe_glob = [&](auto ni_tag, int il, int jl, int ir, int jr, int dir, int gi, int gj,
+                        R& mx) {
+    constexpr int NI = decltype(ni_tag)::value;
+    R ql[NEQ], qr[NEQ], al[NA1], ar[NA1], pl[NP1], pr[NP1];
+    const R* a = qn + row_off(jl, L) + il;
+    const R* b = qn + row_off(jr, L) + ir;
+#pragma unroll
+    for (int c = 0; c < NEQ; ++c) { ql[c] = __ldcg(a + c * L.pitch); qr[c] = __ldcg(b + c * L.pitch); }
+    if (NAUX > 0) {
+      const R* xa = aux + (long long)(jl + 2) * L.astride + il;
+      const R* xb = aux + (long long)(jr + 2) * L.astride + ir;
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) { al[c] = xa[c * L.pitch]; ar[c] = xb[c * L.pitch]; }
+    }
+    S::prims(ql, al, P, pl);
+    S::prims(qr, ar, P, pr);
+    R sm;
+    int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+    if (code) {
+      unsigned long long k = err_key(dir, gi, L.j_off + gj, (code & 0xff) - 1, code >> 8, L.nx);
+      nkey = k < nkey ? k : nkey;
+    } else {
+      mx = nmax(mx, sm);
+    }
+  };
+  // left border: x-edge i0 (tile column > 0) or the periodic wrap pair (nx-1 | 0), edge 0
+  if (s_second[0] && tid < nyv) {
+    const int j = j0 + tid;
+    if (tc > 0) probe_glob(NX{}, i0 - 1, j, i0, j, 0, i0, j, nmx);
+    else probe_glob(NX{}, L.nx - 1, j, 0, j, 0, 0, j, nmx);
+  }
+  // right border
+  if (s_second[1] && tid >= TY && tid < TY + nyv) {
+    const int j = j0 + tid - TY;
+    if (tc + 1 < ntx) probe_glob(NX{}, i0 + TX - 1, j, i0 + TX, j, 0, i0 + TX, j, nmx);
+    else probe_glob(NX{}, L.nx - 1, j, 0, j, 0, 0, j, nmx);
+  }
+  // bottom border: y-edge j0 or the periodic wrap pair (ny-1 | 0), edge 0
+  if (s_second[2] && tid >= 2 * TY && tid < 2 * TY + nxv) {
+    const int i = i0 + tid - 2 * TY;
+    if (tr > 0) probe_glob(NY{}, i, j0 - 1, i, j0, 1, i, j0, nmy);
+    else probe_glob(NY{}, i, L.ny - 1, i, 0, 1, i, 0, nmy);
+  }
+  // top border
+  if (s_second[3] && tid >= 2 * TY + TX && tid < 2 * TY + TX + nxv) {
+    const int i = i0 + tid - 2 * TY - TX;
+    if (tr + 1 < nty) probe_glob(NY{}, i, j0 + TY - 1, i, j0 + TY, 1, i, j0 + TY, nmy);
+    else probe_glob(NY{}, i, L.ny - 1, i, 0, 1, i, 0, nmy);
+  }
+}
+
+// cp.async (LDGSTS): global -> shared without a register round trip, so the
+// next tile's loads are in flight while the current tile is computed
+__device__ __forceinline__ void cp_async(void* smem, const double* g) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_async(void* smem, const float* g) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Persistent CTAs walk the tiles (t = blockIdx.x, += gridDim.x).  Per tile:
+// wait for its staged q(+aux) (issued one tile earlier), compute per-cell
+// primitives, x sweep (solve -> limit -> records), x term, y sweep, y term +
+// correction fluxes, store.  The next tile's loads overlap all of that.
+template <class S, class R, int ORDER, int LIM, int TX, int TY, int NT, bool CHECKS, bool FUSED>
+__global__ void __launch_bounds__(NT, (512 / NT > 0 ? 512 / NT : 1))
 k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn, const Layout L,
          const typename S::template Params<R> P, const StepArgs A, DevState* __restrict__ ds) {
   using G = TileGeom<S, ORDER, TX, TY>;
@@ -190,219 +363,275 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
   constexpr int H = G::H, HX = G::HX, HC = G::HC;
   constexpr int NEXC = G::NEXC, NEX = G::NEX, NEY = G::NEY, NEST = G::NEST, NIST = G::NIST;
   constexpr int KEX = (NEX + NT - 1) / NT, KEY = (NEY + NT - 1) / NT;
-  constexpr int KC = (TX * TY) / NT;
+  constexpr int NCELL = TX * TY;
+  constexpr int KC = (NCELL + NT - 1) / NT;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
-  static_assert(KC * NT == TX * TY, "tile must be a multiple of the block");
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* sQ = reinterpret_cast<R*>(smem_raw);
-  R* sA = sQ + NEQ * HC;
-  R* sP = sA + NAUX * HC;
+  R* sQb[2];
+  R* sAb[2];
+  sQb[0] = reinterpret_cast<R*>(smem_raw);
+  sQb[1] = sQb[0] + NEQ * HC;
+  sAb[0] = sQb[1] + NEQ * HC;
+  sAb[1] = sAb[0] + NAUX * HC;
+  R* sP = sAb[1] + NAUX * HC;
   R* sE = sP + NPR * HC;   // wave records (order 2), then fluctuation/flux records
-  __shared__ Ctl s_ctl;
 
   const int tid = threadIdx.x;
-  if (tid == 0) s_ctl = step_control<R>(A, ds, !CHECKS);
-  __syncthreads();
-  const Ctl ctl = s_ctl;
+  const Ctl ctl = step_control<R>(A, ds, !CHECKS);   // identical in every thread
+  const int ntx = (L.nx + TX - 1) / TX;
+  const int nty = (L.ny + TY - 1) / TY;
+  const int ntiles = ntx * nty;
+  __shared__ unsigned long long s_red[NT / 32];
+  __shared__ int s_second[4];
+  R nmx = (R)0, nmy = (R)0;            // next step's max |s| (FUSED epilogue)
+  unsigned long long nkey = ~0ull;     // next step's first inadmissible edge
 
   if (!ctl.skip) {
-    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
     const R dtdx = (R)(ctl.dt / A.dx);
     const R dtdy = (R)(ctl.dt / A.dy);
     unsigned long long key = ~0ull;
 
-    // ---- stage the tile + halo (BC by index mapping) and per-cell primitives
-    for (int idx = tid; idx < HC; idx += NT) {
-      int lx = idx % HX, ly = idx / HX;
-      int gi = map_i(i0 - H + lx, L), gj = map_j(j0 - H + ly, L);
-      R qc[NEQ], ac[NA1], pc[NP1];
-      const R* src = q + row_off(gj, L) + gi;
+    auto stage = [&](int t, R* dq, R* da) {
+      const int i0 = (t % ntx) * TX, j0 = (t / ntx) * TY;
+      for (int idx = tid; idx < HC; idx += NT) {
+        const int lx = idx % HX, ly = idx / HX;
+        const int gi = map_i(i0 - H + lx, L), gj = map_j(j0 - H + ly, L);
+        const R* src = q + row_off(gj, L) + gi;
 #pragma unroll
-      for (int c = 0; c < NEQ; ++c) { qc[c] = src[c * L.pitch]; sQ[c * HC + idx] = qc[c]; }
-      if (NAUX > 0) {
-        const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+        for (int c = 0; c < NEQ; ++c) cp_async(&dq[c * HC + idx], src + c * L.pitch);
+        if (NAUX > 0) {
+          const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
 #pragma unroll
-        for (int c = 0; c < NAUX; ++c) { ac[c] = asrc[c * L.pitch]; sA[c * HC + idx] = ac[c]; }
-      }
-      if (NPR > 0) {
-        S::prims(qc, ac, P, pc);
-#pragma unroll
-        for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
-      }
-    }
-    __syncthreads();
-
-    R q1[KC][NEQ], dfx[KC][NEQ];
-
-    // one sweep direction: solve -> (limit) -> fluctuation/flux records in sE
-    auto sweep = [&](auto ni_tag) {
-      constexpr int NI = decltype(ni_tag)::value;
-      constexpr int NE = (NI == 1) ? NEX : NEY;
-      constexpr int KE = (NI == 1) ? KEX : KEY;
-      R fm[KE][NEQ], fp[KE][NEQ], ff[KE][NEQ];
-      // solve every edge of the tile (+ the limiter's neighbours for order 2)
-#pragma unroll
-      for (int k = 0; k < KE; ++k) {
-        const int e = tid + k * NT;
-        if (e < NE) {
-          int cl, cr, ei, ej;
-          if (NI == 1) {
-            const int r = e / NEXC, c = e - r * NEXC;
-            cl = (r + H) * HX + c; cr = cl + 1;
-            ei = i0 - (H - 1) + c; ej = j0 + r;
-          } else {
-            const int r = e / TX, c = e - r * TX;
-            cl = r * HX + c + H; cr = cl + HX;
-            ei = i0 + c; ej = j0 - (H - 1) + r;
-          }
-          R ql[NEQ], qr[NEQ], al[NA1], ar[NA1], pl[NP1], pr[NP1];
-#pragma unroll
-          for (int c = 0; c < NEQ; ++c) { ql[c] = sQ[c * HC + cl]; qr[c] = sQ[c * HC + cr]; }
-#pragma unroll
-          for (int c = 0; c < NAUX; ++c) { al[c] = sA[c * HC + cl]; ar[c] = sA[c * HC + cr]; }
-#pragma unroll
-          for (int c = 0; c < NPR; ++c) { pl[c] = sP[c * HC + cl]; pr[c] = sP[c * HC + cr]; }
-          R W[NW][NEQ], s[NW];
-          S::template solve<NI>(ql, qr, pl, pr, al, ar, P, W, s, fm[k], fp[k]);
-          if (ORDER == 2) {
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-#pragma unroll
-              for (int m = 0; m < NEQ; ++m) sE[(w * NEQ + m) * NEST + e] = W[w][m];
-              sE[(NW * NEQ + w) * NEST + e] = s[w];
-            }
-          }
-          if (CHECKS) {
-            bool ref = (NI == 1) ? (ei >= 0 && ei <= L.nx && ej < L.ny)
-                                 : (ei < L.nx && ej >= 0 && ej < L.ny_edges_y);
-            if (ref) {
-              R sm;
-              int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
-              if (code) {
-                unsigned long long kk = err_key(NI - 1, ei, L.j_off + ej, (code & 0xff) - 1,
-                                                code >> 8, L.nx);
-                key = kk < key ? kk : key;
-              }
-            }
-          }
+          for (int c = 0; c < NAUX; ++c) cp_async(&da[c * HC + idx], asrc + c * L.pitch);
         }
       }
-      if (ORDER == 2) {
+      cp_commit();
+    };
+
+    int buf = 0;
+    if ((int)blockIdx.x < ntiles) stage(blockIdx.x, sQb[0], sAb[0]);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
+      R* sQ = sQb[buf];
+      R* sA = sAb[buf];
+      const int i0 = (t % ntx) * TX, j0 = (t / ntx) * TY;
+      const int tn = t + gridDim.x;
+      if (tn < ntiles) { stage(tn, sQb[buf ^ 1], sAb[buf ^ 1]); cp_wait<1>(); }
+      else cp_wait<0>();
+      __syncthreads();
+
+      // ---- per-cell primitives, once per staged cell
+      if (NPR > 0) {
+        for (int idx = tid; idx < HC; idx += NT) {
+          R qc[NEQ], ac[NA1], pc[NP1];
+#pragma unroll
+          for (int c = 0; c < NEQ; ++c) qc[c] = sQ[c * HC + idx];
+#pragma unroll
+          for (int c = 0; c < NAUX; ++c) ac[c] = sA[c * HC + idx];
+          S::prims(qc, ac, P, pc);
+#pragma unroll
+          for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
+        }
         __syncthreads();
-        // limiter + correction flux on the inner edges
-        const R dtdn = (NI == 1) ? dtdx : dtdy;
+      }
+
+      R q1[KC][NEQ], dfx[KC][NEQ];
+
+      // one sweep direction: solve -> (limit) -> fluctuation/flux records in sE
+      auto sweep = [&](auto ni_tag) {
+        constexpr int NI = decltype(ni_tag)::value;
+        constexpr int NE = (NI == 1) ? NEX : NEY;
+        constexpr int KE = (NI == 1) ? KEX : KEY;
+        R fm[KE][NEQ], fp[KE][NEQ], ff[KE][NEQ];
 #pragma unroll
         for (int k = 0; k < KE; ++k) {
           const int e = tid + k * NT;
-          bool inner = false;
           if (e < NE) {
-            if (NI == 1) { const int c = e % NEXC; inner = (c >= H - 1) && (c <= TX + H - 1); }
-            else { const int r = e / TX; inner = (r >= H - 1) && (r <= TY + H - 1); }
-          }
-          if (inner) {
-            constexpr int STEP = (NI == 1) ? 1 : TX;
-            R f[NEQ];
+            int cl, cr, ei, ej;
+            if (NI == 1) {
+              const int r = e / NEXC, c = e - r * NEXC;
+              cl = (r + H) * HX + c; cr = cl + 1;
+              ei = i0 - (H - 1) + c; ej = j0 + r;
+            } else {
+              const int r = e / TX, c = e - r * TX;
+              cl = r * HX + c + H; cr = cl + HX;
+              ei = i0 + c; ej = j0 - (H - 1) + r;
+            }
+            R ql[NEQ], qr[NEQ], al[NA1], ar[NA1], pl[NP1], pr[NP1];
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-              R so = sE[(NW * NEQ + w) * NEST + e];
-              const int up = (so > (R)0) ? e - STEP : e + STEP;
-              R own[NEQ];
+            for (int c = 0; c < NEQ; ++c) { ql[c] = sQ[c * HC + cl]; qr[c] = sQ[c * HC + cr]; }
 #pragma unroll
-              for (int m = 0; m < NEQ; ++m) own[m] = sE[(w * NEQ + m) * NEST + e];
-              R dup = sE[(w * NEQ) * NEST + up] * own[0];
-              R dow = own[0] * own[0];
+            for (int c = 0; c < NAUX; ++c) { al[c] = sA[c * HC + cl]; ar[c] = sA[c * HC + cr]; }
 #pragma unroll
-              for (int m = 1; m < NEQ; ++m) {
-                dup = dup + sE[(w * NEQ + m) * NEST + up] * own[m];
-                dow = dow + own[m] * own[m];
+            for (int c = 0; c < NPR; ++c) { pl[c] = sP[c * HC + cl]; pr[c] = sP[c * HC + cr]; }
+            R W[NW][NEQ], s[NW];
+            S::template solve<NI>(ql, qr, pl, pr, al, ar, P, W, s, fm[k], fp[k]);
+            if (ORDER == 2) {
+#pragma unroll
+              for (int w = 0; w < NW; ++w) {
+#pragma unroll
+                for (int m = 0; m < NEQ; ++m) sE[(w * NEQ + m) * NEST + e] = W[w][m];
+                sE[(NW * NEQ + w) * NEST + e] = s[w];
               }
-              R th = (dow != (R)0) ? dup / dow : (R)0;
-              R ph = limiter_phi<LIM>(th);
-              R a = fabs(so);
-              R coef = a * ((R)1 - dtdn * a);
+            }
+            if (CHECKS) {
+              bool ref = (NI == 1) ? (ei >= 0 && ei <= L.nx && ej < L.ny)
+                                   : (ei < L.nx && ej >= 0 && ej < L.ny_edges_y);
+              if (ref) {
+                R sm;
+                int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+                if (code) {
+                  unsigned long long kk = err_key(NI - 1, ei, L.j_off + ej, (code & 0xff) - 1,
+                                                  code >> 8, L.nx);
+                  key = kk < key ? kk : key;
+                }
+              }
+            }
+          }
+        }
+        if (ORDER == 2) {
+          __syncthreads();
+          // limiter + correction flux on the inner edges
+          const R dtdn = (NI == 1) ? dtdx : dtdy;
+#pragma unroll
+          for (int k = 0; k < KE; ++k) {
+            const int e = tid + k * NT;
+            bool inner = false;
+            if (e < NE) {
+              if (NI == 1) { const int c = e % NEXC; inner = (c >= H - 1) && (c <= TX + H - 1); }
+              else { const int r = e / TX; inner = (r >= H - 1) && (r <= TY + H - 1); }
+            }
+            if (inner) {
+              constexpr int STEP = (NI == 1) ? 1 : TX;
+              R f[NEQ];
+#pragma unroll
+              for (int w = 0; w < NW; ++w) {
+                R so = sE[(NW * NEQ + w) * NEST + e];
+                const int up = (so > (R)0) ? e - STEP : e + STEP;
+                R own[NEQ];
+#pragma unroll
+                for (int m = 0; m < NEQ; ++m) own[m] = sE[(w * NEQ + m) * NEST + e];
+                R dup = sE[(w * NEQ) * NEST + up] * own[0];
+                R dow = own[0] * own[0];
+#pragma unroll
+                for (int m = 1; m < NEQ; ++m) {
+                  dup = dup + sE[(w * NEQ + m) * NEST + up] * own[m];
+                  dow = dow + own[m] * own[m];
+                }
+                R th = (dow != (R)0) ? dup / dow : (R)0;
+                R ph = limiter_phi<LIM>(th);
+                R a = fabs(so);
+                R coef = a * ((R)1 - dtdn * a);
+#pragma unroll
+                for (int m = 0; m < NEQ; ++m) {
+                  R wl = ph * own[m];
+                  f[m] = (w == 0) ? coef * wl : f[m] + coef * wl;
+                }
+              }
+#pragma unroll
+              for (int m = 0; m < NEQ; ++m) ff[k][m] = (R)0.5 * f[m];
+            }
+          }
+        }
+        __syncthreads();
+        // compact fluctuation (+ flux) records of the inner edges
+#pragma unroll
+        for (int k = 0; k < KE; ++k) {
+          const int e = tid + k * NT;
+          if (e < NE) {
+            int ii = -1;
+            if (NI == 1) {
+              const int r = e / NEXC, c = e - r * NEXC;
+              if (c >= H - 1 && c <= TX + H - 1) ii = r * (TX + 1) + (c - (H - 1));
+            } else {
+              const int r = e / TX, c = e - r * TX;
+              if (r >= H - 1 && r <= TY + H - 1) ii = (r - (H - 1)) * TX + c;
+            }
+            if (ii >= 0) {
 #pragma unroll
               for (int m = 0; m < NEQ; ++m) {
-                R wl = ph * own[m];
-                f[m] = (w == 0) ? coef * wl : f[m] + coef * wl;
+                sE[m * NIST + ii] = fm[k][m];
+                sE[(NEQ + m) * NIST + ii] = fp[k][m];
+                if (ORDER == 2) sE[(2 * NEQ + m) * NIST + ii] = ff[k][m];
               }
             }
+          }
+        }
+        __syncthreads();
+      };
+
+      using NX = std::integral_constant<int, 1>;
+      using NY = std::integral_constant<int, 2>;
+
+      // ---- x sweep, then the reference's x term  q1 = q - dtdx*(apdq[i] + amdq[i+1])
+      sweep(NX{});
 #pragma unroll
-            for (int m = 0; m < NEQ; ++m) ff[k][m] = (R)0.5 * f[m];
+      for (int kc = 0; kc < KC; ++kc) {
+        const int cidx = tid + kc * NT;
+        if (cidx < NCELL) {
+          const int li = cidx % TX, lr = cidx / TX;
+          const int el = lr * (TX + 1) + li, er = el + 1;
+#pragma unroll
+          for (int m = 0; m < NEQ; ++m) {
+            R qc = sQ[m * HC + (lr + H) * HX + li + H];
+            q1[kc][m] = qc - dtdx * (sE[(NEQ + m) * NIST + el] + sE[m * NIST + er]);
+            if (ORDER == 2)
+              dfx[kc][m] = sE[(2 * NEQ + m) * NIST + er] - sE[(2 * NEQ + m) * NIST + el];
           }
         }
       }
       __syncthreads();
-      // compact fluctuation (+ flux) records of the inner edges
+
+      // ---- y sweep, the y term, then the correction fluxes
+      sweep(NY{});
 #pragma unroll
-      for (int k = 0; k < KE; ++k) {
-        const int e = tid + k * NT;
-        if (e < NE) {
-          int ii = -1;
-          if (NI == 1) {
-            const int r = e / NEXC, c = e - r * NEXC;
-            if (c >= H - 1 && c <= TX + H - 1) ii = r * (TX + 1) + (c - (H - 1));
-          } else {
-            const int r = e / TX, c = e - r * TX;
-            if (r >= H - 1 && r <= TY + H - 1) ii = (r - (H - 1)) * TX + c;
-          }
-          if (ii >= 0) {
+      for (int kc = 0; kc < KC; ++kc) {
+        const int cidx = tid + kc * NT;
+        if (cidx < NCELL) {
+          const int li = cidx % TX, lr = cidx / TX;
+          const int el = lr * TX + li, eu = el + TX;
+          const int gi = i0 + li, gj = j0 + lr;
+          R out[NEQ];
 #pragma unroll
-            for (int m = 0; m < NEQ; ++m) {
-              sE[m * NIST + ii] = fm[k][m];
-              sE[(NEQ + m) * NIST + ii] = fp[k][m];
-              if (ORDER == 2) sE[(2 * NEQ + m) * NIST + ii] = ff[k][m];
+          for (int m = 0; m < NEQ; ++m) {
+            R v = q1[kc][m] - dtdy * (sE[(NEQ + m) * NIST + el] + sE[m * NIST + eu]);
+            if (ORDER == 2) {
+              v = v - dtdx * dfx[kc][m];
+              v = v - dtdy * (sE[(2 * NEQ + m) * NIST + eu] - sE[(2 * NEQ + m) * NIST + el]);
             }
+            out[m] = v;
+          }
+          if (gi < L.nx && gj < L.ny) {
+            R* dst = qn + row_off(gj, L) + gi;
+#pragma unroll
+            for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = out[m];
+          }
+          if (FUSED) {
+#pragma unroll
+            for (int m = 0; m < NEQ; ++m) sQ[m * HC + (lr + H) * HX + li + H] = out[m];
           }
         }
       }
-      __syncthreads();
-    };
-
-    using NX = std::integral_constant<int, 1>;
-    using NY = std::integral_constant<int, 2>;
-
-    // ---- x sweep, then the reference's x term  q1 = q - dtdx*(apdq[i] + amdq[i+1])
-    sweep(NX{});
-#pragma unroll
-    for (int kc = 0; kc < KC; ++kc) {
-      const int cidx = tid + kc * NT;
-      const int li = cidx % TX, lr = cidx / TX;
-      const int el = lr * (TX + 1) + li, er = el + 1;
-#pragma unroll
-      for (int m = 0; m < NEQ; ++m) {
-        R qc = sQ[m * HC + (lr + H) * HX + li + H];
-        q1[kc][m] = qc - dtdx * (sE[(NEQ + m) * NIST + el] + sE[m * NIST + er]);
-        if (ORDER == 2) dfx[kc][m] = sE[(2 * NEQ + m) * NIST + er] - sE[(2 * NEQ + m) * NIST + el];
+      if (FUSED) {
+        if (!(A.exp & 2)) __threadfence();   // q_new visible device-wide before the border counters
+        next_step_speeds<S, R, TX, TY, NT, H>(sQ, sA, sP, qn, aux, L, P, A, i0, j0, t % ntx,
+                                           t / ntx, ntx, nty, s_second, nmx, nmy, nkey);
       }
+      __syncthreads();   // sQ/sP/sE of this tile are reused two tiles later
     }
+    if (CHECKS && key != ~0ull) atomicMax(&ds->slot[A.cur][2], NKEY_MAX - key);
+  }
+
+  if (FUSED) {
+    // the next step's CFL maxima / first error go to the other slot
+    if (nkey != ~0ull) atomicMax(&ds->slot[A.cur ^ 1][2], NKEY_MAX - nkey);
+    unsigned long long bx = block_max_u64<NT>(Bits<R>::to(nmx), s_red);
     __syncthreads();
-
-    // ---- y sweep, the y term, then the correction fluxes
-    sweep(NY{});
-#pragma unroll
-    for (int kc = 0; kc < KC; ++kc) {
-      const int cidx = tid + kc * NT;
-      const int li = cidx % TX, lr = cidx / TX;
-      const int el = lr * TX + li, eu = el + TX;
-      const int gi = i0 + li, gj = j0 + lr;
-      R out[NEQ];
-#pragma unroll
-      for (int m = 0; m < NEQ; ++m) {
-        R v = q1[kc][m] - dtdy * (sE[(NEQ + m) * NIST + el] + sE[m * NIST + eu]);
-        if (ORDER == 2) {
-          v = v - dtdx * dfx[kc][m];
-          v = v - dtdy * (sE[(2 * NEQ + m) * NIST + eu] - sE[(2 * NEQ + m) * NIST + el]);
-        }
-        out[m] = v;
-      }
-      if (gi < L.nx && gj < L.ny) {
-        R* dst = qn + row_off(gj, L) + gi;
-#pragma unroll
-        for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = out[m];
-      }
+    unsigned long long by = block_max_u64<NT>(Bits<R>::to(nmy), s_red);
+    if (tid == 0) {
+      atomicMax(&ds->slot[A.cur ^ 1][0], bx);
+      atomicMax(&ds->slot[A.cur ^ 1][1], by);
     }
-    if (CHECKS && key != ~0ull) atomicMax(&ds->slot[A.cur][2], ~key);
   }
 
   // ---- last CTA commits the step

@@ -254,9 +254,10 @@ struct EulerHLLE {
     R p0 = nmax(s1, (R)0), p1 = nmax(s2, (R)0);
 #pragma unroll
     for (int m = 0; m < NEQ; ++m) {
-      R qm = (fr[m] - fl[m] - s2 * qr[m] + s1 * ql[m]) * inv;
-      W[0][m] = qm - ql[m];
-      W[1][m] = qr[m] - qm;
+      R df = fr[m] - fl[m];
+      R dq = qr[m] - ql[m];
+      W[0][m] = (df - s2 * dq) * inv;   // q_m - q_l
+      W[1][m] = (s1 * dq - df) * inv;   // q_r - q_m
       am[m] = n0 * W[0][m] + n1 * W[1][m];
       ap[m] = p0 * W[0][m] + p1 * W[1][m];
     }

@@ -1,0 +1,273 @@
+"""Row-strip domain decomposition across GPUs (north_star subsystem 4).
+
+The reference has no domain decomposition (a non-goal); the
+north star asks for row strips along j with 2-cell halos.  Each rank owns
+global rows [j0, j1) (ny/P each, the remainder to the first ranks) and runs
+one C-ABI handle on its GPU.  Per time step:
+
+  1. halo exchange — the first/last two interior rows of every component go
+     to the neighbours' ghost rows (one contiguous block each way, the SoA
+     row layout makes 2 rows x all components contiguous); with periodic y
+     and P > 1 ranks 0 and P-1 are neighbours;
+  2. ws_phase_speeds — local CFL max + admissibility key into a 3 x u64 slot;
+  3. all_reduce(slot, MAX) — speeds are non-negative IEEE bit patterns and
+     the slot stores NKEY_MAX - key, so int64 MAX gives the global max speed
+     and the globally first inadmissible interface (reference order);
+  4. ws_phase_update — every rank computes the identical dt and updates.
+
+Because the max is order independent and the update is local, an N-rank run
+is bitwise identical to the 1-GPU run (the reference's serial-twin guard,
+bench.py:181-185, becomes the 1-vs-N test).
+
+The orchestration is generic over a *shard executor*: ``CudaShard`` (the
+product: device buffers borrowed from torch, NCCL collectives) or any test
+double with the same five methods (tests use a numpy one over gloo).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+
+NKEY_MAX = (1 << 63) - 1
+
+
+@dataclass(frozen=True)
+class RowStrips:
+    """Contiguous row strips along y; remainder rows go to the first ranks."""
+
+    ny: int
+    nranks: int
+
+    def __post_init__(self):
+        if self.nranks < 1 or self.ny < 2 * self.nranks:
+            raise ValueError(f"need at least 2 rows per rank, got ny={self.ny}, "
+                             f"ranks={self.nranks}")
+
+    def bounds(self, rank: int) -> tuple[int, int]:
+        base, extra = divmod(self.ny, self.nranks)
+        j0 = rank * base + min(rank, extra)
+        return j0, j0 + base + (1 if rank < extra else 0)
+
+    def neighbours(self, rank: int, periodic: bool) -> tuple[int | None, int | None]:
+        lo = rank - 1 if rank > 0 else (self.nranks - 1 if periodic and self.nranks > 1 else None)
+        hi = rank + 1 if rank < self.nranks - 1 else (0 if periodic and self.nranks > 1 else None)
+        return lo, hi
+
+    def row_modes(self, rank: int, periodic: bool) -> tuple[int, int]:
+        """ws_rowmode of the bottom / top ghost rows of `rank`."""
+        lo, hi = self.neighbours(rank, periodic)
+        return (_abi.ROWS_MEMORY if lo is not None else _abi.ROWS_BC,
+                _abi.ROWS_MEMORY if hi is not None else _abi.ROWS_BC)
+
+
+def shard_block(global_field: np.ndarray, j0: int, j1: int) -> np.ndarray:
+    """Rows [j0-2, j1+2) of a global (ncomp, nx+4, ny+4) F-order field: the
+    shard's host block, its ghost rows being the neighbours' interior rows."""
+    return np.asfortranarray(global_field[:, :, j0:j1 + 4])
+
+
+def exchange_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=None):
+    """Send the 2 boundary rows to each neighbour, receive its rows into ghosts."""
+    lo, hi = strips.neighbours(rank, periodic)
+    send_lo, send_hi, recv_lo, recv_hi = shard.halo_views()
+    # Fixed per-peer order (NCCL matches point-to-point ops to one peer in
+    # issue order; with periodic P == 2 both neighbours are the same rank):
+    # top rows go up first (tag 1, they land in the upper neighbour's recv_lo),
+    # then bottom rows go down (tag 2, into the lower neighbour's recv_hi).
+    ops = []
+    if hi is not None:
+        ops.append(dist.P2POp(dist.isend, send_hi, hi, group=group, tag=1))
+    if lo is not None:
+        ops.append(dist.P2POp(dist.isend, send_lo, lo, group=group, tag=2))
+    if lo is not None:
+        ops.append(dist.P2POp(dist.irecv, recv_lo, lo, group=group, tag=1))
+    if hi is not None:
+        ops.append(dist.P2POp(dist.irecv, recv_hi, hi, group=group, tag=2))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    shard.halo_received()
+
+
+def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl, group=None):
+    """One globally consistent time step (halo, speeds, MAX all-reduce, update)."""
+    exchange_halos(dist, shard, strips, rank, periodic, group)
+    shard.phase_speeds()
+    slot = shard.slot_view()
+    dist.all_reduce(slot, op=dist.ReduceOp.MAX, group=group)
+    shard.slot_reduced()
+    shard.phase_update(ctl)
+
+
+def decode_slot(slot_words) -> tuple[float, float, int | None]:
+    """(max_sx, max_sy, first error key or None) from the 3 reduced words."""
+    bx, by, nk = (int(w) & ((1 << 64) - 1) for w in slot_words)
+    sx = np.array([bx], dtype=np.uint64).view(np.float64)[0]
+    sy = np.array([by], dtype=np.uint64).view(np.float64)[0]
+    return float(sx), float(sy), (None if nk == 0 else NKEY_MAX - nk)
+
+
+# ---------------------------------------------------------------------------
+# the product executor: one GPU shard, buffers owned by torch
+
+class CudaShard:
+    """DeviceGrid shard whose state/aux/slot buffers are torch tensors, so the
+    halo rows and the reduction slot can be handed to torch.distributed
+    (NCCL) without copies."""
+
+    def __init__(self, case, strips: RowStrips, rank: int, device, periodic_y: bool,
+                 precision: str = "f64"):
+        import torch
+
+        from .device import DeviceGrid
+        from .kernels import make_kernel
+        self.torch = torch
+        j0, j1 = strips.bounds(rank)
+        self.j0, self.j1 = j0, j1
+        self.ny = j1 - j0
+        lo_mode, hi_mode = strips.row_modes(rank, periodic_y)
+        kernel = make_kernel(case.kernel, **case.kernel_params)
+        desc = _abi.WsDesc()
+        desc.nx, desc.ny, desc.dx, desc.dy, desc.num_ghost = case.nx, self.ny, case.dx, case.dy, 2
+        desc.solver = _abi.SOLVER_IDS[case.kernel]
+        desc.order = case.order
+        desc.limiter = _abi.LIMITER_IDS[case.limiter]
+        desc.bc_x = desc.bc_y = _abi.BC_IDS[case.bc]
+        desc.precision = _abi.PRECISION_IDS[precision]
+        desc.ny_global, desc.j_offset = strips.ny, j0
+        desc.rows_lo, desc.rows_hi = lo_mode, hi_mode
+        import ctypes
+        qb, ab, sb = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _abi.check(_abi.lib().ws_buffer_bytes(ctypes.byref(desc), ctypes.byref(qb),
+                                              ctypes.byref(ab), ctypes.byref(sb)))
+        u8 = dict(dtype=torch.uint8, device=device)
+        self.bufs = [torch.zeros(qb.value, **u8), torch.zeros(qb.value, **u8)]
+        self.aux_buf = torch.zeros(max(ab.value, 8), **u8)
+        self.slots = torch.zeros((sb.value + 7) // 8 * 8, **u8)
+        self.grid = DeviceGrid(case.nx, self.ny, case.dx, case.dy, kernel, order=case.order,
+                               limiter=case.limiter, bc_x=case.bc, bc_y=case.bc,
+                               precision=precision, device=device.index or 0,
+                               ny_global=strips.ny, j_offset=j0, rows_lo=lo_mode,
+                               rows_hi=hi_mode,
+                               buffers={"q0": self.bufs[0].data_ptr(),
+                                        "q1": self.bufs[1].data_ptr(),
+                                        "aux": self.aux_buf.data_ptr() if ab.value else None,
+                                        "slots": self.slots.data_ptr()})
+        self.stream = torch.cuda.current_stream(device).cuda_stream
+
+    def _current(self):
+        ptr, pitch, row = self.grid.state_ptr()
+        buf = self.bufs[0] if ptr == self.bufs[0].data_ptr() else self.bufs[1]
+        return buf, row * (8 if self.grid.precision == "f64" else 4)
+
+    def halo_views(self):
+        buf, rbytes = self._current()
+        n = self.ny
+        return (buf[2 * rbytes:4 * rbytes], buf[n * rbytes:(n + 2) * rbytes],
+                buf[0:2 * rbytes], buf[(n + 2) * rbytes:(n + 4) * rbytes])
+
+    def halo_received(self):
+        pass
+
+    def phase_speeds(self):
+        self.grid.phase_speeds(stream=self.stream)
+
+    def slot_view(self):
+        off = self.grid.slot_ptr() - self.slots.data_ptr()
+        return self.slots[off:off + 24].view(self.torch.int64)
+
+    def slot_reduced(self):
+        pass
+
+    def phase_update(self, ctl):
+        self.grid.phase_update(ctl, stream=self.stream)
+
+
+# ---------------------------------------------------------------------------
+# bench.py --gpus N (torchrun): weak scaling of the C2 workload
+
+def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_fn, METRIC, UNIT):
+    import torch
+    import torch.distributed as dist
+
+    from . import configs
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    base = build_case(args.config, precision=args.precision)
+    prec = base.dtype
+    # weak scaling: the per-GPU strip is the 1-GPU workload; strips stack along y
+    ny_g = base.ny * world
+    strips = RowStrips(ny_g, world)
+    j0, j1 = strips.bounds(rank)
+    glob = np.zeros((base.q.shape[0], base.nx + 4, ny_g + 4), order="F")
+    for k in range(world):
+        glob[:, :, 2 + k * base.ny:2 + (k + 1) * base.ny] = base.q[:, :, 2:-2]
+    case = base
+    periodic = base.bc == "periodic"
+    shard = CudaShard(case, strips, rank, dev, periodic, prec)
+    npdt = np.float64 if prec == "f64" else np.float32
+    shard.grid.upload(np.asfortranarray(shard_block(glob, j0, j1), dtype=npdt),
+                      stream=shard.stream)
+    ctl = _abi.make_ctl(case.cfl)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        sharded_step(dist, shard, strips, rank, periodic, ctl)
+    torch.cuda.synchronize()
+    res = shard.grid.poll()
+    shard.grid.raise_for(res.error)
+    k = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(k)]
+    l0 = shard.grid.launches()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(k):
+            flush.zero_()
+            evs[i][0].record()
+            sharded_step(dist, shard, strips, rank, periodic, ctl)
+            evs[i][1].record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    res = shard.grid.poll()
+    shard.grid.raise_for(res.error)
+    launches = shard.grid.launches() - l0
+    cells = case.nx * ny_g
+    value = cells * k / (ms_max / 1e3)
+    if rank == 0:
+        peak, kind = peak_fn()
+        bpc = configs.bytes_per_cell(case.kernel, prec)
+        achieved = cells / world * bpc / (ms_max / k / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k,
+            "warmup": args.warmup, "ms_per_step": ms_max / k, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "config": {"workload": f"{case.name} x{world} strips (weak)", "kernel": case.kernel,
+                       "nx": case.nx, "ny": ny_g, "limiter": case.limiter, "order": case.order,
+                       "cfl": case.cfl, "parallelism": f"row-strips{world}",
+                       "l2": "flushed between timed steps (512 MiB write)",
+                       "timed_step": "halo exchange + CFL pre-pass + MAX all-reduce + update"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "whole step",
+                         "peak_kind": kind},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    shard.grid.close()
+    dist.destroy_process_group()
+    return 0

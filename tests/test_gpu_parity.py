@@ -50,6 +50,15 @@ def test_second_order_periodic_bitwise(name):
     _compare(name, 40, 33, 4, 2, "mc", ("periodic", "periodic"), seed=2)
 
 
+@pytest.mark.parametrize("name,bc", [("shallow-water-roe", "periodic"),
+                                     ("euler-hlle", "extrapolate"), ("euler", "periodic")])
+def test_many_tiles_bitwise(name, bc):
+    # several tile rows/columns, partial edge tiles, periodic wrap borders: the
+    # fused next-step CFL epilogue (shared-border counters) must give every dt
+    _compare(name, 131, 75, 6, 2, "mc", (bc, bc), seed=9)
+    _compare(name, 131, 75, 6, 2, "mc", (bc, bc), seed=9, use_run=True)
+
+
 @pytest.mark.parametrize("name", ["shallow-water-roe", "acoustics-const"])
 def test_graph_run_equals_steps(name):
     _compare(name, 64, 48, 9, 2, "mc", ("extrapolate", "extrapolate"), seed=3, use_run=True)
