@@ -286,6 +286,11 @@ def gpu_arm(args):
             pass
 
     # whole simulation, device resident: the configured number of steps via graphs
+    # (one untimed run first so graph capture/instantiation is not timed)
+    g.upload(host_q, host_aux, stream=sp)
+    g.run(min(case.steps, 8), ctl, stream=sp)
+    torch.cuda.synchronize()
+    g.poll()
     g.upload(host_q, host_aux, stream=sp)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -14,16 +14,16 @@ import sys
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-SRC = HERE / "csrc" / "wavestep.cu"
+CSRC = HERE / "csrc"
+SOURCES = [CSRC / "wavestep.cu"] + sorted(CSRC.glob("ws_inst_*.cu"))
 OUT = HERE / "_lib" / "libwavestep.so"
-DEPS = [SRC, HERE / "csrc" / "ws_common.cuh", HERE / "csrc" / "ws_solvers.cuh",
-        HERE / "csrc" / "ws_kernels.cuh", HERE.parent / "include" / "wavestep.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [HERE.parent / "include" / "wavestep.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "--fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -42,17 +42,39 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every translation unit (in parallel) and link libwavestep.so."""
     if not force and up_to_date():
         return OUT
+    from concurrent.futures import ThreadPoolExecutor
     OUT.parent.mkdir(parents=True, exist_ok=True)
+    objdir = OUT.parent / "obj"
+    objdir.mkdir(exist_ok=True)
+    log = OUT.parent / "build.log"
+
+    def compile_one(src: Path):
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, "-Xptxas", "-v", "-c", "-o", str(obj), str(src)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, res
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    text = []
+    for src, obj, cmd, res in results:
+        text.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        if res.returncode != 0:
+            log.write_text("\n".join(text))
+            sys.stderr.write(res.stderr[-4000:])
+            raise RuntimeError(f"nvcc failed on {src.name} ({res.returncode}); see {log}")
     tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-Xptxas", "-v", "-o", str(tmp), str(SRC)]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = HERE / "_lib" / "build.log"
-    log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+            "-Xcompiler", "-fPIC", "-o", str(tmp)] + [str(r[1]) for r in results]
+    res = subprocess.run(link, capture_output=True, text=True)
+    text.append(" ".join(link) + "\n" + res.stdout + res.stderr)
+    log.write_text("\n".join(text))
     if res.returncode != 0:
         sys.stderr.write(res.stderr[-4000:])
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+        raise RuntimeError(f"link failed ({res.returncode}); see {log}")
     os.replace(tmp, OUT)
     if verbose:
         print(f"built {OUT}")

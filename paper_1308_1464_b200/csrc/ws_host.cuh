@@ -1,0 +1,348 @@
+// ws_host.cuh — host-side launch machinery shared by the C-ABI translation
+// unit (wavestep.cu) and the per-solver instantiation units (ws_inst_*.cu).
+#pragma once
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/wavestep.h"
+#include "ws_kernels.cuh"
+
+using namespace ws;
+
+struct ws_handle;
+
+namespace wsh {
+
+template <class S, class R, int ORDER> struct TileCfg {
+  static constexpr int TX = 32, TY = 16, NT = 256;
+};
+// Euler-Roe's 15-value wave record would cap residency at 1 CTA/SM at 32x16
+template <class R> struct TileCfg<EulerRoe, R, 2> {
+  static constexpr int TX = 32, TY = 8, NT = 256;
+};
+constexpr int SPD_TX = 32, SPD_TY = 16, SPD_NT = 256;
+
+struct Ops {
+  void (*speeds)(ws_handle*, const void* q, int cur, cudaStream_t);
+  void (*update)(ws_handle*, const void* q, void* qn, const StepArgs&, cudaStream_t);
+  void (*to_soa)(ws_handle*, const void* stage, void* dst, int ncomp, cudaStream_t);
+  void (*to_aos)(ws_handle*, const void* cur, const void* gsrc, void* stage, cudaStream_t);
+  void (*static_speed)(ws_handle*, cudaStream_t);
+  void (*prepare)();   // one-time kernel attributes (never inside a capture)
+  int static_speeds;   // solver has q-independent speeds
+};
+
+}  // namespace wsh
+
+struct ws_handle {
+  using Ops = wsh::Ops;
+  ws_desc d{};
+  int neq = 0, naux = 0;
+  size_t esz = 8;
+  Layout L{};
+  void* q[2] = {nullptr, nullptr};
+  void* aux = nullptr;
+  DevState* ds = nullptr;
+  bool own_q[2] = {false, false}, own_aux = false, own_ds = false;
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t last_stream = nullptr;
+  long long enq = 0;            // steps enqueued since upload (== committed after a poll)
+  long long nrep_seen = 0;
+  bool multi = false;           // row-strip shard with memory ghost rows
+  bool uploaded = false;
+  double host_static[2] = {0, 0};
+  Ops ops{};
+  std::vector<char> params;     // typed Params<R> blob
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  ws_ctl gctl{};
+  cudaStream_t gstream = nullptr;
+  long long launches = 0;
+  int variant = 0;              // WS_TILE experiment selector (0 = default tiles)
+  bool fused = false;           // next-step CFL maxima computed in the update epilogue
+  bool need_prepass = true;     // fused mode: slot of the current state not yet filled
+  int* borders = nullptr;       // tile-border counters of the fused epilogue
+  int exp = 0;                  // WS_EXP timing-study switches
+  bool line_kernel = true;      // warp-per-line k_update_w (else the smem-tile k_update)
+  size_t border_bytes = 0;
+  std::string err;
+};
+
+namespace wsh {
+
+// defined in wavestep.cu (per-handle message, or the thread's create error)
+int fail(ws_handle* h, int code, const std::string& msg);
+
+inline int cuda_fail(ws_handle* h, cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  return fail(h, WS_ERR_CUDA, m);
+}
+
+#define WS_CUDA(h, call)                                   \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_fail((h), e_, #call); \
+  } while (0)
+
+inline cudaStream_t pick(ws_handle* h, void* s) {
+  cudaStream_t st = s ? reinterpret_cast<cudaStream_t>(s) : h->stream;
+  h->last_stream = st;
+  return st;
+}
+
+// persistent grid: resident CTAs (occupancy query, cached per kernel), capped
+// by the tile count
+template <class K>
+int persistent_grid(K kernel, int nt, size_t smem, int nx, int ny, int tx, int ty) {
+  static std::unordered_map<const void*, int> cache;   // resident CTAs per SM, per kernel
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  auto it = cache.find((const void*)kernel);
+  int per_sm;
+  if (it == cache.end()) {
+    per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem);
+    if (per_sm < 1) per_sm = 1;
+    cache[(const void*)kernel] = per_sm;
+  } else {
+    per_sm = it->second;
+  }
+  const long long tiles = (long long)((nx + tx - 1) / tx) * ((ny + ty - 1) / ty);
+  const long long g = (long long)per_sm * sms;
+  return (int)(tiles < g ? tiles : g);
+}
+
+// ---- tile-shape experiments (WS_TILE=k selects variant k; SW fp64 order 2 MC)
+template <class S, class R, int ORDER, int LIM, int TX, int TY, int NT>
+void launch_variant(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
+  using G = TileGeom<S, ORDER, TX, TY>;
+  const size_t smem = G::template smem_bytes<R>();
+  auto go = [&](auto k) {
+    static bool done = false;
+    if (!done) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); done = true; }
+    dim3 grid(persistent_grid(k, NT, smem, h->L.nx, h->L.ny, TX, TY));
+    k<<<grid, NT, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
+                              static_cast<R*>(qn), h->L,
+                              *reinterpret_cast<const typename S::template Params<R>*>(h->params.data()),
+                              a, h->ds);
+  };
+  if (h->fused) go(k_update<S, R, ORDER, LIM, TX, TY, NT, false, true>);
+  else go(k_update<S, R, ORDER, LIM, TX, TY, NT, false, false>);
+  h->launches++;
+}
+
+template <class S, class R, int ORDER, int LIM>
+bool variant_update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
+  if constexpr (std::is_same<S, ShallowRoe>::value && std::is_same<R, double>::value &&
+                ORDER == 2 && LIM == LIM_MC) {
+    switch (h->variant) {
+      case 1: launch_variant<S, R, 2, LIM_MC, 32, 8, 256>(h, q, qn, a, st); return true;
+      case 2: launch_variant<S, R, 2, LIM_MC, 32, 13, 256>(h, q, qn, a, st); return true;
+      case 3: launch_variant<S, R, 2, LIM_MC, 64, 8, 256>(h, q, qn, a, st); return true;
+      case 4: launch_variant<S, R, 2, LIM_MC, 32, 16, 128>(h, q, qn, a, st); return true;
+      case 5: launch_variant<S, R, 2, LIM_MC, 16, 16, 256>(h, q, qn, a, st); return true;
+      case 6: launch_variant<S, R, 2, LIM_MC, 32, 8, 128>(h, q, qn, a, st); return true;
+      case 7: launch_variant<S, R, 2, LIM_MC, 64, 6, 256>(h, q, qn, a, st); return true;
+      case 8: launch_variant<S, R, 2, LIM_MC, 32, 12, 192>(h, q, qn, a, st); return true;
+      default: return false;
+    }
+  }
+  return false;
+}
+
+// ---- typed launchers -----------------------------------------------------
+template <class S, class R, int ORDER, int LIM> struct Impl {
+  using P = typename S::template Params<R>;
+  using C = TileCfg<S, R, ORDER>;
+  using G = TileGeom<S, ORDER, C::TX, C::TY>;
+
+  static const P& prm(ws_handle* h) { return *reinterpret_cast<const P*>(h->params.data()); }
+
+  static void speeds(ws_handle* h, const void* q, int cur, cudaStream_t st) {
+    dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + SPD_TY - 1) / SPD_TY);
+    k_speeds<S, R, SPD_TX, SPD_TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(
+        static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
+    h->launches++;
+  }
+
+  template <bool CHECKS, bool FUSED> static auto kern() {
+    return k_update<S, R, ORDER, LIM, C::TX, C::TY, C::NT, CHECKS, FUSED>;
+  }
+
+  static void prepare() {
+    const int lsmem = (int)LineGeom<S>::template smem_bytes<R>();
+    cudaFuncSetAttribute(kern_w<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+    cudaFuncSetAttribute(kern_w<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+    const int smem = (int)G::template smem_bytes<R>();
+    cudaFuncSetAttribute(kern<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern<false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+
+  template <bool CHECKS, bool FUSED> static void update_t(ws_handle* h, const void* q, void* qn,
+                                                          const StepArgs& a, cudaStream_t st) {
+    auto k = kern<CHECKS, FUSED>();
+    const size_t smem = G::template smem_bytes<R>();
+    dim3 grid(persistent_grid(k, C::NT, smem, h->L.nx, h->L.ny, C::TX, C::TY));
+    k<<<grid, C::NT, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
+                                 static_cast<R*>(qn), h->L, prm(h), a, h->ds);
+    h->launches++;
+  }
+
+  static constexpr int LNW = 10;  // warps per CTA of the warp-line kernel (29 lines / 10 ~ 97%)
+  template <bool CHECKS> static auto kern_w() {
+    return k_update_w<S, R, ORDER, LIM, LNW, CHECKS>;
+  }
+  template <bool CHECKS> static void update_w(ws_handle* h, const void* q, void* qn,
+                                              const StepArgs& a, cudaStream_t st) {
+    auto k = kern_w<CHECKS>();
+    const size_t smem = LineGeom<S>::template smem_bytes<R>();
+    dim3 grid((h->L.nx + 28) / 29, (h->L.ny + 28) / 29);
+    k<<<grid, LNW * 32, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
+                                    static_cast<R*>(qn), h->L, prm(h), a, h->ds);
+    h->launches++;
+  }
+
+  static void update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
+    if (h->variant > 0 && variant_update<S, R, ORDER, LIM>(h, q, qn, a, st)) return;
+    if (h->line_kernel && !h->fused) {
+      if (S::STATIC_SPEEDS && !h->multi) update_w<true>(h, q, qn, a, st);
+      else update_w<false>(h, q, qn, a, st);
+      return;
+    }
+    if (S::STATIC_SPEEDS && !h->multi) update_t<true, false>(h, q, qn, a, st);
+    else if (h->fused) update_t<false, true>(h, q, qn, a, st);
+    else update_t<false, false>(h, q, qn, a, st);
+  }
+
+  static void to_soa(ws_handle* h, const void* stage, void* dst, int ncomp, cudaStream_t st) {
+    int blocks = 148 * 8;
+    k_to_soa<R, R><<<blocks, 256, 0, st>>>(static_cast<const R*>(stage), static_cast<R*>(dst),
+                                           ncomp, h->L.nx, h->L.ny, h->L.pitch);
+    h->launches++;
+  }
+
+  static void to_aos(ws_handle* h, const void* cur, const void* gsrc, void* stage,
+                     cudaStream_t st) {
+    int blocks = 148 * 8;
+    k_to_aos<R, R><<<blocks, 256, 0, st>>>(static_cast<const R*>(cur),
+                                           static_cast<const R*>(gsrc), static_cast<R*>(stage),
+                                           h->L, h->neq);
+    h->launches++;
+  }
+
+  static void static_speed(ws_handle* h, cudaStream_t st) {
+    if (S::NAUX > 0) {
+      k_static_speed<R><<<148 * 4, 256, 0, st>>>(static_cast<const R*>(h->aux), h->L, h->ds);
+      h->launches++;
+    }
+  }
+
+  static Ops ops() {
+    Ops o;
+    o.speeds = &speeds;
+    o.update = &update;
+    o.to_soa = &to_soa;
+    o.to_aos = &to_aos;
+    o.static_speed = &static_speed;
+    o.prepare = &prepare;
+    o.static_speeds = S::STATIC_SPEEDS ? 1 : 0;
+    return o;
+  }
+};
+
+template <class S, class R> Ops pick_lim(int order, int lim) {
+  if (order == 1 || lim == LIM_NONE) return Impl<S, R, 1, LIM_NONE>::ops();
+  switch (lim) {
+    case LIM_MINMOD: return Impl<S, R, 2, LIM_MINMOD>::ops();
+    case LIM_SUPERBEE: return Impl<S, R, 2, LIM_SUPERBEE>::ops();
+    default: return Impl<S, R, 2, LIM_MC>::ops();
+  }
+}
+
+// per-solver factories, one translation unit each (ws_inst_*.cu), so the
+// heavy template instantiations compile in parallel
+Ops ops_acoustics_const(int prec, int order, int lim);
+Ops ops_acoustics_var(int prec, int order, int lim);
+Ops ops_euler_roe(int prec, int order, int lim);
+Ops ops_euler_hlle(int prec, int order, int lim);
+Ops ops_shallow_roe(int prec, int order, int lim);
+
+// batched pointwise plugin call (ws_riemann), fp64
+int riemann_acoustics_const(const double* p, int dir, long long n, const double* ql,
+                            const double* qr, const double* al, const double* ar, double* w,
+                            double* s, double* am, double* ap, int* codes);
+int riemann_acoustics_var(const double* p, int dir, long long n, const double* ql,
+                          const double* qr, const double* al, const double* ar, double* w,
+                          double* s, double* am, double* ap, int* codes);
+int riemann_euler_roe(const double* p, int dir, long long n, const double* ql, const double* qr,
+                      const double* al, const double* ar, double* w, double* s, double* am,
+                      double* ap, int* codes);
+int riemann_euler_hlle(const double* p, int dir, long long n, const double* ql,
+                       const double* qr, const double* al, const double* ar, double* w,
+                       double* s, double* am, double* ap, int* codes);
+int riemann_shallow_roe(const double* p, int dir, long long n, const double* ql,
+                        const double* qr, const double* al, const double* ar, double* w,
+                        double* s, double* am, double* ap, int* codes);
+
+template <class S>
+int riemann_t(const typename S::template Params<double>& P, int dir, long long n,
+              const double* ql, const double* qr, const double* al, const double* ar,
+              double* waves, double* speeds, double* amdq, double* apdq, int* codes) {
+  constexpr int NEQ = S::NEQ, NW = S::NW, NAUX = S::NAUX;
+  if (NAUX > 0 && (!al || !ar)) return fail(nullptr, WS_ERR_CONFIG, "this solver needs aux data");
+  const size_t b = sizeof(double) * (size_t)n;
+  double *dql, *dqr, *dal = nullptr, *dar = nullptr, *dw, *ds, *dm, *dp;
+  int* dc;
+  cudaError_t e;
+  std::vector<void*> bufs;
+  auto alloc = [&](void** p, size_t bytes) {
+    e = cudaMalloc(p, bytes > 0 ? bytes : 8);
+    if (e == cudaSuccess) bufs.push_back(*p);
+    return e == cudaSuccess;
+  };
+  auto cleanup = [&]() { for (void* p : bufs) cudaFree(p); };
+  bool ok = alloc((void**)&dql, b * NEQ) && alloc((void**)&dqr, b * NEQ) &&
+            alloc((void**)&dw, b * NW * NEQ) && alloc((void**)&ds, b * NW) &&
+            alloc((void**)&dm, b * NEQ) && alloc((void**)&dp, b * NEQ) &&
+            alloc((void**)&dc, sizeof(int) * (size_t)(n > 0 ? n : 1));
+  if (ok && NAUX > 0) ok = alloc((void**)&dal, b * NAUX) && alloc((void**)&dar, b * NAUX);
+  if (!ok) { cleanup(); return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e)); }
+  cudaMemcpy(dql, ql, b * NEQ, cudaMemcpyHostToDevice);
+  cudaMemcpy(dqr, qr, b * NEQ, cudaMemcpyHostToDevice);
+  if (NAUX > 0) {
+    cudaMemcpy(dal, al, b * NAUX, cudaMemcpyHostToDevice);
+    cudaMemcpy(dar, ar, b * NAUX, cudaMemcpyHostToDevice);
+  }
+  if (n > 0) {
+    const int blocks = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+    if (dir == 0)
+      k_riemann<S, double, 1><<<blocks, 256>>>(P, n, dql, dqr, dal, dar, dw, ds, dm, dp, dc);
+    else
+      k_riemann<S, double, 2><<<blocks, 256>>>(P, n, dql, dqr, dal, dar, dw, ds, dm, dp, dc);
+  }
+  e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(waves, dw, b * NW * NEQ, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(speeds, ds, b * NW, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(amdq, dm, b * NEQ, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(apdq, dp, b * NEQ, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(codes, dc, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e != cudaSuccess) return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+  return WS_OK;
+}
+
+
+}  // namespace wsh

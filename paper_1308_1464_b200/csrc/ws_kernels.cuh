@@ -46,17 +46,24 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 }
 
 // --------------------------------------------------------------------------
-// CFL / admissibility pre-pass
-template <class S, class R, int TX, int TY>
-__global__ void __launch_bounds__(TX * TY)
+// CFL / admissibility pre-pass.  Tile of TX x TY "edge cells" (x-edge = left
+// edge of the cell, y-edge = bottom edge, plus the domain's last column/row),
+// NT threads, each TX*TY/NT cells.  Per-cell admissibility (finite, positive)
+// is evaluated once per cell while staging; a tile whose cells all pass uses
+// the check-free probe (only the pairwise Roe c^2 test remains).
+template <class S, class R, int TX, int TY, int NT>
+__global__ void __launch_bounds__(NT)
 k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
          const typename S::template Params<R> P, const int cur, DevState* __restrict__ ds) {
-  constexpr int NT = TX * TY, NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int HX = TX + 1, HY = TY + 1, HC = HX * HY;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  constexpr int KC = TX * TY / NT;
+  static_assert(KC * NT == TX * TY, "tile must be a multiple of the block");
   __shared__ R sQ[NEQ][HC];
-  __shared__ R sA[NAUX > 0 ? NAUX : 1][HC];
-  __shared__ R sP[NPR > 0 ? NPR : 1][HC];
-  __shared__ unsigned long long sred[NT / 32];
+  __shared__ R sA[NA1][HC];
+  __shared__ R sP[NP1][HC];
+  __shared__ unsigned long long sred[2][NT / 32];
   __shared__ int s_skip;
   const int tid = threadIdx.x;
   // one L2 read per CTA (the flags cannot change during this kernel: only the
@@ -66,10 +73,13 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   if (s_skip) return;
   const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
   // tile cell (lx, ly) = cell (i0 - 1 + lx, j0 - 1 + ly)
+  const bool inner = i0 >= 1 && i0 + TX <= L.nx && j0 >= 1 && j0 + TY <= L.ny;
+  bool ok = true;
   for (int idx = tid; idx < HC; idx += NT) {
-    int lx = idx % HX, ly = idx / HX;
-    int gi = map_i(i0 - 1 + lx, L), gj = map_j(j0 - 1 + ly, L);
-    R qc[NEQ], ac[NAUX > 0 ? NAUX : 1], pc[NPR > 0 ? NPR : 1];
+    const int lx = idx % HX, ly = idx / HX;
+    int gi = i0 - 1 + lx, gj = j0 - 1 + ly;
+    if (!inner) { gi = map_i(gi, L); gj = map_j(gj, L); }
+    R qc[NEQ], ac[NA1], pc[NP1];
     const R* src = q + row_off(gj, L) + gi;
 #pragma unroll
     for (int c = 0; c < NEQ; ++c) { qc[c] = src[c * L.pitch]; sQ[c][idx] = qc[c]; }
@@ -83,17 +93,15 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
 #pragma unroll
       for (int c = 0; c < NPR; ++c) sP[c][idx] = pc[c];
     }
+    ok = ok && S::cell_ok(qc, ac, pc, P);
   }
-  __syncthreads();
+  const bool clean = __syncthreads_and(ok);
 
-  const int li = tid % TX, lj = tid / TX;
-  const int i = i0 + li, j = j0 + lj;
   R mx = (R)0, my = (R)0;
   unsigned long long key = ~0ull;
   auto edge = [&](auto ni_tag, int cl, int cr, int dir, int ei, int ej) {
     constexpr int NI = decltype(ni_tag)::value;
-    R ql[NEQ], qr[NEQ], al[NAUX > 0 ? NAUX : 1], ar[NAUX > 0 ? NAUX : 1];
-    R pl[NPR > 0 ? NPR : 1], pr[NPR > 0 ? NPR : 1];
+    R ql[NEQ], qr[NEQ], al[NA1], ar[NA1], pl[NP1], pr[NP1];
 #pragma unroll
     for (int c = 0; c < NEQ; ++c) { ql[c] = sQ[c][cl]; qr[c] = sQ[c][cr]; }
 #pragma unroll
@@ -101,7 +109,8 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
 #pragma unroll
     for (int c = 0; c < NPR; ++c) { pl[c] = sP[c][cl]; pr[c] = sP[c][cr]; }
     R sm;
-    int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+    int code = clean ? S::template probe_fast<NI>(ql, qr, pl, pr, al, ar, P, sm)
+                     : S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
     if (code) {
       unsigned long long k = err_key(dir, ei, L.j_off + ej, (code & 0xff) - 1, code >> 8, L.nx);
       key = k < key ? k : key;
@@ -110,19 +119,39 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   };
   using NX = std::integral_constant<int, 1>;
   using NY = std::integral_constant<int, 2>;
-  if (i <= L.nx && j < L.ny) {
-    R s = edge(NX{}, (lj + 1) * HX + li, (lj + 1) * HX + li + 1, 0, i, j);
-    mx = nmax(mx, s);   // NaN-free unless inadmissible (flagged)
-  }
-  if (i < L.nx && j < L.ny_edges_y) {
-    R s = edge(NY{}, lj * HX + li + 1, (lj + 1) * HX + li + 1, 1, i, j);
-    my = nmax(my, s);
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const int cidx = tid + kc * NT;
+    const int li = cidx % TX, lj = cidx / TX;
+    const int i = i0 + li, j = j0 + lj;
+    if (i <= L.nx && j < L.ny) {
+      R s = edge(NX{}, (lj + 1) * HX + li, (lj + 1) * HX + li + 1, 0, i, j);
+      mx = nmax(mx, s);   // NaN-free unless inadmissible (flagged)
+    }
+    if (i < L.nx && j < L.ny_edges_y) {
+      R s = edge(NY{}, lj * HX + li + 1, (lj + 1) * HX + li + 1, 1, i, j);
+      my = nmax(my, s);
+    }
   }
   if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
-  unsigned long long bx = block_max_u64<NT>(Bits<R>::to(mx), sred);
+  // both maxima in one warp-shuffle tree
+  unsigned long long bx = Bits<R>::to(mx), by = Bits<R>::to(my);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long wx = __shfl_xor_sync(0xffffffffu, bx, o);
+    unsigned long long wy = __shfl_xor_sync(0xffffffffu, by, o);
+    bx = wx > bx ? wx : bx;
+    by = wy > by ? wy : by;
+  }
+  const int lane = tid & 31, wid = tid >> 5;
+  if (lane == 0) { sred[0][wid] = bx; sred[1][wid] = by; }
   __syncthreads();
-  unsigned long long by = block_max_u64<NT>(Bits<R>::to(my), sred);
   if (tid == 0) {
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) {
+      bx = sred[0][w] > bx ? sred[0][w] : bx;
+      by = sred[1][w] > by ? sred[1][w] : by;
+    }
     atomicMax(&ds->slot[cur][0], bx);
     atomicMax(&ds->slot[cur][1], by);
   }
@@ -647,6 +676,216 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
   }
 }
 
+// one edge per lane of a grid line (see k_update_w): solve, optional
+// admissibility probe, wave limiter against lane +-1 (register shuffles),
+// correction flux; returns this lane's apdq / flux and the next lane's
+// amdq / flux (the right edge of the lane's cell)
+template <class S, class R, int ORDER, int LIM, bool CHECKS, int NI, int HC>
+__device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
+                                          const typename S::template Params<R>& P,
+                                          const Layout& L, int cl, int cr, int ei, int ej,
+                                          bool ref, R dtdn, unsigned long long& key,
+                                          R* ap, R* amn, R* fl, R* fr) {
+  constexpr int NEQ = S::NEQ, NW = S::NW, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  constexpr unsigned FULL = 0xffffffffu;
+  R ql[NEQ], qr[NEQ], al[NA1], ar[NA1], pl[NP1], pr[NP1];
+#pragma unroll
+  for (int c = 0; c < NEQ; ++c) { ql[c] = sQ[c * HC + cl]; qr[c] = sQ[c * HC + cr]; }
+#pragma unroll
+  for (int c = 0; c < NAUX; ++c) { al[c] = sA[c * HC + cl]; ar[c] = sA[c * HC + cr]; }
+#pragma unroll
+  for (int c = 0; c < NPR; ++c) { pl[c] = sP[c * HC + cl]; pr[c] = sP[c * HC + cr]; }
+  R W[NW][NEQ], s[NW], am[NEQ], apl[NEQ];
+  S::template solve<NI>(ql, qr, pl, pr, al, ar, P, W, s, am, apl);
+  if (CHECKS && ref) {
+    R sm;
+    int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+    if (code) {
+      unsigned long long kk = err_key(NI - 1, ei, L.j_off + ej, (code & 0xff) - 1, code >> 8,
+                                      L.nx);
+      key = kk < key ? kk : key;
+    }
+  }
+  R f[NEQ];
+#pragma unroll
+  for (int m = 0; m < NEQ; ++m) f[m] = (R)0;
+  if (ORDER == 2) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      R dup = (R)0, dow = (R)0;
+      // upwind edge: lane-1 if s > 0 else lane+1 (one indexed shuffle per value)
+      const int src = (s[w] > (R)0) ? (int)(threadIdx.x & 31) - 1 : (int)(threadIdx.x & 31) + 1;
+#pragma unroll
+      for (int m = 0; m < NEQ; ++m) {
+        const R up = __shfl_sync(FULL, W[w][m], src & 31);
+        dup = (m == 0) ? up * W[w][m] : dup + up * W[w][m];
+        dow = (m == 0) ? W[w][m] * W[w][m] : dow + W[w][m] * W[w][m];
+      }
+      R th = (dow != (R)0) ? dup / dow : (R)0;
+      R ph = limiter_phi<LIM>(th);
+      R a = fabs(s[w]);
+      R coef = a * ((R)1 - dtdn * a);
+#pragma unroll
+      for (int m = 0; m < NEQ; ++m) {
+        R wl = ph * W[w][m];
+        f[m] = (w == 0) ? coef * wl : f[m] + coef * wl;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < NEQ; ++m) f[m] = (R)0.5 * f[m];
+  }
+#pragma unroll
+  for (int m = 0; m < NEQ; ++m) {
+    ap[m] = apl[m];
+    amn[m] = __shfl_down_sync(FULL, am[m], 1);
+    fr[m] = __shfl_down_sync(FULL, f[m], 1);
+    fl[m] = f[m];
+  }
+}
+
+// --------------------------------------------------------------------------
+// Warp-per-line fused update (default for 3-component systems).
+//
+// Tile = LW x LW cells with LW = 29: one warp's 32 lanes own the 32
+// consecutive edges of one grid line that the tile's 29 cells need (their 30
+// edges plus the limiter's two outer neighbours).  So:
+//   * the wave limiter fetches the upwind neighbour's wave with a register
+//     shuffle (lane +-1) instead of a shared-memory round trip;
+//   * the next edge's amdq / flux for the cell update is one more shuffle;
+//   * each sweep direction is ONE barrier-free pass (x: warps walk rows,
+//     y: warps walk columns), 3 barriers per tile in total.
+// The x pass leaves q1 = q - dtdx (apdq_i + amdq_{i+1}) and dFx per cell in
+// shared memory; the y pass adds the y term and both correction fluxes in
+// the reference order and writes q_new back to shared memory, from which
+// the tile is stored row-coalesced.
+template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS>
+__global__ void __launch_bounds__(NWARP * 32, (16 / NWARP > 0 ? 16 / NWARP : 1))
+k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
+           const Layout L, const typename S::template Params<R> P, const StepArgs A,
+           DevState* __restrict__ ds) {
+  constexpr int NEQ = S::NEQ, NW = S::NW, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int LW = 29, HW = 33, HC = HW * HW, NT = NWARP * 32;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  constexpr unsigned FULL = 0xffffffffu;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sQ = reinterpret_cast<R*>(smem_raw);
+  R* sA = sQ + NEQ * HC;
+  R* sP = sA + NAUX * HC;
+  R* sX = sP + NPR * HC;          // [2*NEQ][LW*LW]: q1 and dFx, later q_new
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Ctl ctl = step_control<R>(A, ds, !CHECKS);
+  if (!ctl.skip) {
+    const int i0 = blockIdx.x * LW, j0 = blockIdx.y * LW;
+    const R dtdx = (R)(ctl.dt / A.dx);
+    const R dtdy = (R)(ctl.dt / A.dy);
+    unsigned long long key = ~0ull;
+
+    // ---- stage tile + 2-cell halo (BC by index mapping), per-cell primitives
+    const bool inner = i0 >= 2 && i0 + LW + 2 <= L.nx && j0 >= 2 && j0 + LW + 2 <= L.ny;
+    for (int idx = tid; idx < HC; idx += NT) {
+      const int lx = idx % HW, ly = idx / HW;
+      int gi = i0 - 2 + lx, gj = j0 - 2 + ly;
+      if (!inner) { gi = map_i(gi, L); gj = map_j(gj, L); }
+      R qc[NEQ], ac[NA1], pc[NP1];
+      const R* src = q + row_off(gj, L) + gi;
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) { qc[c] = src[c * L.pitch]; sQ[c * HC + idx] = qc[c]; }
+      if (NAUX > 0) {
+        const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+#pragma unroll
+        for (int c = 0; c < NAUX; ++c) { ac[c] = asrc[c * L.pitch]; sA[c * HC + idx] = ac[c]; }
+      }
+      if (NPR > 0) {
+        S::prims(qc, ac, P, pc);
+#pragma unroll
+        for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
+      }
+    }
+    __syncthreads();
+
+    const bool cell_lane = lane >= 1 && lane <= LW;
+
+    // ---- x pass: warps walk rows; lane l = x-edge i0-1+l
+    for (int r = warp; r < LW; r += NWARP) {
+      if (j0 + r >= L.ny) break;
+      const int cl = (r + 2) * HW + lane, cr = cl + 1;
+      const int ei = i0 - 1 + lane;
+      R ap[NEQ], amn[NEQ], fl[NEQ], fr[NEQ];
+      line_edge<S, R, ORDER, LIM, CHECKS, 1, HC>(sQ, sA, sP, P, L, cl, cr, ei, j0 + r,
+                                                  lane >= 1 && lane <= 30 && ei <= L.nx, dtdx,
+                                                  key, ap, amn, fl, fr);
+      if (cell_lane) {
+        const int c = lane - 1;
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) {
+          const R qc = sQ[m * HC + cr];
+          sX[m * (LW * LW) + r * LW + c] = qc - dtdx * (ap[m] + amn[m]);
+          if (ORDER == 2) sX[(NEQ + m) * (LW * LW) + r * LW + c] = fr[m] - fl[m];
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- y pass: warps walk columns; lane l = y-edge j0-1+l
+    for (int c = warp; c < LW; c += NWARP) {
+      if (i0 + c >= L.nx) break;
+      const int cl = lane * HW + c + 2, cr = cl + HW;
+      const int ej = j0 - 1 + lane;
+      R ap[NEQ], amn[NEQ], fl[NEQ], fr[NEQ];
+      line_edge<S, R, ORDER, LIM, CHECKS, 2, HC>(sQ, sA, sP, P, L, cl, cr, i0 + c, ej,
+                                                  lane >= 1 && lane <= 30 && ej < L.ny_edges_y,
+                                                  dtdy, key, ap, amn, fl, fr);
+      if (cell_lane) {
+        const int rr = lane - 1, o = rr * LW + c;
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) {
+          R v = sX[m * (LW * LW) + o] - dtdy * (ap[m] + amn[m]);
+          if (ORDER == 2) {
+            v = v - dtdx * sX[(NEQ + m) * (LW * LW) + o];
+            v = v - dtdy * (fr[m] - fl[m]);
+          }
+          sX[m * (LW * LW) + o] = v;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- row-coalesced store of the tile
+    for (int idx = tid; idx < LW * LW; idx += NT) {
+      const int rr = idx / LW, c = idx % LW;
+      const int gi = i0 + c, gj = j0 + rr;
+      if (gi < L.nx && gj < L.ny) {
+        R* dst = qn + row_off(gj, L) + gi;
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = sX[m * (LW * LW) + idx];
+      }
+    }
+    if (CHECKS && key != ~0ull) atomicMax(&ds->slot[A.cur][2], NKEY_MAX - key);
+  }
+
+  // ---- last CTA commits the step
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int nblk = gridDim.x * gridDim.y;
+    const int prev = atomicAdd(&ds->done, 1);
+    if (prev == nblk - 1) {
+      __threadfence();
+      commit_step<R>(ds, A, ctl, L);
+    }
+  }
+}
+
+template <class S> struct LineGeom {
+  static constexpr int LW = 29, HC = 33 * 33;
+  template <class R> static constexpr size_t smem_bytes() {
+    return sizeof(R) * (size_t)((S::NEQ + S::NAUX + S::NPR) * HC + 2 * S::NEQ * LW * LW);
+  }
+};
+
 // --------------------------------------------------------------------------
 // layout conversion: host block (ncomp, nx+4, ny+4) F-order <-> SoA rows
 template <class R, class HR>
@@ -746,6 +985,7 @@ __global__ void k_riemann(const typename S::template Params<R> P, long long n,
 
 // ghost fill of an F-order (ncomp, nx+4, ny+4) field: ghost (i, j) takes
 // cell (map_x(i), map_y(j)) — the composition of grid.py's x then y pass
+template <int UNUSED = 0>
 __global__ void k_fill_ghost(double* __restrict__ d, int ncomp, int nx, int ny, int bcx, int bcy) {
   const int nxt = nx + 4, nyt = ny + 4;
   const long long n = (long long)nxt * nyt;

@@ -33,6 +33,14 @@ __device__ __forceinline__ int finite_code(const R* ql, const R* qr) {
   return 0;
 }
 
+// exponent-field test, no FP64 pipe work
+template <class R, int N> __device__ __forceinline__ bool all_finite(const R* q) {
+  bool ok = true;
+#pragma unroll
+  for (int m = 0; m < N; ++m) ok = ok && isfinite(q[m]);
+  return ok;
+}
+
 // float32: every positive float exceeds 1e-300, so the floor is 0 (numpy's
 // float32 comparison against 1e-300 behaves the same way)
 template <class R> __device__ __forceinline__ R floor_v() { return (R)0; }
@@ -70,6 +78,18 @@ struct AcousticsConst {
                                               const R*, const R*, const P& p, R& smax) {
     smax = p.c;
     return finite_code<R, NEQ>(ql, qr);
+  }
+
+  // per-cell part of the admissibility tests; probe_fast assumes both cells pass
+  template <class R, class P>
+  __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R*, const P&) {
+    return all_finite<R, NEQ>(q);
+  }
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe_fast(const R*, const R*, const R*, const R*,
+                                                   const R*, const R*, const P& p, R& smax) {
+    smax = p.c;
+    return 0;
   }
 };
 
@@ -115,6 +135,17 @@ struct AcousticsVar {
     if (bad_pos(al[1])) return 4;
     if (bad_pos(ar[0])) return 5;
     if (bad_pos(ar[1])) return 6;
+    return 0;
+  }
+
+  template <class R, class P>
+  __device__ static __forceinline__ bool cell_ok(const R* q, const R* a, const R*, const P&) {
+    return all_finite<R, NEQ>(q) && !bad_pos(a[0]) && !bad_pos(a[1]);
+  }
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe_fast(const R*, const R*, const R*, const R*,
+                                                   const R* al, const R* ar, const P&, R& smax) {
+    smax = nmax(al[1], ar[1]);
     return 0;
   }
 };
@@ -195,6 +226,16 @@ struct EulerRoe {
     if (bad_pos(qr[0])) { smax = (R)0; return 4; }
     if (bad_pos(pl[2])) { smax = (R)0; return 5; }
     if (bad_pos(pr[2])) { smax = (R)0; return 6; }
+    return probe_fast<NI>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax);
+  }
+
+  template <class R, class P>
+  __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R* pr, const P&) {
+    return all_finite<R, NEQ>(q) && !bad_pos(q[0]) && !bad_pos(pr[2]);
+  }
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe_fast(const R*, const R*, const R* pl, const R* pr,
+                                                   const R*, const R*, const P& p, R& smax) {
     R uh, vh, hh, kin, c2;
     roe<NI>(pl, pr, p, uh, vh, hh, kin, c2);
     if (!(c2 > (R)0)) { smax = (R)0; return 7; }
@@ -273,6 +314,16 @@ struct EulerHLLE {
     if (bad_pos(qr[0])) { smax = (R)0; return 4; }
     if (bad_pos(pl[2])) { smax = (R)0; return 5; }
     if (bad_pos(pr[2])) { smax = (R)0; return 6; }
+    return probe_fast<NI>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax);
+  }
+
+  template <class R, class P>
+  __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R* pr, const P&) {
+    return all_finite<R, NEQ>(q) && !bad_pos(q[0]) && !bad_pos(pr[2]);
+  }
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe_fast(const R*, const R*, const R* pl, const R* pr,
+                                                   const R*, const R*, const P& p, R& smax) {
     R s1, s2, c2;
     speeds<NI>(pl, pr, p, s1, s2, c2);
     if (!(c2 > (R)0)) { smax = (R)0; return 7; }
@@ -351,6 +402,17 @@ struct ShallowRoe {
     if (c) { smax = (R)0; return c; }
     if (bad_pos(ql[0])) { smax = (R)0; return 3; }
     if (bad_pos(qr[0])) { smax = (R)0; return 4; }
+    return probe_fast<NI>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax);
+  }
+
+  template <class R, class P>
+  __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R*, const P&) {
+    return all_finite<R, NEQ>(q) && !bad_pos(q[0]);
+  }
+  template <int NI, class R, class P>
+  __device__ static __forceinline__ int probe_fast(const R* ql, const R* qr, const R* pl,
+                                                   const R* pr, const R*, const R*, const P& p,
+                                                   R& smax) {
     R uh, vh, ch;
     roe<NI>(ql, qr, pl, pr, p, uh, vh, ch);
     smax = nmax(nmax(fabs(uh - ch), fabs(uh)), fabs(uh + ch));
