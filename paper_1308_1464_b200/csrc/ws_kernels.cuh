@@ -45,6 +45,25 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
   return v;  // valid in thread 0
 }
 
+// limiter ratio (W_up . W) / (W . W), 0 for a zero wave (oracle correction_flux)
+template <class R> __device__ __forceinline__ R theta(R dup, R dow) {
+  if (dow == (R)0) return (R)0;
+  bool ok = true;
+  const R q = FastMath::div(dup, dow, ok);
+  return ok ? q : dup / dow;
+}
+
+// per-cell primitives with FastMath; IEEE re-evaluation if a range test failed
+template <class S, class R, class P>
+__device__ __forceinline__ void prims_fast(const R* q, const R* a, const P& p, R* pr) {
+  bool ok = true;
+  S::template prims<FastMath>(q, a, p, pr, ok);
+  if (!ok) {
+    bool d = true;
+    S::template prims<IeeeMath>(q, a, p, pr, d);
+  }
+}
+
 // --------------------------------------------------------------------------
 // CFL / admissibility pre-pass.  Tile of TX x TY "edge cells" (x-edge = left
 // edge of the cell, y-edge = bottom edge, plus the domain's last column/row),
@@ -89,7 +108,7 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
       for (int c = 0; c < NAUX; ++c) { ac[c] = asrc[c * L.pitch]; sA[c][idx] = ac[c]; }
     }
     if (NPR > 0) {
-      S::prims(qc, ac, P, pc);
+      prims_fast<S>(qc, ac, P, pc);
 #pragma unroll
       for (int c = 0; c < NPR; ++c) sP[c][idx] = pc[c];
     }
@@ -109,8 +128,14 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
 #pragma unroll
     for (int c = 0; c < NPR; ++c) { pl[c] = sP[c][cl]; pr[c] = sP[c][cr]; }
     R sm;
-    int code = clean ? S::template probe_fast<NI>(ql, qr, pl, pr, al, ar, P, sm)
-                     : S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+    bool ok = true;
+    int code;
+    if (clean) {
+      code = S::template probe_fast<NI, FastMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+      if (!ok) code = S::template probe_fast<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    } else {
+      code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    }
     if (code) {
       unsigned long long k = err_key(dir, ei, L.j_off + ej, (code & 0xff) - 1, code >> 8, L.nx);
       key = k < key ? k : key;
@@ -245,7 +270,7 @@ __device__ __forceinline__ void next_step_speeds(
     for (int c = 0; c < NEQ; ++c) qc[c] = sQ[c * HC + idx];
 #pragma unroll
     for (int c = 0; c < NAUX; ++c) ac[c] = sA[c * HC + idx];
-    S::prims(qc, ac, P, pc);
+    prims_fast<S>(qc, ac, P, pc);
 #pragma unroll
     for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
   }
@@ -261,7 +286,8 @@ __device__ __forceinline__ void next_step_speeds(
 #pragma unroll
     for (int c = 0; c < NPR; ++c) { pl[c] = sP[c * HC + cl]; pr[c] = sP[c * HC + cr]; }
     R sm;
-    int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+    bool okm = true;
+    int code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, okm);
     if (code) {
       unsigned long long k = err_key(dir, gi, L.j_off + gj, (code & 0xff) - 1, code >> 8, L.nx);
       nkey = k < nkey ? k : nkey;
@@ -327,10 +353,11 @@ __device__ __forceinline__ void next_step_speeds(
 #pragma unroll
       for (int c = 0; c < NAUX; ++c) { al[c] = xa[c * L.pitch]; ar[c] = xb[c * L.pitch]; }
     }
-    S::prims(ql, al, P, pl);
-    S::prims(qr, ar, P, pr);
+    prims_fast<S>(ql, al, P, pl);
+    prims_fast<S>(qr, ar, P, pr);
     R sm;
-    int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+    bool okm = true;
+    int code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, okm);
     if (code) {
       unsigned long long k = err_key(dir, gi, L.j_off + gj, (code & 0xff) - 1, code >> 8, L.nx);
       nkey = k < nkey ? k : nkey;
@@ -457,7 +484,7 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
           for (int c = 0; c < NEQ; ++c) qc[c] = sQ[c * HC + idx];
 #pragma unroll
           for (int c = 0; c < NAUX; ++c) ac[c] = sA[c * HC + idx];
-          S::prims(qc, ac, P, pc);
+          prims_fast<S>(qc, ac, P, pc);
 #pragma unroll
           for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
         }
@@ -494,7 +521,9 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
 #pragma unroll
             for (int c = 0; c < NPR; ++c) { pl[c] = sP[c * HC + cl]; pr[c] = sP[c * HC + cr]; }
             R W[NW][NEQ], s[NW];
-            S::template solve<NI>(ql, qr, pl, pr, al, ar, P, W, s, fm[k], fp[k]);
+            bool oks = true;
+            S::template solve<NI, FastMath>(ql, qr, pl, pr, al, ar, P, W, s, fm[k], fp[k], oks);
+            if (!oks) S::template solve<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, W, s, fm[k], fp[k], oks);
             if (ORDER == 2) {
 #pragma unroll
               for (int w = 0; w < NW; ++w) {
@@ -508,7 +537,8 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
                                    : (ei < L.nx && ej >= 0 && ej < L.ny_edges_y);
               if (ref) {
                 R sm;
-                int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+                bool okm = true;
+                int code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, okm);
                 if (code) {
                   unsigned long long kk = err_key(NI - 1, ei, L.j_off + ej, (code & 0xff) - 1,
                                                   code >> 8, L.nx);
@@ -547,7 +577,7 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
                   dup = dup + sE[(w * NEQ + m) * NEST + up] * own[m];
                   dow = dow + own[m] * own[m];
                 }
-                R th = (dow != (R)0) ? dup / dow : (R)0;
+                R th = theta(dup, dow);
                 R ph = limiter_phi<LIM>(th);
                 R a = fabs(so);
                 R coef = a * ((R)1 - dtdn * a);
@@ -697,10 +727,13 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
 #pragma unroll
   for (int c = 0; c < NPR; ++c) { pl[c] = sP[c * HC + cl]; pr[c] = sP[c * HC + cr]; }
   R W[NW][NEQ], s[NW], am[NEQ], apl[NEQ];
-  S::template solve<NI>(ql, qr, pl, pr, al, ar, P, W, s, am, apl);
+  bool oks = true;
+  S::template solve<NI, FastMath>(ql, qr, pl, pr, al, ar, P, W, s, am, apl, oks);
+  if (!oks) S::template solve<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, W, s, am, apl, oks);
   if (CHECKS && ref) {
     R sm;
-    int code = S::template probe<NI>(ql, qr, pl, pr, al, ar, P, sm);
+    bool okm = true;
+    int code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, okm);
     if (code) {
       unsigned long long kk = err_key(NI - 1, ei, L.j_off + ej, (code & 0xff) - 1, code >> 8,
                                       L.nx);
@@ -708,28 +741,53 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
     }
   }
   R f[NEQ];
+  bool fz[NEQ];
 #pragma unroll
-  for (int m = 0; m < NEQ; ++m) f[m] = (R)0;
+  for (int m = 0; m < NEQ; ++m) { f[m] = (R)0; fz[m] = true; }
   if (ORDER == 2) {
+    R dupw[NW], doww[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
       R dup = (R)0, dow = (R)0;
+      bool first = true;
       // upwind edge: lane-1 if s > 0 else lane+1 (one indexed shuffle per value)
       const int src = (s[w] > (R)0) ? (int)(threadIdx.x & 31) - 1 : (int)(threadIdx.x & 31) + 1;
 #pragma unroll
       for (int m = 0; m < NEQ; ++m) {
+        if (S::template wzero<NI>(w, m)) continue;   // structural zero: no term
         const R up = __shfl_sync(FULL, W[w][m], src & 31);
-        dup = (m == 0) ? up * W[w][m] : dup + up * W[w][m];
-        dow = (m == 0) ? W[w][m] * W[w][m] : dow + W[w][m] * W[w][m];
+        dup = first ? up * W[w][m] : dup + up * W[w][m];
+        dow = first ? W[w][m] * W[w][m] : dow + W[w][m] * W[w][m];
+        first = false;
       }
-      R th = (dow != (R)0) ? dup / dow : (R)0;
+      dupw[w] = dup;
+      doww[w] = dow;
+    }
+    // the NW limiter ratios as independent FastMath divisions, one fallback
+    R thw[NW];
+    bool okt = true;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const bool nz = doww[w] != (R)0;
+      const R q = FastMath::div(nz ? dupw[w] : (R)0, nz ? doww[w] : (R)1, okt);
+      thw[w] = nz ? q : (R)0;
+    }
+    if (!okt) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) thw[w] = (doww[w] != (R)0) ? dupw[w] / doww[w] : (R)0;
+    }
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      R th = thw[w];
       R ph = limiter_phi<LIM>(th);
       R a = fabs(s[w]);
       R coef = a * ((R)1 - dtdn * a);
 #pragma unroll
       for (int m = 0; m < NEQ; ++m) {
+        if (S::template wzero<NI>(w, m)) continue;
         R wl = ph * W[w][m];
-        f[m] = (w == 0) ? coef * wl : f[m] + coef * wl;
+        f[m] = fz[m] ? coef * wl : f[m] + coef * wl;
+        fz[m] = false;
       }
     }
 #pragma unroll
@@ -760,7 +818,7 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
 // the reference order and writes q_new back to shared memory, from which
 // the tile is stored row-coalesced.
 template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS>
-__global__ void __launch_bounds__(NWARP * 32, (16 / NWARP > 0 ? 16 / NWARP : 1))
+__global__ void __launch_bounds__(NWARP * 32, (20 / NWARP > 0 ? 20 / NWARP : 1))
 k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
            const Layout L, const typename S::template Params<R> P, const StepArgs A,
            DevState* __restrict__ ds) {
@@ -799,7 +857,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         for (int c = 0; c < NAUX; ++c) { ac[c] = asrc[c * L.pitch]; sA[c * HC + idx] = ac[c]; }
       }
       if (NPR > 0) {
-        S::prims(qc, ac, P, pc);
+        prims_fast<S>(qc, ac, P, pc);
 #pragma unroll
         for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
       }
@@ -967,11 +1025,15 @@ __global__ void k_riemann(const typename S::template Params<R> P, long long n,
     for (int c = 0; c < NEQ; ++c) { a[c] = ql[c * n + e]; b[c] = qr[c * n + e]; }
 #pragma unroll
     for (int c = 0; c < NAUX; ++c) { xa[c] = al[c * n + e]; xb[c] = ar[c * n + e]; }
-    if (NPR > 0) { S::prims(a, xa, P, pa); S::prims(b, xb, P, pb); }
+    bool ok = true;
+    if (NPR > 0) {
+      S::template prims<IeeeMath>(a, xa, P, pa, ok);
+      S::template prims<IeeeMath>(b, xb, P, pb, ok);
+    }
     R sm;
-    codes[e] = S::template probe<NI>(a, b, pa, pb, xa, xb, P, sm);
+    codes[e] = S::template probe<NI, IeeeMath>(a, b, pa, pb, xa, xb, P, sm, ok);
     R W[NW][NEQ], s[NW], am[NEQ], ap[NEQ];
-    S::template solve<NI>(a, b, pa, pb, xa, xb, P, W, s, am, ap);
+    S::template solve<NI, IeeeMath>(a, b, pa, pb, xa, xb, P, W, s, am, ap, ok);
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
 #pragma unroll

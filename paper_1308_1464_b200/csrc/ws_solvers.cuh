@@ -6,16 +6,21 @@
 //   NEQ, NW, NAUX, NPR           components, waves, aux fields, per-cell primitives
 //   STATIC_SPEEDS                speeds independent of q (acoustics)
 //   Params<R>                    bound parameters (reference make_kernel, kernels.py:589-633)
-//   prims(q, aux, P, pr)         per-cell quantities shared by the 4 edges of a cell
-//   solve<NI>(ql,qr,pl,pr,al,ar,P,W,s,amdq,apdq)   one edge, NI = normal slot (1=x, 2=y)
-//   probe<NI>(...,smax) -> code  admissibility tests in the reference order and
+//   prims<M>(q, aux, P, pr, ok)  per-cell quantities shared by the 4 edges of a cell
+//   solve<NI,M>(ql,qr,pl,pr,al,ar,P,W,s,amdq,apdq,ok)  one edge, NI = normal slot (1=x, 2=y)
+//   probe<NI,M>(...,smax,ok) -> code  admissibility tests in the reference order and
 //                                the edge's max |s| (for the CFL reduction)
+//   cell_ok / probe_fast         the per-cell part of those tests / the rest
+// M is the math policy for / and sqrt (ws_math.cuh): IeeeMath, or FastMath
+// whose results equal IeeeMath's whenever `ok` stays true (callers
+// re-evaluate with IeeeMath otherwise).
 // Every expression keeps the association of the numpy oracle
 // (oracle/wavestep_oracle.py) and of the reference for the solvers it has;
 // the translation unit is compiled with --fmad=false, IEEE div/sqrt, so
 // fp64 results are bitwise identical to numpy.
 #pragma once
 #include "ws_common.cuh"
+#include "ws_math.cuh"
 
 namespace ws {
 
@@ -52,20 +57,24 @@ template <class R> __device__ __forceinline__ bool bad_pos(R v) { return !(v > f
 struct AcousticsConst {
   static constexpr int NEQ = 3, NW = 2, NAUX = 0, NPR = 0;
   static constexpr bool STATIC_SPEEDS = true;
+  // structurally zero wave components (skipped by the limiter; adding the
+  // oracle's exact zeros would not change any value)
+  template <int NI> __host__ __device__ static constexpr bool wzero(int, int m) { return m == 3 - NI; }
   template <class R> struct Params { R z, twoz, c; };
 
-  template <class R, class P>
-  __device__ static __forceinline__ void prims(const R*, const R*, const P&, R*) {}
+  template <class M, class R, class P>
+  __device__ static __forceinline__ void prims(const R*, const R*, const P&, R*, bool&) {}
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R*, const R*,
                                                const R*, const R*, const P& p, R (&W)[NW][NEQ],
-                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ],
+                                               bool& ok) {
     constexpr int TI = 3 - NI;
     R dp = qr[0] - ql[0];
     R dn = qr[NI] - ql[NI];
-    R a1 = (-dp + p.z * dn) / p.twoz;
-    R a2 = (dp + p.z * dn) / p.twoz;
+    R a1 = M::div(-dp + p.z * dn, p.twoz, ok);
+    R a2 = M::div(dp + p.z * dn, p.twoz, ok);
     W[0][0] = (-p.z) * a1; W[0][NI] = a1; W[0][TI] = (R)0;
     W[1][0] = p.z * a2;    W[1][NI] = a2; W[1][TI] = (R)0;
     s[0] = -p.c; s[1] = p.c;
@@ -73,9 +82,9 @@ struct AcousticsConst {
     for (int m = 0; m < NEQ; ++m) { am[m] = (-p.c) * W[0][m]; ap[m] = p.c * W[1][m]; }
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R*, const R*,
-                                              const R*, const R*, const P& p, R& smax) {
+                                              const R*, const R*, const P& p, R& smax, bool&) {
     smax = p.c;
     return finite_code<R, NEQ>(ql, qr);
   }
@@ -85,9 +94,10 @@ struct AcousticsConst {
   __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R*, const P&) {
     return all_finite<R, NEQ>(q);
   }
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe_fast(const R*, const R*, const R*, const R*,
-                                                   const R*, const R*, const P& p, R& smax) {
+                                                   const R*, const R*, const P& p, R& smax,
+                                                   bool&) {
     smax = p.c;
     return 0;
   }
@@ -98,25 +108,27 @@ struct AcousticsConst {
 struct AcousticsVar {
   static constexpr int NEQ = 3, NW = 2, NAUX = 2, NPR = 1;  // pr[0] = Z = rho*c
   static constexpr bool STATIC_SPEEDS = true;
+  template <int NI> __host__ __device__ static constexpr bool wzero(int, int m) { return m == 3 - NI; }
   template <class R> struct Params { R unused; };
 
-  template <class R, class P>
-  __device__ static __forceinline__ void prims(const R*, const R* a, const P&, R* pr) {
+  template <class M, class R, class P>
+  __device__ static __forceinline__ void prims(const R*, const R* a, const P&, R* pr, bool&) {
     pr[0] = a[0] * a[1];
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R* pl, const R* pr,
                                                const R* al, const R* ar, const P&, R (&W)[NW][NEQ],
-                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ],
+                                               bool& ok) {
     constexpr int TI = 3 - NI;
     R zl = pl[0], zr = pr[0];
     R cl = al[1], cr = ar[1];
     R dp = qr[0] - ql[0];
     R dn = qr[NI] - ql[NI];
     R den = zl + zr;
-    R a1 = (-dp + zr * dn) / den;
-    R a2 = (dp + zl * dn) / den;
+    R a1 = M::div(-dp + zr * dn, den, ok);
+    R a2 = M::div(dp + zl * dn, den, ok);
     W[0][0] = (-zl) * a1; W[0][NI] = a1; W[0][TI] = (R)0;
     W[1][0] = zr * a2;    W[1][NI] = a2; W[1][TI] = (R)0;
     s[0] = -cl; s[1] = cr;
@@ -124,9 +136,10 @@ struct AcousticsVar {
     for (int m = 0; m < NEQ; ++m) { am[m] = (-cl) * W[0][m]; ap[m] = cr * W[1][m]; }
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R*, const R*,
-                                              const R* al, const R* ar, const P&, R& smax) {
+                                              const R* al, const R* ar, const P&, R& smax,
+                                              bool&) {
     smax = nmax(al[1], ar[1]);
     int c = finite_code<R, NEQ>(ql, qr);
     if (c) return c;
@@ -142,9 +155,10 @@ struct AcousticsVar {
   __device__ static __forceinline__ bool cell_ok(const R* q, const R* a, const R*, const P&) {
     return all_finite<R, NEQ>(q) && !bad_pos(a[0]) && !bad_pos(a[1]);
   }
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe_fast(const R*, const R*, const R*, const R*,
-                                                   const R* al, const R* ar, const P&, R& smax) {
+                                                   const R* al, const R* ar, const P&, R& smax,
+                                                   bool&) {
     smax = nmax(al[1], ar[1]);
     return 0;
   }
@@ -154,54 +168,56 @@ struct AcousticsVar {
 // ideal gas, shared per-cell primitives (reference kernels.py:475-478, 482, 487)
 //   pr = {u = q1/rho, v = q2/rho, p, sqrt(rho), sqrt(rho)*(E+p)/rho [, c]}
 // p uses (u*u + v*v); the y sweep's (v*v + u*u) is the same IEEE sum.
-template <class R, class P>
-__device__ __forceinline__ void gas_prims(const R* q, const P& p, R* pr) {
+template <class M, class R, class P>
+__device__ __forceinline__ void gas_prims(const R* q, const P& p, R* pr, bool& ok) {
   R rho = q[0];
-  R u = q[1] / rho;
-  R v = q[2] / rho;
+  R u = M::div(q[1], rho, ok);
+  R v = M::div(q[2], rho, ok);
   R pp = p.gm1 * (q[3] - (R)0.5 * rho * (u * u + v * v));
-  R sq = sqrt(rho);
-  pr[0] = u; pr[1] = v; pr[2] = pp; pr[3] = sq; pr[4] = sq * (q[3] + pp) / rho;
+  R sq = M::sqrt_(rho, ok);
+  pr[0] = u; pr[1] = v; pr[2] = pp; pr[3] = sq; pr[4] = M::div(sq * (q[3] + pp), rho, ok);
 }
 
 // Euler, Roe linearisation, no entropy fix — reference kernels.py:457-533
 struct EulerRoe {
   static constexpr int NEQ = 4, NW = 3, NAUX = 0, NPR = 5;
   static constexpr bool STATIC_SPEEDS = false;
+  template <int NI> __host__ __device__ static constexpr bool wzero(int, int) { return false; }
   template <class R> struct Params { R gm1; };
 
-  template <class R, class P>
-  __device__ static __forceinline__ void prims(const R* q, const R*, const P& p, R* pr) {
-    gas_prims(q, p, pr);
+  template <class M, class R, class P>
+  __device__ static __forceinline__ void prims(const R* q, const R*, const P& p, R* pr, bool& ok) {
+    gas_prims<M>(q, p, pr, ok);
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void roe(const R* pl, const R* pr, const P& p, R& uh, R& vh,
-                                             R& hh, R& kin, R& c2) {
+                                             R& hh, R& kin, R& c2, bool& ok) {
     constexpr int UN = NI - 1, UT = 2 - NI;
     R ws = pl[3] + pr[3];
-    uh = (pl[3] * pl[UN] + pr[3] * pr[UN]) / ws;
-    vh = (pl[3] * pl[UT] + pr[3] * pr[UT]) / ws;
-    hh = (pl[4] + pr[4]) / ws;
+    uh = M::div(pl[3] * pl[UN] + pr[3] * pr[UN], ws, ok);
+    vh = M::div(pl[3] * pl[UT] + pr[3] * pr[UT], ws, ok);
+    hh = M::div(pl[4] + pr[4], ws, ok);
     kin = (R)0.5 * (uh * uh + vh * vh);
     c2 = p.gm1 * (hh - kin);
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R* pl, const R* pr,
                                                const R*, const R*, const P& p, R (&W)[NW][NEQ],
-                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ],
+                                               bool& ok) {
     constexpr int TI = 3 - NI;
     R uh, vh, hh, kin, c2;
-    roe<NI>(pl, pr, p, uh, vh, hh, kin, c2);
-    R ch = sqrt(c2);
+    roe<NI, M>(pl, pr, p, uh, vh, hh, kin, c2, ok);
+    R ch = M::sqrt_(c2, ok);
     R d0 = qr[0] - ql[0];
     R dm = qr[NI] - ql[NI];
     R dt = qr[TI] - ql[TI];
     R de = qr[3] - ql[3];
     R ash = dt - vh * d0;
-    R amid = p.gm1 / c2 * ((hh - uh * uh) * d0 + uh * dm - (de - ash * vh));
-    R span = (dm - uh * d0) / ch;
+    R amid = M::div(p.gm1, c2, ok) * ((hh - uh * uh) * d0 + uh * dm - (de - ash * vh));
+    R span = M::div(dm - uh * d0, ch, ok);
     R apl = (R)0.5 * (span + d0 - amid);
     R ami = d0 - amid - apl;
     W[0][0] = ami;  W[0][NI] = ami * (uh - ch);  W[0][TI] = ami * vh;       W[0][3] = ami * (hh - uh * ch);
@@ -217,29 +233,30 @@ struct EulerRoe {
     }
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R* pl, const R* pr,
-                                              const R*, const R*, const P& p, R& smax) {
+                                              const R*, const R*, const P& p, R& smax, bool& ok) {
     int c = finite_code<R, NEQ>(ql, qr);
     if (c) { smax = (R)0; return c; }
     if (bad_pos(ql[0])) { smax = (R)0; return 3; }
     if (bad_pos(qr[0])) { smax = (R)0; return 4; }
     if (bad_pos(pl[2])) { smax = (R)0; return 5; }
     if (bad_pos(pr[2])) { smax = (R)0; return 6; }
-    return probe_fast<NI>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax);
+    return probe_fast<NI, M>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax, ok);
   }
 
   template <class R, class P>
   __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R* pr, const P&) {
     return all_finite<R, NEQ>(q) && !bad_pos(q[0]) && !bad_pos(pr[2]);
   }
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe_fast(const R*, const R*, const R* pl, const R* pr,
-                                                   const R*, const R*, const P& p, R& smax) {
+                                                   const R*, const R*, const P& p, R& smax,
+                                                   bool& ok) {
     R uh, vh, hh, kin, c2;
-    roe<NI>(pl, pr, p, uh, vh, hh, kin, c2);
+    roe<NI, M>(pl, pr, p, uh, vh, hh, kin, c2, ok);
     if (!(c2 > (R)0)) { smax = (R)0; return 7; }
-    R ch = sqrt(c2);
+    R ch = M::sqrt_(c2, ok);
     smax = nmax(nmax(fabs(uh - ch), fabs(uh)), fabs(uh + ch));
     return 0;
   }
@@ -249,48 +266,50 @@ struct EulerRoe {
 struct EulerHLLE {
   static constexpr int NEQ = 4, NW = 2, NAUX = 0, NPR = 6;  // gas prims + c
   static constexpr bool STATIC_SPEEDS = false;
+  template <int NI> __host__ __device__ static constexpr bool wzero(int, int) { return false; }
   template <class R> struct Params { R gm1, gam; };
 
-  template <class R, class P>
-  __device__ static __forceinline__ void prims(const R* q, const R*, const P& p, R* pr) {
-    gas_prims(q, p, pr);
-    pr[5] = sqrt(p.gam * pr[2] / q[0]);
+  template <class M, class R, class P>
+  __device__ static __forceinline__ void prims(const R* q, const R*, const P& p, R* pr, bool& ok) {
+    gas_prims<M>(q, p, pr, ok);
+    pr[5] = M::sqrt_(M::div(p.gam * pr[2], q[0], ok), ok);
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void roe(const R* pl, const R* pr, const P& p, R& uh, R& vh,
-                                             R& c2) {
+                                             R& c2, bool& ok) {
     constexpr int UN = NI - 1, UT = 2 - NI;
-    R iws = (R)1 / (pl[3] + pr[3]);
+    R iws = M::rcp(pl[3] + pr[3], ok);
     uh = (pl[3] * pl[UN] + pr[3] * pr[UN]) * iws;
     vh = (pl[3] * pl[UT] + pr[3] * pr[UT]) * iws;
     R hh = (pl[4] + pr[4]) * iws;
     c2 = p.gm1 * (hh - (R)0.5 * (uh * uh + vh * vh));
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void speeds(const R* pl, const R* pr, const P& p, R& s1,
-                                                R& s2, R& c2) {
+                                                R& s2, R& c2, bool& ok) {
     constexpr int UN = NI - 1;
     R uh, vh;
-    roe<NI>(pl, pr, p, uh, vh, c2);
-    R ch = sqrt(c2);
+    roe<NI, M>(pl, pr, p, uh, vh, c2, ok);
+    R ch = M::sqrt_(c2, ok);
     s1 = nmin(pl[UN] - pl[5], uh - ch);
     s2 = nmax(pr[UN] + pr[5], uh + ch);
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R* pl, const R* pr,
                                                const R*, const R*, const P& p, R (&W)[NW][NEQ],
-                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ],
+                                               bool& ok) {
     constexpr int TI = 3 - NI, UN = NI - 1;
     R s1, s2, c2;
-    speeds<NI>(pl, pr, p, s1, s2, c2);
+    speeds<NI, M>(pl, pr, p, s1, s2, c2, ok);
     R ul = pl[UN], ur = pr[UN];
     R fl[NEQ], fr[NEQ];
     fl[0] = ql[NI]; fl[NI] = ql[NI] * ul + pl[2]; fl[TI] = ql[TI] * ul; fl[3] = ul * (ql[3] + pl[2]);
     fr[0] = qr[NI]; fr[NI] = qr[NI] * ur + pr[2]; fr[TI] = qr[TI] * ur; fr[3] = ur * (qr[3] + pr[2]);
-    R inv = (R)1 / (s1 - s2);
+    R inv = M::rcp(s1 - s2, ok);
     R n0 = nmin(s1, (R)0), n1 = nmin(s2, (R)0);
     R p0 = nmax(s1, (R)0), p1 = nmax(s2, (R)0);
 #pragma unroll
@@ -305,27 +324,28 @@ struct EulerHLLE {
     s[0] = s1; s[1] = s2;
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R* pl, const R* pr,
-                                              const R*, const R*, const P& p, R& smax) {
+                                              const R*, const R*, const P& p, R& smax, bool& ok) {
     int c = finite_code<R, NEQ>(ql, qr);
     if (c) { smax = (R)0; return c; }
     if (bad_pos(ql[0])) { smax = (R)0; return 3; }
     if (bad_pos(qr[0])) { smax = (R)0; return 4; }
     if (bad_pos(pl[2])) { smax = (R)0; return 5; }
     if (bad_pos(pr[2])) { smax = (R)0; return 6; }
-    return probe_fast<NI>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax);
+    return probe_fast<NI, M>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax, ok);
   }
 
   template <class R, class P>
   __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R* pr, const P&) {
     return all_finite<R, NEQ>(q) && !bad_pos(q[0]) && !bad_pos(pr[2]);
   }
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe_fast(const R*, const R*, const R* pl, const R* pr,
-                                                   const R*, const R*, const P& p, R& smax) {
+                                                   const R*, const R*, const P& p, R& smax,
+                                                   bool& ok) {
     R s1, s2, c2;
-    speeds<NI>(pl, pr, p, s1, s2, c2);
+    speeds<NI, M>(pl, pr, p, s1, s2, c2, ok);
     if (!(c2 > (R)0)) { smax = (R)0; return 7; }
     smax = nmax(fabs(s1), fabs(s2));
     return 0;
@@ -338,37 +358,40 @@ struct EulerHLLE {
 struct ShallowRoe {
   static constexpr int NEQ = 3, NW = 3, NAUX = 0, NPR = 3;
   static constexpr bool STATIC_SPEEDS = false;
+  // W2 = a2 (0, 0, 1): only the transverse slot
+  template <int NI> __host__ __device__ static constexpr bool wzero(int w, int m) { return w == 1 && m != 3 - NI; }
   template <class R> struct Params { R grav, sqg; };
 
-  template <class R, class P>
-  __device__ static __forceinline__ void prims(const R* q, const R*, const P&, R* pr) {
-    R rh = (R)1 / q[0];
+  template <class M, class R, class P>
+  __device__ static __forceinline__ void prims(const R* q, const R*, const P&, R* pr, bool& ok) {
+    R rh = M::rcp(q[0], ok);
     pr[0] = q[1] * rh;
     pr[1] = q[2] * rh;
-    pr[2] = sqrt(q[0]);
+    pr[2] = M::sqrt_(q[0], ok);
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void roe(const R* ql, const R* qr, const R* pl, const R* pr,
-                                             const P& p, R& uh, R& vh, R& ch) {
+                                             const P& p, R& uh, R& vh, R& ch, bool& ok) {
     constexpr int UN = NI - 1, UT = 2 - NI;
-    R iws = (R)1 / (pl[2] + pr[2]);
+    R iws = M::rcp(pl[2] + pr[2], ok);
     uh = (pl[2] * pl[UN] + pr[2] * pr[UN]) * iws;
     vh = (pl[2] * pl[UT] + pr[2] * pr[UT]) * iws;
-    ch = sqrt(p.grav * ((R)0.5 * (ql[0] + qr[0])));
+    ch = M::sqrt_(p.grav * ((R)0.5 * (ql[0] + qr[0])), ok);
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R* pl, const R* pr,
                                                const R*, const R*, const P& p, R (&W)[NW][NEQ],
-                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ]) {
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ],
+                                               bool& ok) {
     constexpr int TI = 3 - NI, UN = NI - 1;
     R uh, vh, ch;
-    roe<NI>(ql, qr, pl, pr, p, uh, vh, ch);
+    roe<NI, M>(ql, qr, pl, pr, p, uh, vh, ch, ok);
     R d0 = qr[0] - ql[0];
     R d1 = qr[NI] - ql[NI];
     R d2 = qr[TI] - ql[TI];
-    R i2c = (R)0.5 / ch;
+    R i2c = M::div((R)0.5, ch, ok);
     R s1 = uh - ch, s3 = uh + ch;
     R a1 = (s3 * d0 - d1) * i2c;
     R a2 = d2 - vh * d0;
@@ -383,8 +406,8 @@ struct ShallowRoe {
     R del1 = nmax((R)0, (ur - cr) - (ul - cl));
     R del3 = nmax((R)0, (ur + cr) - (ul + cl));
     R f1 = fabs(s1), f2 = fabs(uh), f3 = fabs(s3);
-    if (f1 < del1) f1 = (s1 * s1 + del1 * del1) / ((R)2 * del1);
-    if (f3 < del3) f3 = (s3 * s3 + del3 * del3) / ((R)2 * del3);
+    if (f1 < del1) f1 = M::div(s1 * s1 + del1 * del1, (R)2 * del1, ok);
+    if (f3 < del3) f3 = M::div(s3 * s3 + del3 * del3, (R)2 * del3, ok);
     R am1 = (R)0.5 * (s1 - f1), am2 = (R)0.5 * (uh - f2), am3 = (R)0.5 * (s3 - f3);
     R ap1 = (R)0.5 * (s1 + f1), ap2 = (R)0.5 * (uh + f2), ap3 = (R)0.5 * (s3 + f3);
     am[0] = am1 * W[0][0] + am3 * W[2][0];
@@ -395,26 +418,26 @@ struct ShallowRoe {
     ap[TI] = ap1 * W[0][TI] + ap2 * a2 + ap3 * W[2][TI];
   }
 
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R* pl, const R* pr,
-                                              const R*, const R*, const P& p, R& smax) {
+                                              const R*, const R*, const P& p, R& smax, bool& ok) {
     int c = finite_code<R, NEQ>(ql, qr);
     if (c) { smax = (R)0; return c; }
     if (bad_pos(ql[0])) { smax = (R)0; return 3; }
     if (bad_pos(qr[0])) { smax = (R)0; return 4; }
-    return probe_fast<NI>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax);
+    return probe_fast<NI, M>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, p, smax, ok);
   }
 
   template <class R, class P>
   __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R*, const P&) {
     return all_finite<R, NEQ>(q) && !bad_pos(q[0]);
   }
-  template <int NI, class R, class P>
+  template <int NI, class M, class R, class P>
   __device__ static __forceinline__ int probe_fast(const R* ql, const R* qr, const R* pl,
                                                    const R* pr, const R*, const R*, const P& p,
-                                                   R& smax) {
+                                                   R& smax, bool& ok) {
     R uh, vh, ch;
-    roe<NI>(ql, qr, pl, pr, p, uh, vh, ch);
+    roe<NI, M>(ql, qr, pl, pr, p, uh, vh, ch, ok);
     smax = nmax(nmax(fabs(uh - ch), fabs(uh)), fabs(uh + ch));
     return 0;
   }

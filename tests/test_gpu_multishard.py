@@ -1,0 +1,97 @@
+"""Row-strip shards on ONE GPU (no NCCL, nothing waits on another kernel):
+P CudaShard handles with torch-owned buffers; halo rows are moved with
+torch copies and the 3-word slot is max-reduced with torch — the same data
+flow sharded_step runs over NCCL.  Must equal the single-domain oracle
+bitwise (state of every shard, every dt), including periodic wrap-around
+between the first and last strip and an inadmissible cell on one strip."""
+
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from helpers import PARAMS, oracle_run, random_state
+from oracle import wavestep_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc):
+    import torch
+
+    from paper_1308_1464_b200 import _abi
+    from paper_1308_1464_b200 import parallel as PL
+    dev = torch.device("cuda", 0)
+    case = SimpleNamespace(kernel=name, kernel_params=PARAMS[name], nx=nx, dx=dx, dy=dy,
+                           order=order, limiter=limiter, bc=bc)
+    periodic = bc == "periodic"
+    strips = PL.RowStrips(ny, P)
+    shards = [PL.CudaShard(case, strips, r, dev, periodic) for r in range(P)]
+    for r, sh in enumerate(shards):
+        j0, j1 = strips.bounds(r)
+        sh.grid.upload(PL.shard_block(gq, j0, j1),
+                       PL.shard_block(gaux, j0, j1) if gaux is not None else None,
+                       stream=sh.stream)
+    ctl = _abi.make_ctl(0.9)
+    for _ in range(steps):
+        views = [sh.halo_views() for sh in shards]
+        for r in range(P):
+            lo, hi = strips.neighbours(r, periodic)
+            if hi is not None:
+                views[hi][2].copy_(views[r][1])     # my top rows -> upper neighbour's low ghosts
+            if lo is not None:
+                views[lo][3].copy_(views[r][0])     # my bottom rows -> lower neighbour's high ghosts
+        for sh in shards:
+            sh.phase_speeds()
+        slot = shards[0].slot_view().clone()
+        for sh in shards[1:]:
+            slot = torch.maximum(slot, sh.slot_view())
+        for sh in shards:
+            sh.slot_view().copy_(slot)
+            sh.phase_update(ctl)
+    torch.cuda.synchronize()
+    out, reps, errs = [], [], []
+    for sh in shards:
+        res = sh.grid.poll()
+        reps.append([r[0] for r in res.reports])
+        errs.append(res.error)
+        out.append(sh.grid.download()[:, 2:-2, 2:-2])
+        sh.grid.close()
+    return out, reps, errs, strips
+
+
+@pytest.mark.parametrize("name,P,bc,order,limiter", [
+    ("shallow-water-roe", 2, "extrapolate", 2, "mc"),
+    ("shallow-water-roe", 3, "periodic", 2, "superbee"),
+    ("euler-hlle", 2, "periodic", 2, "minmod"),
+    ("acoustics-var", 3, "extrapolate", 2, "mc"),
+    ("acoustics-const", 2, "periodic", 1, "none"),
+    ("euler", 4, "extrapolate", 1, "none"),
+])
+def test_fake_shards_bitwise_single_domain(name, P, bc, order, limiter):
+    nx, ny, steps = 45, 70, 5
+    dx, dy = 1 / nx, 1 / ny
+    gq, gaux = random_state(name, nx, ny, 21)
+    ref, oreps = oracle_run(name, gq, gaux, nx, ny, dx, dy, steps=steps, order=order,
+                            limiter=limiter, bc_x=bc, bc_y=bc)
+    out, reps, errs, strips = fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order,
+                                           limiter, bc)
+    for r in range(P):
+        j0, j1 = strips.bounds(r)
+        assert errs[r].code == 0
+        assert reps[r] == [o.dt for o in oreps]
+        assert np.array_equal(out[r], ref[:, 2:-2, 2 + j0:2 + j1]), f"shard {r}"
+
+
+def test_fake_shards_report_the_global_first_error():
+    from paper_1308_1464_b200 import _abi
+    name, nx, ny = "shallow-water-roe", 20, 24
+    gq, _ = random_state(name, nx, ny, 22)
+    gq[0, 2 + 7, 2 + 19] = -1.0            # lives on strip 2 of 3
+    with pytest.raises(O.OracleError) as oe:
+        oracle_run(name, gq, None, nx, ny, 1 / nx, 1 / ny, steps=1, order=2, limiter="mc")
+    _, _, errs, _ = fake_sharded(name, gq, None, nx, ny, 1 / nx, 1 / ny, 3, 1, 2, "mc",
+                                 "extrapolate")
+    for e in errs:
+        assert e.code == _abi.WS_ERR_KERNEL
+        assert f"{'xy'[e.direction]}-interface (i={e.i}, j={e.j})" == str(oe.value).split(":")[0]
