@@ -42,7 +42,8 @@ enum ws_solver { WS_ACOUSTICS_CONST = 0,   /* kernels.py:374-406, params rho, bu
                  WS_ACOUSTICS_VAR = 1,     /* kernels.py:409-454, aux (rho, c)          */
                  WS_EULER_ROE = 2,         /* kernels.py:457-533, params gamma          */
                  WS_EULER_HLLE = 3,        /* extension, params gamma                   */
-                 WS_SHALLOW_ROE = 4 };     /* extension (Roe + Harten fix), params grav */
+                 WS_SHALLOW_ROE = 4,       /* extension (Roe + Harten fix), params grav */
+                 WS_ADVECTION = 5 };       /* kernels.py:356-371, params u, v           */
 
 enum ws_limiter { WS_LIM_NONE = 0, WS_LIM_MINMOD = 1, WS_LIM_SUPERBEE = 2, WS_LIM_MC = 3 };
 enum ws_bc { WS_BC_PERIODIC = 0, WS_BC_EXTRAPOLATE = 1 };  /* grid.py:12-16 */
@@ -58,7 +59,8 @@ typedef struct ws_desc {
   double dx, dy;             /* cell widths                                         */
   int32_t num_ghost;         /* must be 2 (reference default grid.py:36)            */
   int32_t solver;            /* enum ws_solver                                      */
-  double params[4];          /* acoustics-const: rho, bulk; euler*: gamma; sw: grav */
+  double params[4];          /* acoustics-const: rho, bulk; euler*: gamma; sw: grav;
+                                advection: u, v                                      */
   int32_t order;             /* 1 = reference donor cell, 2 = + limited correction */
   int32_t limiter;           /* enum ws_limiter (ignored for order 1)               */
   int32_t bc_x, bc_y;        /* enum ws_bc                                          */

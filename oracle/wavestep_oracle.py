@@ -147,6 +147,19 @@ class Solver:
             return _CHECK[self.name](ni, ql, qr, auxl, auxr, self.params)
 
 
+def rp_advection(ni, ql, qr, auxl, auxr, p):
+    """kernels.py:356-371 — one wave qr-ql at u (x) or v (y)."""
+    sp = p["u"] if ni == 1 else p["v"]
+    jump = qr - ql
+    w = jump[np.newaxis]
+    s = np.full((1,) + jump.shape[1:], sp, dtype=jump.dtype)
+    return w, s, min(sp, 0.0) * jump, max(sp, 0.0) * jump
+
+
+def _chk_advection(ni, ql, qr, auxl, auxr, p):
+    return _finite_checks(ql, qr)
+
+
 def acoustics_const_params(rho: float, bulk: float) -> dict:
     # kernels.py:305-311: c = sqrt(K/rho), Z = rho*c (Python floats)
     c = math.sqrt(bulk / rho)
@@ -441,6 +454,7 @@ def _chk_shallow(ni, ql, qr, auxl, auxr, p):
 
 
 _SOLVE = {
+    "advection": rp_advection,
     "acoustics-const": rp_acoustics_const,
     "acoustics-var": rp_acoustics_var,
     "euler": rp_euler_roe,
@@ -448,6 +462,7 @@ _SOLVE = {
     "shallow-water-roe": rp_shallow_roe,
 }
 _CHECK = {
+    "advection": _chk_advection,
     "acoustics-const": _chk_acoustics_const,
     "acoustics-var": _chk_acoustics_var,
     "euler": _chk_gas,
@@ -455,6 +470,7 @@ _CHECK = {
     "shallow-water-roe": _chk_shallow,
 }
 _SHAPES = {  # (num_eqn, num_waves, num_aux)
+    "advection": (1, 1, 0),
     "acoustics-const": (3, 2, 0),
     "acoustics-var": (3, 2, 2),
     "euler": (4, 3, 0),
@@ -467,7 +483,9 @@ def make_solver(name: str, **params) -> Solver:
     if name not in _SOLVE:
         raise ValueError(f"unknown kernel {name!r}")
     neq, mw, naux = _SHAPES[name]
-    if name == "acoustics-const":
+    if name == "advection":
+        prm = {"u": float(params["u"]), "v": float(params["v"])}
+    elif name == "acoustics-const":
         prm = acoustics_const_params(float(params["rho"]), float(params["bulk"]))
     elif name in ("euler", "euler-hlle"):
         prm = {"gamma": float(params.get("gamma", 1.4))}

@@ -24,6 +24,7 @@ SOLVER_IDS = {
     "euler": 2,
     "euler-hlle": 3,
     "shallow-water-roe": 4,
+    "advection": 5,
 }
 LIMITER_IDS = {"none": 0, "minmod": 1, "superbee": 2, "mc": 3}
 BC_IDS = {"periodic": 0, "extrapolate": 1}

@@ -185,7 +185,7 @@ BUILDERS = {
 
 def bytes_per_cell(kernel: str, dtype: str = "f64") -> int:
     """Algorithmic bytes per cell-update: q read + aux read + q write."""
-    neq = {"acoustics-const": 3, "acoustics-var": 3, "euler": 4, "euler-hlle": 4,
+    neq = {"advection": 1, "acoustics-const": 3, "acoustics-var": 3, "euler": 4, "euler-hlle": 4,
            "shallow-water-roe": 3}[kernel]
     naux = 2 if kernel == "acoustics-var" else 0
     return (2 * neq + naux) * (8 if dtype == "f64" else 4)

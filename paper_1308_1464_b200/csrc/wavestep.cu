@@ -77,6 +77,22 @@ template <class R> bool bind(ws_handle* h, std::string& msg) {
       h->neq = 4; h->naux = 0;
       return true;
     }
+    case WS_ADVECTION: {
+      // reference kernels.py:362-363: non-finite velocity is a KernelError
+      if (!(std::isfinite(p[0]) && std::isfinite(p[1]))) {
+        char b[128];
+        snprintf(b, sizeof b, "non-finite advection velocity (%.17g, %.17g)", p[0], p[1]);
+        msg = b;
+        return false;
+      }
+      Advection::Params<R> pr{(R)p[0], (R)p[1]};
+      h->params.assign((char*)&pr, (char*)&pr + sizeof pr);
+      h->host_static[0] = std::fabs((double)(R)p[0]);
+      h->host_static[1] = std::fabs((double)(R)p[1]);
+      h->ops = ops_advection(d.precision, d.order, d.limiter);
+      h->neq = 1; h->naux = 0;
+      return true;
+    }
     case WS_SHALLOW_ROE: {
       if (!(p[0] > 0)) {
         char b[96];
@@ -217,7 +233,8 @@ int ws_buffer_bytes(const ws_desc* d, uint64_t* q_bytes, uint64_t* aux_bytes,
   int rc = validate(d, m);
   if (rc) return fail(nullptr, rc, m);
   size_t esz = d->precision == WS_FP32 ? 4 : 8;
-  int neq = (d->solver == WS_EULER_ROE || d->solver == WS_EULER_HLLE) ? 4 : 3;
+  int neq = (d->solver == WS_EULER_ROE || d->solver == WS_EULER_HLLE) ? 4
+            : (d->solver == WS_ADVECTION ? 1 : 3);
   int naux = d->solver == WS_ACOUSTICS_VAR ? 2 : 0;
   long long pitch = pitch_for(d->nx, esz);
   if (q_bytes) *q_bytes = (uint64_t)(d->ny + 4) * neq * pitch * esz;
@@ -261,11 +278,20 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   h->ds = static_cast<DevState*>(dsp);
   // fused next-step CFL epilogue: correct (bitwise) but slower than the
   // pre-pass on B200 in round 1 (profiles/r1_exp_fused.md) -> opt-in
-  h->fused = !h->ops.static_speeds && !h->multi && std::getenv("WS_FUSE") &&
-             std::atoi(std::getenv("WS_FUSE")) != 0;
+  // fused next-step CFL epilogues (line kernel: in-tile probes + tile-border
+  // kernel; tile kernel: shared-border counters) are bitwise correct but not
+  // faster than the k_speeds pre-pass on B200 (profiles/r1_exp_fused.md):
+  // opt-in with WS_FUSE=1
   if (const char* v = std::getenv("WS_EXP")) h->exp = std::atoi(v);
-  h->line_kernel = h->neq == 3;   // 4-component systems exceed 1 CTA/SM of line smem
+  h->line_kernel = h->neq <= 3;   // 4-component systems exceed 1 CTA/SM of line smem
   if (const char* v = std::getenv("WS_KERNEL")) h->line_kernel = std::strcmp(v, "tile") != 0;
+  {
+    const char* v = std::getenv("WS_FUSE");
+    const bool env_on = v && std::atoi(v) != 0, env_off = v && std::atoi(v) == 0;
+    (void)env_off;
+    if (h->line_kernel) h->fused = h->ops.can_fuse_line && !h->multi && env_on;
+    else h->fused = !h->ops.static_speeds && !h->multi && env_on;
+  }
   // generous for every tile shape (TX >= 16, TY >= 4): vertical + horizontal borders
   h->border_bytes = sizeof(int) * 2 * (size_t)((d->nx + 15) / 16 + 1) * ((d->ny + 3) / 4 + 1);
   if ((e = cudaMalloc(&h->borders, h->border_bytes)) != cudaSuccess) {
@@ -334,9 +360,10 @@ static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz
       h->ops.static_speed(h, st);
     } else {
       unsigned long long b[2];
-      if (h->esz == 8) { std::memcpy(&b[0], &h->host_static[0], 8); }
-      else { float f = (float)h->host_static[0]; unsigned u; std::memcpy(&u, &f, 4); b[0] = u; }
-      b[1] = b[0];
+      for (int k = 0; k < 2; ++k) {
+        if (h->esz == 8) { std::memcpy(&b[k], &h->host_static[k], 8); }
+        else { float f = (float)h->host_static[k]; unsigned u; std::memcpy(&u, &f, 4); b[k] = u; }
+      }
       // pageable source: synchronous w.r.t. the host, ordered on st
       WS_CUDA(h, cudaMemcpyAsync(&h->ds->static_bits[0], b, sizeof b, cudaMemcpyHostToDevice, st));
       WS_CUDA(h, cudaStreamSynchronize(st));
@@ -489,16 +516,16 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
       enqueue_step(h, c, 0, st);
       enqueue_step(h, c, 1, st);
       WS_CUDA(h, cudaStreamEndCapture(st, &g));
+      h->graph_launches = h->launches - l0;
       h->launches = l0;
       WS_CUDA(h, cudaGraphInstantiate(&h->gexec, g, 0));
       cudaGraphDestroy(g);
       h->gctl = *c;
       h->gstream = st;
     }
-    const int per_pair = (h->ops.static_speeds && !h->multi) || h->fused ? 2 : 4;
     while (left >= 2) {
       WS_CUDA(h, cudaGraphLaunch(h->gexec, st));
-      h->launches += per_pair;
+      h->launches += h->graph_launches;
       h->enq += 2;
       left -= 2;
     }
@@ -601,6 +628,9 @@ int ws_riemann(int32_t solver, const double* p, int32_t direction, int64_t n, co
       return riemann_euler_hlle(p, direction, n, ql, qr, al, ar, waves, speeds, amdq, apdq,
                                 codes);
     }
+    case WS_ADVECTION:
+      return riemann_advection(p, direction, n, ql, qr, al, ar, waves, speeds, amdq, apdq,
+                               codes);
     case WS_SHALLOW_ROE: {
       if (!(p[0] > 0)) return fail(nullptr, WS_ERR_CONFIG, "gravity must be positive");
       return riemann_shallow_roe(p, direction, n, ql, qr, al, ar, waves, speeds, amdq, apdq,

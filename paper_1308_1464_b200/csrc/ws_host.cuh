@@ -36,6 +36,7 @@ struct Ops {
   void (*static_speed)(ws_handle*, cudaStream_t);
   void (*prepare)();   // one-time kernel attributes (never inside a capture)
   int static_speeds;   // solver has q-independent speeds
+  int can_fuse_line;   // warp-line kernel has the fused next-step CFL epilogue
 };
 
 }  // namespace wsh
@@ -66,6 +67,7 @@ struct ws_handle {
   ws_ctl gctl{};
   cudaStream_t gstream = nullptr;
   long long launches = 0;
+  long long graph_launches = 0;  // kernels per replay of the 2-step graph
   int variant = 0;              // WS_TILE experiment selector (0 = default tiles)
   bool fused = false;           // next-step CFL maxima computed in the update epilogue
   bool need_prepass = true;     // fused mode: slot of the current state not yet filled
@@ -183,8 +185,10 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
 
   static void prepare() {
     const int lsmem = (int)LineGeom<S>::template smem_bytes<R>();
-    cudaFuncSetAttribute(kern_w<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
-    cudaFuncSetAttribute(kern_w<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+    cudaFuncSetAttribute(kern_w<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+    cudaFuncSetAttribute(kern_w<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+    if constexpr (CAN_FUSE)
+      cudaFuncSetAttribute(kern_w<false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
     const int smem = (int)G::template smem_bytes<R>();
     cudaFuncSetAttribute(kern<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(kern<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -202,24 +206,36 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   }
 
   static constexpr int LNW = 10;  // warps per CTA of the warp-line kernel (29 lines / 10 ~ 97%)
-  template <bool CHECKS> static auto kern_w() {
-    return k_update_w<S, R, ORDER, LIM, LNW, CHECKS>;
+  static constexpr bool CAN_FUSE = !S::STATIC_SPEEDS && S::NAUX == 0 && S::NPR <= S::NEQ;
+  template <bool CHECKS, bool FUSED> static auto kern_w() {
+    return k_update_w<S, R, ORDER, LIM, LNW, CHECKS, FUSED>;
   }
-  template <bool CHECKS> static void update_w(ws_handle* h, const void* q, void* qn,
-                                              const StepArgs& a, cudaStream_t st) {
-    auto k = kern_w<CHECKS>();
+  template <bool CHECKS, bool FUSED> static void update_w(ws_handle* h, const void* q, void* qn,
+                                                          const StepArgs& a, cudaStream_t st) {
+    auto k = kern_w<CHECKS, FUSED>();
     const size_t smem = LineGeom<S>::template smem_bytes<R>();
     dim3 grid((h->L.nx + 28) / 29, (h->L.ny + 28) / 29);
     k<<<grid, LNW * 32, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
                                     static_cast<R*>(qn), h->L, prm(h), a, h->ds);
     h->launches++;
+    if (FUSED) {
+      // tile-border edges of the new state, into the next step's slot
+      k_border<S, R, 29, 256><<<148 * 2, 256, 0, st>>>(static_cast<const R*>(qn), h->L, prm(h),
+                                                       a.cur ^ 1, h->ds);
+      h->launches++;
+    }
   }
 
   static void update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
     if (h->variant > 0 && variant_update<S, R, ORDER, LIM>(h, q, qn, a, st)) return;
-    if (h->line_kernel && !h->fused) {
-      if (S::STATIC_SPEEDS && !h->multi) update_w<true>(h, q, qn, a, st);
-      else update_w<false>(h, q, qn, a, st);
+    if (h->line_kernel) {
+      if (S::STATIC_SPEEDS && !h->multi) update_w<true, false>(h, q, qn, a, st);
+      else if constexpr (CAN_FUSE) {
+        if (h->fused) update_w<false, true>(h, q, qn, a, st);
+        else update_w<false, false>(h, q, qn, a, st);
+      } else {
+        update_w<false, false>(h, q, qn, a, st);
+      }
       return;
     }
     if (S::STATIC_SPEEDS && !h->multi) update_t<true, false>(h, q, qn, a, st);
@@ -259,6 +275,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     o.static_speed = &static_speed;
     o.prepare = &prepare;
     o.static_speeds = S::STATIC_SPEEDS ? 1 : 0;
+    o.can_fuse_line = CAN_FUSE ? 1 : 0;
     return o;
   }
 };
@@ -279,6 +296,7 @@ Ops ops_acoustics_var(int prec, int order, int lim);
 Ops ops_euler_roe(int prec, int order, int lim);
 Ops ops_euler_hlle(int prec, int order, int lim);
 Ops ops_shallow_roe(int prec, int order, int lim);
+Ops ops_advection(int prec, int order, int lim);
 
 // batched pointwise plugin call (ws_riemann), fp64
 int riemann_acoustics_const(const double* p, int dir, long long n, const double* ql,
@@ -296,6 +314,9 @@ int riemann_euler_hlle(const double* p, int dir, long long n, const double* ql,
 int riemann_shallow_roe(const double* p, int dir, long long n, const double* ql,
                         const double* qr, const double* al, const double* ar, double* w,
                         double* s, double* am, double* ap, int* codes);
+int riemann_advection(const double* p, int dir, long long n, const double* ql,
+                      const double* qr, const double* al, const double* ar, double* w,
+                      double* s, double* am, double* ap, int* codes);
 
 template <class S>
 int riemann_t(const typename S::template Params<double>& P, int dir, long long n,

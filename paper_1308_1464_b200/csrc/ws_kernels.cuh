@@ -706,6 +706,101 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
   }
 }
 
+// FUSED epilogue helper: admissibility + max |s| of one edge of the NEXT
+// state (cell-local tests already known through `clean`)
+template <class S, class R, int NI>
+__device__ __forceinline__ void probe_next(const R* ql, const R* qr, const R* pl, const R* pr,
+                                           bool clean, const typename S::template Params<R>& P,
+                                           const Layout& L, int gi, int gj, R& mx,
+                                           unsigned long long& key) {
+  R sm;
+  bool ok = true;
+  int code;
+  if (clean) {
+    code = S::template probe_fast<NI, FastMath>(ql, qr, pl, pr, (const R*)nullptr,
+                                                (const R*)nullptr, P, sm, ok);
+    if (!ok) code = S::template probe_fast<NI, IeeeMath>(ql, qr, pl, pr, (const R*)nullptr,
+                                                         (const R*)nullptr, P, sm, ok);
+  } else {
+    code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr,
+                                           P, sm, ok);
+  }
+  if (code) {
+    unsigned long long k = err_key(NI - 1, gi, L.j_off + gj, (code & 0xff) - 1, code >> 8, L.nx);
+    key = k < key ? k : key;
+  } else {
+    mx = nmax(mx, sm);
+  }
+}
+
+// Edges on the borders between LW x LW tiles (and the periodic wrap, reported
+// as edge 0), probed on the new state after the FUSED update kernel: the
+// only reference edges its epilogue cannot see.  One thread per edge.
+template <class S, class R, int LW, int NT>
+__global__ void __launch_bounds__(NT)
+k_border(const R* __restrict__ q, const Layout L, const typename S::template Params<R> P,
+         const int slot, DevState* __restrict__ ds) {
+  constexpr int NEQ = S::NEQ, NPR = S::NPR, NP1 = NPR > 0 ? NPR : 1;
+  __shared__ unsigned long long sred[2][NT / 32];
+  __shared__ int s_skip;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_skip = __ldcg(&ds->err) | __ldcg(&ds->finished);
+  __syncthreads();
+  if (s_skip) return;
+  const int ntx = (L.nx + LW - 1) / LW, nty = (L.ny + LW - 1) / LW;
+  const bool perx = L.bcx == BC_PERIODIC, pery = L.bcy == BC_PERIODIC;
+  const int nvb = ntx - 1 + (perx ? 1 : 0), nhb = nty - 1 + (pery ? 1 : 0);
+  const long long nv = (long long)nvb * L.ny, n = nv + (long long)nhb * L.nx;
+  R mx = (R)0, my = (R)0;
+  unsigned long long key = ~0ull;
+  for (long long t = blockIdx.x * (long long)NT + tid; t < n; t += (long long)gridDim.x * NT) {
+    int il, jl, ir, jr, gi, gj, dir;
+    if (t < nv) {
+      const int b = (int)(t / L.ny), j = (int)(t % L.ny);
+      dir = 0; gj = j; jl = jr = j;
+      if (b < ntx - 1) { gi = (b + 1) * LW; il = gi - 1; ir = gi; }
+      else { gi = 0; il = L.nx - 1; ir = 0; }
+    } else {
+      const long long u = t - nv;
+      const int b = (int)(u / L.nx), i = (int)(u % L.nx);
+      dir = 1; gi = i; il = ir = i;
+      if (b < nty - 1) { gj = (b + 1) * LW; jl = gj - 1; jr = gj; }
+      else { gj = 0; jl = L.ny - 1; jr = 0; }
+    }
+    R ql[NEQ], qr[NEQ], pl[NP1], pr[NP1];
+    const R* a = q + row_off(jl, L) + il;
+    const R* b = q + row_off(jr, L) + ir;
+#pragma unroll
+    for (int c = 0; c < NEQ; ++c) { ql[c] = a[c * L.pitch]; qr[c] = b[c * L.pitch]; }
+    prims_fast<S>(ql, (const R*)nullptr, P, pl);
+    prims_fast<S>(qr, (const R*)nullptr, P, pr);
+    const bool clean = S::cell_ok(ql, (const R*)nullptr, pl, P) &&
+                       S::cell_ok(qr, (const R*)nullptr, pr, P);
+    if (dir == 0) probe_next<S, R, 1>(ql, qr, pl, pr, clean, P, L, gi, gj, mx, key);
+    else probe_next<S, R, 2>(ql, qr, pl, pr, clean, P, L, gi, gj, my, key);
+  }
+  if (key != ~0ull) atomicMax(&ds->slot[slot][2], NKEY_MAX - key);
+  unsigned long long bx = Bits<R>::to(mx), by = Bits<R>::to(my);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long wx = __shfl_xor_sync(0xffffffffu, bx, o);
+    unsigned long long wy = __shfl_xor_sync(0xffffffffu, by, o);
+    bx = wx > bx ? wx : bx;
+    by = wy > by ? wy : by;
+  }
+  const int lane = tid & 31, wid = tid >> 5;
+  if (lane == 0) { sred[0][wid] = bx; sred[1][wid] = by; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < NT / 32; ++w) {
+      bx = sred[0][w] > bx ? sred[0][w] : bx;
+      by = sred[1][w] > by ? sred[1][w] : by;
+    }
+    atomicMax(&ds->slot[slot][0], bx);
+    atomicMax(&ds->slot[slot][1], by);
+  }
+}
+
 // one edge per lane of a grid line (see k_update_w): solve, optional
 // admissibility probe, wave limiter against lane +-1 (register shuffles),
 // correction flux; returns this lane's apdq / flux and the next lane's
@@ -817,7 +912,7 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
 // shared memory; the y pass adds the y term and both correction fluxes in
 // the reference order and writes q_new back to shared memory, from which
 // the tile is stored row-coalesced.
-template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS>
+template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUSED>
 __global__ void __launch_bounds__(NWARP * 32, (20 / NWARP > 0 ? 20 / NWARP : 1))
 k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
            const Layout L, const typename S::template Params<R> P, const StepArgs A,
@@ -888,6 +983,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     __syncthreads();
 
     // ---- y pass: warps walk columns; lane l = y-edge j0-1+l
+    const int nxv = min(LW, L.nx - i0), nyv = min(LW, L.ny - j0);
+    R nmx = (R)0, nmy = (R)0;             // FUSED: next state's max |s|
+    unsigned long long nkey = ~0ull;      // FUSED: next state's first bad edge
     for (int c = warp; c < LW; c += NWARP) {
       if (i0 + c >= L.nx) break;
       const int cl = lane * HW + c + 2, cr = cl + HW;
@@ -896,8 +994,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       line_edge<S, R, ORDER, LIM, CHECKS, 2, HC>(sQ, sA, sP, P, L, cl, cr, i0 + c, ej,
                                                   lane >= 1 && lane <= 30 && ej < L.ny_edges_y,
                                                   dtdy, key, ap, amn, fl, fr);
+      R qnew[NEQ];
+      const int rr = lane - 1, o = rr * LW + c;
       if (cell_lane) {
-        const int rr = lane - 1, o = rr * LW + c;
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
           R v = sX[m * (LW * LW) + o] - dtdy * (ap[m] + amn[m]);
@@ -906,10 +1005,94 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
             v = v - dtdy * (fr[m] - fl[m]);
           }
           sX[m * (LW * LW) + o] = v;
+          qnew[m] = v;
+        }
+      }
+      if (FUSED) {
+        // the next state's primitives (kept in the consumed dFx slots) and its
+        // y-edges inside this tile column: the lower cell is lane - 1
+        static_assert(!FUSED || (NPR <= NEQ && NAUX == 0), "FUSED epilogue layout");
+        R pn[NP1];
+        bool cok = false;
+        if (cell_lane) {
+          prims_fast<S>(qnew, (const R*)nullptr, P, pn);
+#pragma unroll
+          for (int k = 0; k < NPR; ++k) sX[(NEQ + k) * (LW * LW) + o] = pn[k];
+          cok = S::cell_ok(qnew, (const R*)nullptr, pn, P);
+        } else {
+#pragma unroll
+          for (int m = 0; m < NEQ; ++m) qnew[m] = (R)1;
+#pragma unroll
+          for (int k = 0; k < NPR; ++k) pn[k] = (R)1;
+        }
+        R ql[NEQ], pl[NP1];
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) ql[m] = __shfl_up_sync(0xffffffffu, qnew[m], 1);
+#pragma unroll
+        for (int k = 0; k < NPR; ++k) pl[k] = __shfl_up_sync(0xffffffffu, pn[k], 1);
+        const bool okl = __shfl_up_sync(0xffffffffu, cok, 1);
+        const int gj = j0 + rr;
+        if (cell_lane && rr < nyv) {
+          if (rr >= 1)
+            probe_next<S, R, 2>(ql, qnew, pl, pn, okl && cok, P, L, i0 + c, gj, nmy, nkey);
+          if (rr == 0 && gj == 0 && L.bcy != BC_PERIODIC)
+            probe_next<S, R, 2>(qnew, qnew, pn, pn, cok, P, L, i0 + c, 0, nmy, nkey);
+          if (rr == nyv - 1 && gj + 1 == L.ny && L.bcy != BC_PERIODIC)
+            probe_next<S, R, 2>(qnew, qnew, pn, pn, cok, P, L, i0 + c, L.ny, nmy, nkey);
         }
       }
     }
     __syncthreads();
+
+    if (FUSED) {
+      // x-edges inside each tile row of the next state: lane l = cell l
+      for (int r = warp; r < LW; r += NWARP) {
+        if (r >= nyv) break;
+        const int l = lane < LW ? lane : LW - 1;
+        const int o = r * LW + l;
+        R qc[NEQ], pc[NP1], ql[NEQ], pl[NP1];
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) qc[m] = sX[m * (LW * LW) + o];
+#pragma unroll
+        for (int k = 0; k < NPR; ++k) pc[k] = sX[(NEQ + k) * (LW * LW) + o];
+        const bool cok = S::cell_ok(qc, (const R*)nullptr, pc, P);
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) ql[m] = __shfl_up_sync(0xffffffffu, qc[m], 1);
+#pragma unroll
+        for (int k = 0; k < NPR; ++k) pl[k] = __shfl_up_sync(0xffffffffu, pc[k], 1);
+        const bool okl = __shfl_up_sync(0xffffffffu, cok, 1);
+        const int gj = j0 + r, gi = i0 + lane;
+        if (lane < nxv) {
+          if (lane >= 1)
+            probe_next<S, R, 1>(ql, qc, pl, pc, okl && cok, P, L, gi, gj, nmx, nkey);
+          if (lane == 0 && gi == 0 && L.bcx != BC_PERIODIC)
+            probe_next<S, R, 1>(qc, qc, pc, pc, cok, P, L, 0, gj, nmx, nkey);
+          if (lane == nxv - 1 && gi + 1 == L.nx && L.bcx != BC_PERIODIC)
+            probe_next<S, R, 1>(qc, qc, pc, pc, cok, P, L, L.nx, gj, nmx, nkey);
+        }
+      }
+      // CTA reduction of the next state's maxima into the other slot
+      __shared__ unsigned long long s_red2[2][NWARP];
+      unsigned long long bx = Bits<R>::to(nmx), by = Bits<R>::to(nmy);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        unsigned long long wx = __shfl_xor_sync(0xffffffffu, bx, off);
+        unsigned long long wy = __shfl_xor_sync(0xffffffffu, by, off);
+        bx = wx > bx ? wx : bx;
+        by = wy > by ? wy : by;
+      }
+      if (lane == 0) { s_red2[0][warp] = bx; s_red2[1][warp] = by; }
+      if (nkey != ~0ull) atomicMax(&ds->slot[A.cur ^ 1][2], NKEY_MAX - nkey);
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < NWARP; ++w) {
+          bx = s_red2[0][w] > bx ? s_red2[0][w] : bx;
+          by = s_red2[1][w] > by ? s_red2[1][w] : by;
+        }
+        atomicMax(&ds->slot[A.cur ^ 1][0], bx);
+        atomicMax(&ds->slot[A.cur ^ 1][1], by);
+      }
+    }
 
     // ---- row-coalesced store of the tile
     for (int idx = tid; idx < LW * LW; idx += NT) {

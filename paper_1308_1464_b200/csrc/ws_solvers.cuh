@@ -444,6 +444,53 @@ struct ShallowRoe {
 };
 
 // ---------------------------------------------------------------------------
+// scalar advection with constant velocity (u, v) — reference kernels.py:356-371
+//   one wave W = qr - ql at s = u (x) or v (y); amdq = min(s,0) W, apdq = max(s,0) W
+//   with Python's min/max on floats: min(s, 0.0) = 0.0 if 0.0 < s else s
+struct Advection {
+  static constexpr int NEQ = 1, NW = 1, NAUX = 0, NPR = 0;
+  static constexpr bool STATIC_SPEEDS = true;
+  template <int NI> __host__ __device__ static constexpr bool wzero(int, int) { return false; }
+  template <class R> struct Params { R u, v; };
+
+  template <class M, class R, class P>
+  __device__ static __forceinline__ void prims(const R*, const R*, const P&, R*, bool&) {}
+
+  template <int NI, class M, class R, class P>
+  __device__ static __forceinline__ void solve(const R* ql, const R* qr, const R*, const R*,
+                                               const R*, const R*, const P& p, R (&W)[NW][NEQ],
+                                               R (&s)[NW], R (&am)[NEQ], R (&ap)[NEQ], bool&) {
+    const R sp = (NI == 1) ? p.u : p.v;
+    const R jump = qr[0] - ql[0];
+    const R mn = ((R)0 < sp) ? (R)0 : sp;
+    const R mx = ((R)0 > sp) ? (R)0 : sp;
+    W[0][0] = jump;
+    s[0] = sp;
+    am[0] = mn * jump;
+    ap[0] = mx * jump;
+  }
+
+  template <int NI, class M, class R, class P>
+  __device__ static __forceinline__ int probe(const R* ql, const R* qr, const R*, const R*,
+                                              const R*, const R*, const P& p, R& smax, bool&) {
+    smax = fabs((NI == 1) ? p.u : p.v);
+    return finite_code<R, NEQ>(ql, qr);
+  }
+
+  template <class R, class P>
+  __device__ static __forceinline__ bool cell_ok(const R* q, const R*, const R*, const P&) {
+    return all_finite<R, NEQ>(q);
+  }
+  template <int NI, class M, class R, class P>
+  __device__ static __forceinline__ int probe_fast(const R*, const R*, const R*, const R*,
+                                                   const R*, const R*, const P& p, R& smax,
+                                                   bool&) {
+    smax = fabs((NI == 1) ? p.u : p.v);
+    return 0;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // wave limiters (oracle phi(); LeVeque 2002 §6.9)
 template <int LIM, class R> __device__ __forceinline__ R limiter_phi(R th) {
   if (LIM == LIM_MINMOD) return nmax((R)0, nmin((R)1, th));

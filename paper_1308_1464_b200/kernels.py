@@ -53,9 +53,9 @@ class KernelDescriptor:
     arithmetic_intensity: Fraction
 
 
-# reference kernels.py:282-287 (the advection kernel is not part of the
-# north-star path) plus the two north-star solvers the reference lacks
+# reference kernels.py:282-287 plus the two north-star solvers the reference lacks
 DESCRIPTORS: dict[str, KernelDescriptor] = {
+    "advection": KernelDescriptor("advection", 1, 1, 0, Fraction(1, 3)),
     "acoustics-const": KernelDescriptor("acoustics-const", 3, 2, 0, Fraction(4, 5)),
     "acoustics-var": KernelDescriptor("acoustics-var", 3, 2, 2, Fraction(1)),
     "euler": KernelDescriptor("euler", 4, 3, 0, Fraction(1)),
@@ -68,6 +68,7 @@ KERNEL_NAMES = tuple(DESCRIPTORS)
 # (reference kernels.py:338-349, 428-430, 473-494)
 _FINITE = [("non-finite left state", "left"), ("non-finite right state", "right")]
 STAGES = {
+    "advection": _FINITE,
     "acoustics-const": _FINITE,
     "acoustics-var": _FINITE + [("nonpositive density on left side", "left"),
                                 ("nonpositive sound speed on left side", "left"),
@@ -134,6 +135,8 @@ class Kernel:
 
     def native_params(self) -> list[float]:
         p = self.params
+        if self.name == "advection":
+            return [p["u"], p["v"], 0.0, 0.0]
         if self.name == "acoustics-const":
             return [p["rho"], p["bulk"], 0.0, 0.0]
         if self.name in ("euler", "euler-hlle"):
@@ -208,11 +211,16 @@ class Kernel:
 def make_kernel(name: str, **params) -> Kernel:
     """Bind a solver to parameters (reference kernels.py:589-633).
 
-    acoustics-const(rho, bulk), acoustics-var() reading per-cell (rho, c)
+    advection(u, v), acoustics-const(rho, bulk), acoustics-var() reading per-cell (rho, c)
     from aux, euler(gamma=1.4), euler-hlle(gamma=1.4),
     shallow-water-roe(grav=9.81).
     """
-    if name == "acoustics-const":
+    if name == "advection":
+        u, v = float(params.pop("u")), float(params.pop("v"))
+        if not (math.isfinite(u) and math.isfinite(v)):
+            raise KernelError(f"non-finite advection velocity ({u}, {v})")
+        bound = {"u": u, "v": v}
+    elif name == "acoustics-const":
         p = AcousticsParams(float(params.pop("rho")), float(params.pop("bulk")))
         bound = {"rho": p.density, "bulk": p.bulk}
     elif name == "acoustics-var":

@@ -57,6 +57,9 @@ STEP_CASES = [
     ("acoustics-var-mix", "acoustics-var", {}, 31, 40, 6, "periodic", "extrapolate", 3),
     ("euler-per", "euler", {"gamma": 1.4}, 37, 29, 6, "periodic", "periodic", 4),
     ("euler-ext", "euler", {"gamma": 1.4}, 45, 21, 6, "extrapolate", "extrapolate", 5),
+    ("advection-per", "advection", {"u": 0.7, "v": -1.3}, 33, 26, 8, "periodic", "periodic", 6),
+    ("advection-ext", "advection", {"u": -0.4, "v": 2.0}, 20, 31, 8, "extrapolate",
+     "extrapolate", 7),
 ]
 
 
@@ -98,12 +101,18 @@ def reference_steps(W):
 
 def reference_kernels(W):
     from wavesweep.kernels import (AcousticsParams, Direction, EulerParams, rp_acoustics_const,
-                                   rp_acoustics_var, rp_euler)
+                                   rp_acoustics_var, rp_advection, rp_euler)
     from wavesweep.oracles import random_gas_states
     rng = np.random.default_rng(20240817)
     out = {}
     n = 64
     for dname, d in (("x", Direction.X), ("y", Direction.Y)):
+        ql, qr = rng.normal(size=(2, 1, n))
+        r = rp_advection(d, ql, qr, 1.25, -0.75)
+        out[f"advection-{dname}"] = dict(ql=ql.tolist(), qr=qr.tolist(),
+                                          params={"u": 1.25, "v": -0.75},
+                                          amdq=r.amdq.tolist(), apdq=r.apdq.tolist(),
+                                          speeds=r.speeds.tolist(), waves=r.waves.tolist())
         ql, qr = rng.normal(size=(2, 3, n))
         r = rp_acoustics_const(d, ql, qr, AcousticsParams(1.7, 2.9))
         out[f"acoustics-const-{dname}"] = dict(ql=ql.tolist(), qr=qr.tolist(),

@@ -7,13 +7,14 @@ import numpy as np
 from oracle import wavestep_oracle as O
 
 PARAMS = {
+    "advection": {"u": 0.7, "v": -1.3},
     "acoustics-const": {"rho": 1.3, "bulk": 2.1},
     "acoustics-var": {},
     "euler": {"gamma": 1.4},
     "euler-hlle": {"gamma": 1.4},
     "shallow-water-roe": {"grav": 9.81},
 }
-SHAPES = {"acoustics-const": (3, 0), "acoustics-var": (3, 2), "euler": (4, 0),
+SHAPES = {"advection": (1, 0), "acoustics-const": (3, 0), "acoustics-var": (3, 2), "euler": (4, 0),
           "euler-hlle": (4, 0), "shallow-water-roe": (3, 0)}
 
 
@@ -26,7 +27,10 @@ def random_state(name, nx, ny, seed=0, dtype=np.float64, smooth=True):
     xx, yy = np.meshgrid((np.arange(nx) + 0.5) / nx, (np.arange(ny) + 0.5) / ny, indexing="ij")
     bump = np.exp(-40.0 * ((xx - 0.4) ** 2 + (yy - 0.55) ** 2)) if smooth else 0.0
     I = (slice(None), slice(2, nx + 2), slice(2, ny + 2))
-    if name in ("acoustics-const", "acoustics-var"):
+    if name == "advection":
+        q[I] = rng.normal(0.0, 0.1, (1, nx, ny))
+        q[0, 2:nx + 2, 2:ny + 2] += bump
+    elif name in ("acoustics-const", "acoustics-var"):
         q[I] = rng.normal(0.0, 0.1, (3, nx, ny))
         q[0, 2:nx + 2, 2:ny + 2] += bump
         if naux:

@@ -14,7 +14,8 @@ from oracle import wavestep_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-SOLVERS = ["acoustics-const", "acoustics-var", "euler", "euler-hlle", "shallow-water-roe"]
+SOLVERS = ["advection", "acoustics-const", "acoustics-var", "euler", "euler-hlle",
+           "shallow-water-roe"]
 BCS = [("extrapolate", "extrapolate"), ("periodic", "periodic"), ("periodic", "extrapolate")]
 
 
@@ -104,6 +105,8 @@ def test_inadmissible_cell_reports_reference_location(name):
     q, aux = random_state(name, nx, ny, 8)
     if name.startswith("acoustics"):
         q[1, 2 + 5, 2 + 3] = np.nan
+    elif name == "advection":
+        q[0, 2 + 5, 2 + 3] = np.inf
     else:
         q[0, 2 + 5, 2 + 3] = -1.0
     with pytest.raises(O.OracleError) as oe:
@@ -183,3 +186,79 @@ def test_dt_max_remaining_and_fixed_dt_match_oracle():
                                 limiter="superbee", **kw)
         assert [r.dt for r in oreps] == [r[0] for r in res.reports]
         assert same_bits(oq, dq)
+
+
+# ---------------------------------------------------------------------------
+# the device against the REFERENCE's own outputs (tests/golden, generated by
+# running wavesweep itself) — no oracle in between
+
+import hashlib
+import json
+import os
+
+GOLD = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                   "reference_golden.json")))
+
+
+def _hash(q):
+    return hashlib.sha256((np.asfortranarray(q, dtype=np.float64) + 0.0).tobytes(order="F")).hexdigest()
+
+
+@pytest.mark.parametrize("name", sorted(GOLD["steps"]))
+def test_device_matches_reference_golden(name):
+    from paper_1308_1464_b200 import DeviceGrid, _abi, make_kernel
+    c = GOLD["steps"][name]
+    if name == "c1-full":
+        from paper_1308_1464_b200 import configs
+        q, aux = configs.c1_acoustics().q, None
+    else:
+        q, aux = random_state(c["kernel"], c["nx"], c["ny"], c["seed"])
+    g = DeviceGrid(c["nx"], c["ny"], c["dx"], c["dy"], make_kernel(c["kernel"], **c["params"]),
+                   order=1, bc_x=c["bc_x"], bc_y=c["bc_y"])
+    g.upload(q, aux)
+    g.run(c["steps"], _abi.make_ctl(0.9))
+    res = g.poll()
+    out = g.download()
+    g.close()
+    assert [r[0] for r in res.reports] == c["dts"]
+    assert [r[2] for r in res.reports] == c["msx"]
+    assert [r[3] for r in res.reports] == c["msy"]
+    assert _hash(out) == c["q_sha256"]
+
+
+@pytest.mark.parametrize("key", sorted(GOLD["kernels"]))
+def test_device_kernel_solve_matches_reference(key):
+    from paper_1308_1464_b200 import Direction, make_kernel
+    c = GOLD["kernels"][key]
+    name, d = key.rsplit("-", 1)
+    k = make_kernel(name, **c["params"])
+    r = k.solve(Direction.X if d == "x" else Direction.Y, np.array(c["ql"]), np.array(c["qr"]),
+                np.array(c["auxl"]) if "auxl" in c else None,
+                np.array(c["auxr"]) if "auxr" in c else None)
+    assert np.array_equal(r.amdq, np.array(c["amdq"]))
+    assert np.array_equal(r.apdq, np.array(c["apdq"]))
+    assert np.array_equal(r.speeds, np.array(c["speeds"]))
+    assert np.array_equal(r.waves, np.array(c["waves"]))
+
+
+@pytest.mark.parametrize("key", sorted(GOLD["errors"]))
+def test_device_error_text_matches_reference(key):
+    from paper_1308_1464_b200 import (BoundaryCondition, GridSpec, SimulationConfig, StateField,
+                                      AuxField, SweepError, TimestepController, step)
+    from paper_1308_1464_b200.kernels import DESCRIPTORS
+    c = GOLD["errors"][key]
+    q, aux = random_state(c["kernel"], c["nx"], c["ny"], c["seed"])
+    q[c["comp"], 2 + 5, 2 + 3] = float(eval(c["value"], {"nan": np.nan, "inf": np.inf}))
+    d = DESCRIPTORS[c["kernel"]]
+    spec = GridSpec(nx=c["nx"], ny=c["ny"], dx=1 / c["nx"], dy=1 / c["ny"], num_eqn=d.num_eqn,
+                    num_aux=d.num_aux)
+    st, ax = StateField(spec), AuxField(spec)
+    st.data[...] = q
+    if aux is not None:
+        ax.data[...] = aux
+    cfg = SimulationConfig(spec=spec, kernel=c["kernel"], ic="x", num_steps=1,
+                           bc_x=BoundaryCondition.EXTRAPOLATE,
+                           bc_y=BoundaryCondition.EXTRAPOLATE, kernel_params=c["params"])
+    with pytest.raises(SweepError) as e:
+        step(st, ax, cfg, TimestepController(0.9))
+    assert str(e.value) == c["message"]
