@@ -277,11 +277,19 @@ def gpu_arm(args):
                 "peak_kind": peak_kind, "kernel_ms": upd_ms,
                 "speeds_kernel_ms": statistics.mean(t_spd) if dyn else 0.0,
                 "algorithmic_bytes_per_cell": bpc}
+    roofline["kernel"] = "k_update_w" if case.kernel not in ("euler", "euler-hlle") else "k_update"
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                roofline["traffic"] = json.load(f).get(args.config, {}).get("bytes_per_launch")
+                pr = json.load(f).get(args.config, {})
+            roofline["traffic"] = pr.get("bytes_per_launch")
+            if pr.get("fp64_pipe_active_pct") is not None:
+                # the binding resource: FP64 pipe, from the ncu capture
+                roofline["fp64"] = {"pipe_active_frac_ncu": pr["fp64_pipe_active_pct"] / 100.0,
+                                    "instr_per_cell": pr.get("fp64_instr_per_cell_approx"),
+                                    "peak_instr_per_s": pr.get("fp64_peak_instr_per_s"),
+                                    "peak_source": pr.get("fp64_peak_source")}
         except Exception:
             pass
 

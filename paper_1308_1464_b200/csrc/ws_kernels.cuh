@@ -929,13 +929,19 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   R* sX = sP + NPR * HC;          // [2*NEQ][LW*LW]: q1 and dFx, later q_new
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const Ctl ctl = step_control<R>(A, ds, !CHECKS);
-  if (!ctl.skip) {
-    const int i0 = blockIdx.x * LW, j0 = blockIdx.y * LW;
-    const R dtdx = (R)(ctl.dt / A.dx);
-    const R dtdy = (R)(ctl.dt / A.dy);
-    unsigned long long key = ~0ull;
-
+  // thread 0 evaluates the step control (dt from this step's maxima, 5
+  // dependent divisions) while the other threads stage the tile; the result
+  // is handed over at the post-staging barrier
+  __shared__ Ctl s_ctl;
+  __shared__ R s_dtd[2];
+  const int i0 = blockIdx.x * LW, j0 = blockIdx.y * LW;
+  if (tid == 0) {
+    const Ctl c0 = step_control<R>(A, ds, !CHECKS);
+    s_ctl = c0;
+    s_dtd[0] = (R)(c0.dt / A.dx);
+    s_dtd[1] = (R)(c0.dt / A.dy);
+  }
+  {
     // ---- stage tile + 2-cell halo (BC by index mapping), per-cell primitives
     const bool inner = i0 >= 2 && i0 + LW + 2 <= L.nx && j0 >= 2 && j0 + LW + 2 <= L.ny;
     for (int idx = tid; idx < HC; idx += NT) {
@@ -957,7 +963,13 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
       }
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  const Ctl ctl = s_ctl;
+  if (!ctl.skip) {
+    const R dtdx = s_dtd[0];
+    const R dtdy = s_dtd[1];
+    unsigned long long key = ~0ull;
 
     const bool cell_lane = lane >= 1 && lane <= LW;
 
