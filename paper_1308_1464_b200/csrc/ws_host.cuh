@@ -26,7 +26,12 @@ template <class S, class R, int ORDER> struct TileCfg {
 template <class R> struct TileCfg<EulerRoe, R, 2> {
   static constexpr int TX = 32, TY = 8, NT = 256;
 };
-constexpr int SPD_TX = 32, SPD_TY = 16, SPD_NT = 256;
+constexpr int SPD_TX = 32, SPD_NT = 256;
+// pre-pass tile height: 32 rows (4 cells per thread) when the staged halo tile
+// fits the 48 KB static shared-memory window, else 16
+template <class S, class R> constexpr int spd_ty() {
+  return (S::NEQ + S::NAUX + S::NPR) * 33 * 33 * sizeof(R) <= 46 * 1024 ? 32 : 16;
+}
 
 struct Ops {
   void (*speeds)(ws_handle*, const void* q, int cur, cudaStream_t);
@@ -173,8 +178,9 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   static const P& prm(ws_handle* h) { return *reinterpret_cast<const P*>(h->params.data()); }
 
   static void speeds(ws_handle* h, const void* q, int cur, cudaStream_t st) {
-    dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + SPD_TY - 1) / SPD_TY);
-    k_speeds<S, R, SPD_TX, SPD_TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(
+    constexpr int TY = spd_ty<S, R>();
+    dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + TY - 1) / TY);
+    k_speeds<S, R, SPD_TX, TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(
         static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
     h->launches++;
   }

@@ -80,8 +80,8 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   constexpr int KC = TX * TY / NT;
   static_assert(KC * NT == TX * TY, "tile must be a multiple of the block");
   __shared__ R sQ[NEQ][HC];
-  __shared__ R sA[NA1][HC];
-  __shared__ R sP[NP1][HC];
+  __shared__ R sA[NA1][NAUX > 0 ? HC : 1];
+  __shared__ R sP[NP1][NPR > 0 ? HC : 1];
   __shared__ unsigned long long sred[2][NT / 32];
   __shared__ int s_skip;
   const int tid = threadIdx.x;

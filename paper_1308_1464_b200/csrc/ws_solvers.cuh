@@ -257,7 +257,8 @@ struct EulerRoe {
     roe<NI, M>(pl, pr, p, uh, vh, hh, kin, c2, ok);
     if (!(c2 > (R)0)) { smax = (R)0; return 7; }
     R ch = M::sqrt_(c2, ok);
-    smax = nmax(nmax(fabs(uh - ch), fabs(uh)), fabs(uh + ch));
+    // |uh| never exceeds max(|uh-c|, |uh+c|) for c >= 0 (rounding is monotone)
+    smax = nmax(fabs(uh - ch), fabs(uh + ch));
     return 0;
   }
 };
@@ -391,7 +392,9 @@ struct ShallowRoe {
     R d0 = qr[0] - ql[0];
     R d1 = qr[NI] - ql[NI];
     R d2 = qr[TI] - ql[TI];
-    R i2c = M::div((R)0.5, ch, ok);
+    // 0.5/c == 0.5 * (1/c) bit for bit (power-of-two scaling commutes with
+    // rounding), and the reciprocal is the cheaper sequence
+    R i2c = (R)0.5 * M::rcp(ch, ok);
     R s1 = uh - ch, s3 = uh + ch;
     R a1 = (s3 * d0 - d1) * i2c;
     R a2 = d2 - vh * d0;
@@ -438,7 +441,8 @@ struct ShallowRoe {
                                                    R& smax, bool& ok) {
     R uh, vh, ch;
     roe<NI, M>(ql, qr, pl, pr, p, uh, vh, ch, ok);
-    smax = nmax(nmax(fabs(uh - ch), fabs(uh)), fabs(uh + ch));
+    // |uh| never exceeds max(|uh-c|, |uh+c|) for c >= 0 (rounding is monotone)
+    smax = nmax(fabs(uh - ch), fabs(uh + ch));
     return 0;
   }
 };
