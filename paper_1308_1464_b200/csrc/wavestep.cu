@@ -285,6 +285,8 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   if (const char* v = std::getenv("WS_EXP")) h->exp = std::atoi(v);
   h->line_kernel = h->neq <= 3;   // 4-component systems exceed 1 CTA/SM of line smem
   if (const char* v = std::getenv("WS_KERNEL")) h->line_kernel = std::strcmp(v, "tile") != 0;
+  if (const char* v = std::getenv("WS_SPEEDS")) h->speeds_smem = std::strcmp(v, "smem") == 0;
+  if (const char* v = std::getenv("WS_SPW")) h->spw = std::atoi(v);
   {
     const char* v = std::getenv("WS_FUSE");
     const bool env_on = v && std::atoi(v) != 0, env_off = v && std::atoi(v) == 0;

@@ -183,6 +183,136 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
 }
 
 // --------------------------------------------------------------------------
+// CFL / admissibility pre-pass, register form (the default).  One warp owns a
+// strip of 31 edge columns x KC edge rows: lane l holds cell column
+// x0 - 1 + l, so the x-edge left of its cell pairs it with lane l-1 (one
+// shuffle per used field), and the warp marches up its rows keeping the
+// previous row's cell in registers for the y-edge below.  No shared-memory
+// staging, no per-cell index division; prims are evaluated (31+1)/31 x
+// (KC+1)/KC times per cell.  Per edge, the check-free probe runs when both
+// cells are admissible — exactly what the checked probe computes for them —
+// and the checked probe (reference stage order) otherwise.
+template <class S, class R, int KC, int NWS, int UNR, int MINB>
+__global__ void __launch_bounds__(NWS * 32, MINB)
+k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
+           const typename S::template Params<R> P, const int cur, DevState* __restrict__ ds) {
+  constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  __shared__ unsigned long long sred[2][NWS];
+  __shared__ int s_skip;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_skip = __ldcg(&ds->err) | __ldcg(&ds->finished);
+  __syncthreads();
+  if (s_skip) return;
+  const int ci = blockIdx.x * 31 - 1 + lane;                 // this lane's cell column
+  const int gi = map_i(ci < L.nx ? ci : L.nx, L);
+  const int jb = (blockIdx.y * NWS + wid) * KC;              // first edge row of the warp
+  const bool xcol = lane >= 1 && ci <= L.nx;                  // owns x-edge ci
+  const bool ycol = lane >= 1 && ci < L.nx;                   // owns y-edge column ci
+
+  auto load = [&](int r, R (&qc)[NEQ], R (&ac)[NA1]) {
+    const int gj = map_j(r < L.ny ? r : L.ny, L);
+    const R* src = q + row_off(gj, L) + gi;
+#pragma unroll
+    for (int c = 0; c < NEQ; ++c) qc[c] = src[c * L.pitch];
+    if (NAUX > 0) {
+      const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) ac[c] = asrc[c * L.pitch];
+    }
+  };
+  auto cell = [&](const R (&qc)[NEQ], const R (&ac)[NA1], R (&pc)[NP1]) -> bool {
+    if (NPR > 0) prims_fast<S>(qc, ac, P, pc);
+    return S::cell_ok(qc, ac, pc, P);
+  };
+
+  R mx = (R)0, my = (R)0;
+  unsigned long long key = ~0ull;
+  auto probe = [&](auto ni_tag, const R* ql, const R* qr, const R* pl, const R* pr,
+                   const R* al, const R* ar, bool clean, int dir, int ei, int ej) -> R {
+    constexpr int NI = decltype(ni_tag)::value;
+    R sm;
+    bool ok = true;
+    int code;
+    if (clean) {
+      code = S::template probe_fast<NI, FastMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+      if (!ok) code = S::template probe_fast<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    } else {
+      code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    }
+    if (code) {
+      unsigned long long k = err_key(dir, ei, L.j_off + ej, (code & 0xff) - 1, code >> 8, L.nx);
+      key = k < key ? k : key;
+    }
+    return sm;
+  };
+  using NX = std::integral_constant<int, 1>;
+  using NY = std::integral_constant<int, 2>;
+
+  // edge rows this warp owns: [jb, jb + nk), nothing past the last edge row
+  const int rows = L.ny > L.ny_edges_y ? L.ny : L.ny_edges_y;
+  const int nk = rows - jb < KC ? rows - jb : KC;
+  if (nk > 0) {
+    R qp[NEQ], ap[NA1], pp[NP1], qn[NEQ], an[NA1];
+    load(jb - 1, qp, ap);
+    load(jb, qn, an);                       // next row in flight while this one computes
+    bool okp = cell(qp, ap, pp);
+#pragma unroll UNR
+    for (int k = 0; k < KC; ++k) {
+      if (k >= nk) break;
+      const int r = jb + k;
+      R qc[NEQ], ac[NA1], pc[NP1];
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) qc[c] = qn[c];
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) ac[c] = an[c];
+      load(r + 1, qn, an);
+      const bool okc = cell(qc, ac, pc);
+      // left neighbour (lane - 1) of the current row
+      R ql[NEQ], al[NA1], pl[NP1];
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) ql[c] = __shfl_up_sync(0xffffffffu, qc[c], 1);
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) al[c] = __shfl_up_sync(0xffffffffu, ac[c], 1);
+#pragma unroll
+      for (int c = 0; c < NPR; ++c) pl[c] = __shfl_up_sync(0xffffffffu, pc[c], 1);
+      const bool okl = __shfl_up_sync(0xffffffffu, okc, 1);
+      if (xcol && r < L.ny)
+        mx = nmax(mx, probe(NX{}, ql, qc, pl, pc, al, ac, okl && okc, 0, ci, r));
+      if (ycol && r < L.ny_edges_y)
+        my = nmax(my, probe(NY{}, qp, qc, pp, pc, ap, ac, okp && okc, 1, ci, r));
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) qp[c] = qc[c];
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) ap[c] = ac[c];
+#pragma unroll
+      for (int c = 0; c < NPR; ++c) pp[c] = pc[c];
+      okp = okc;
+    }
+  }
+  if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
+  unsigned long long bx = Bits<R>::to(mx), by = Bits<R>::to(my);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long wx = __shfl_xor_sync(0xffffffffu, bx, o);
+    unsigned long long wy = __shfl_xor_sync(0xffffffffu, by, o);
+    bx = wx > bx ? wx : bx;
+    by = wy > by ? wy : by;
+  }
+  if (lane == 0) { sred[0][wid] = bx; sred[1][wid] = by; }
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int w = 1; w < NWS; ++w) {
+      bx = sred[0][w] > bx ? sred[0][w] : bx;
+      by = sred[1][w] > by ? sred[1][w] : by;
+    }
+    atomicMax(&ds->slot[cur][0], bx);
+    atomicMax(&ds->slot[cur][1], by);
+  }
+}
+
+// --------------------------------------------------------------------------
 // commit: run by thread 0 of the last CTA of an update kernel
 template <class R>
 __device__ __forceinline__ void commit_step(DevState* ds, const StepArgs& A, const Ctl& c,
