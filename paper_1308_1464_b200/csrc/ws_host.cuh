@@ -199,7 +199,9 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
         case 1: speeds_w<16, 4, 1, MB>(h, q, cur, st); break;
         case 2: speeds_w<8, 8, 1, MB / 2>(h, q, cur, st); break;
         case 3: speeds_w<8, 4, 2, MB>(h, q, cur, st); break;
-        case 4: speeds_w<32, 2, 1, MB * 2>(h, q, cur, st); break;
+        case 4: speeds_w<8, 4, 1, MB * 3 / 4>(h, q, cur, st); break;
+        case 5: speeds_w<8, 1, 1, MB * 4>(h, q, cur, st); break;
+        case 6: speeds_w<16, 1, 1, MB * 4>(h, q, cur, st); break;
         default: speeds_w<8, 4, 1, MB>(h, q, cur, st); break;
       }
     }
