@@ -200,7 +200,8 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   __shared__ unsigned long long sred[2][NWS];
   __shared__ int s_skip;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // warp index via lane-0 broadcast = known warp-uniform (see k_update_w)
+  const int tid = threadIdx.x, lane = tid & 31, wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
   if (tid == 0) s_skip = __ldcg(&ds->err) | __ldcg(&ds->finished);
   __syncthreads();
   if (s_skip) return;
@@ -1058,7 +1059,10 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   R* sP = sA + NAUX * HC;
   R* sX = sP + NPR * HC;          // [2*NEQ][LW*LW]: q1 and dFx, later q_new
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp index through a lane-0 broadcast: the compiler then treats it as
+  // warp-uniform, so the line loops below (trip count depends on it) keep
+  // their shuffles plain instead of divergent-warp collectives
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   // thread 0 evaluates the step control (dt from this step's maxima, 5
   // dependent divisions) while the other threads stage the tile; the result
   // is handed over at the post-staging barrier
