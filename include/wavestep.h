@@ -172,6 +172,13 @@ int ws_fill_ghost(double* data, int32_t ncomp, int32_t nx, int32_t ny, int32_t b
 /* number of kernel launches this handle has issued (bench evidence) */
 int64_t ws_launch_count(const ws_handle* h);
 
+/* Diagnostics (no reference counterpart): with WS_TRACE=1 in the environment
+ * at ws_create, every CTA of the CFL pre-pass (region 0) and of the update
+ * kernel (region 1) writes {start ns, end ns, smid, block} (%globaltimer) on
+ * each launch.  Copies up to `cap` words of the last launch's records;
+ * *n = 0 when tracing is off. */
+int ws_trace(ws_handle* h, uint64_t* out, int64_t cap, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

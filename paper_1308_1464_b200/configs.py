@@ -137,7 +137,7 @@ def c5_bumps(nx: int = 16384, ny: int | None = None, seed: int = 0, steps: int =
     centres y offset by the square index).  Each bump is separable,
     exp(-(x-xk)^2/2w^2) * exp(-(y-yk)^2/2w^2), summed bump by bump in draw
     order.  With ``device`` set the sum runs in torch on that device and
-    the returned Case carries the device tensor in meta["q_dev_interior"].
+    the returned Case carries the device tensor in meta["h_dev"] ([j][i], fp64).
     """
     ny = nx if ny is None else ny
     squares = max(1, ny // nx)

@@ -176,6 +176,8 @@ void compute_layout(ws_handle* h) {
   L.hi = d.rows_hi == WS_ROWS_MEMORY ? ROWS_MEMORY : ROWS_BC;
   L.j_off = d.j_offset;
   L.nx_glob = d.nx;
+  L.trace = nullptr;
+  L.trace_cap = 0;
   L.pitch = pitch_for(d.nx, h->esz);
   L.rstride = (long long)h->neq * L.pitch;
   L.astride = (long long)h->naux * L.pitch;
@@ -287,6 +289,7 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   if (const char* v = std::getenv("WS_KERNEL")) h->line_kernel = std::strcmp(v, "tile") != 0;
   if (const char* v = std::getenv("WS_SPEEDS")) h->speeds_smem = std::strcmp(v, "smem") == 0;
   if (const char* v = std::getenv("WS_SPW")) h->spw = std::atoi(v);
+  if (const char* v = std::getenv("WS_PDL")) h->pdl = std::atoi(v) != 0;
   {
     const char* v = std::getenv("WS_FUSE");
     const bool env_on = v && std::atoi(v) != 0, env_off = v && std::atoi(v) == 0;
@@ -302,6 +305,18 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   }
   cudaMemsetAsync(h->borders, 0, h->border_bytes, h->stream);
   h->ops.prepare();
+  if (const char* v = std::getenv("WS_TRACE")) {
+    if (std::atoi(v) != 0) {
+      // diagnostics: one {start, end, smid, block} record per CTA of the pre-pass
+      // (region 0) and the update kernel (region 1), overwritten every launch
+      const long long cap = ((long long)(d->nx + 31) / 29 + 1) * ((d->ny + 31) / 16 + 1);
+      if (cudaMalloc(&h->trace, sizeof(unsigned long long) * 8 * cap) == cudaSuccess) {
+        cudaMemsetAsync(h->trace, 0, sizeof(unsigned long long) * 8 * cap, h->stream);
+        h->L.trace = h->trace;
+        h->L.trace_cap = (int)cap;
+      }
+    }
+  }
   if (const char* v = std::getenv("WS_TILE")) h->variant = std::atoi(v);
   // zero everything once so ghost rows / padding are defined
   cudaMemsetAsync(h->q[0], 0, qb, h->stream);
@@ -323,6 +338,7 @@ void ws_destroy(ws_handle* h) {
   if (h->own_ds && h->ds) cudaFree(h->ds);
   if (h->stage) cudaFree(h->stage);
   if (h->borders) cudaFree(h->borders);
+  if (h->trace) cudaFree(h->trace);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -594,6 +610,19 @@ int ws_sync(ws_handle* h) {
 }
 
 int64_t ws_launch_count(const ws_handle* h) { return h ? h->launches : 0; }
+
+int ws_trace(ws_handle* h, uint64_t* out, int64_t cap, int64_t* n) {
+  if (!h || !out || !n) return WS_ERR_CONFIG;
+  *n = 0;
+  if (!h->trace) return WS_OK;
+  const int64_t words = 8ll * h->L.trace_cap;
+  const int64_t m = cap < words ? cap : words;
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e == cudaSuccess) e = cudaMemcpy(out, h->trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(h, e, "ws_trace");
+  *n = m;
+  return WS_OK;
+}
 
 }  // extern "C"
 

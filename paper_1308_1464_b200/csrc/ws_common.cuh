@@ -34,7 +34,35 @@ struct Layout {
   long long pitch;        // elements per component row
   long long rstride;      // elements per grid row of q   (num_eqn * pitch)
   long long astride;      // elements per grid row of aux (num_aux * pitch)
+  unsigned long long* trace;  // CTA timeline (WS_TRACE=1 diagnostics) or null
+  int trace_cap;              // CTAs per traced kernel
 };
+
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start before its predecessor in
+// the stream finishes; griddepcontrol.wait blocks until the predecessor has
+// completed and flushed, launch_dependents lets the successor launch once
+// every CTA of this grid has issued it.  No-ops for plain launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// CTA timeline record (diagnostics): {start ns, end ns, smid, linear block}
+// written by thread 0; region 0 = CFL pre-pass, region 1 = update kernel
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_cta(const Layout& L, int region, unsigned long long t0) {
+  const int b = blockIdx.y * gridDim.x + blockIdx.x;
+  if (L.trace == nullptr || b >= L.trace_cap) return;
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  unsigned long long* r = L.trace + 4ull * ((unsigned long long)region * L.trace_cap + b);
+  r[0] = t0; r[1] = gtimer(); r[2] = smid; r[3] = b;
+}
 
 struct Report { double dt, cfl, msx, msy; };
 

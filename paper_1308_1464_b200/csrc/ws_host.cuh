@@ -77,10 +77,12 @@ struct ws_handle {
   bool fused = false;           // next-step CFL maxima computed in the update epilogue
   bool need_prepass = true;     // fused mode: slot of the current state not yet filled
   int* borders = nullptr;       // tile-border counters of the fused epilogue
+  unsigned long long* trace = nullptr;   // CTA timeline buffer (WS_TRACE=1)
   int exp = 0;                  // WS_EXP timing-study switches
   bool line_kernel = true;      // warp-per-line k_update_w (else the smem-tile k_update)
   bool speeds_smem = false;     // shared-memory tile pre-pass (else the register k_speeds_w)
   int spw = 0;                  // register pre-pass geometry variant (experiments)
+  bool pdl = true;              // programmatic dependent launch of the step kernels
   size_t border_bytes = 0;
   std::string err;
 };
@@ -171,6 +173,24 @@ bool variant_update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cu
   return false;
 }
 
+// kernel launch, with programmatic dependent launch when enabled (the two
+// per-step kernels: k_speeds_w and k_update_w, see ws_common.cuh pdl_*)
+template <class... KArgs, class... Args>
+inline void launch(ws_handle* h, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = h->pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // ---- typed launchers -----------------------------------------------------
 template <class S, class R, int ORDER, int LIM> struct Impl {
   using P = typename S::template Params<R>;
@@ -183,8 +203,8 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   template <int KC, int NW, int UNR, int MINB>
   static void speeds_w(ws_handle* h, const void* q, int cur, cudaStream_t st) {
     dim3 grid((h->L.nx + 1 + 30) / 31, (h->L.ny + 1 + KC * NW - 1) / (KC * NW));
-    k_speeds_w<S, R, KC, NW, UNR, MINB><<<grid, NW * 32, 0, st>>>(
-        static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
+    launch(h, k_speeds_w<S, R, KC, NW, UNR, MINB>, grid, dim3(NW * 32), 0, st,
+           static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
   }
 
   static void speeds(ws_handle* h, const void* q, int cur, cudaStream_t st) {
@@ -244,8 +264,8 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     auto k = kern_w<CHECKS, FUSED>();
     const size_t smem = LineGeom<S>::template smem_bytes<R>();
     dim3 grid((h->L.nx + 28) / 29, (h->L.ny + 28) / 29);
-    k<<<grid, LNW * 32, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
-                                    static_cast<R*>(qn), h->L, prm(h), a, h->ds);
+    launch(h, k, grid, dim3(LNW * 32), smem, st, static_cast<const R*>(q),
+           static_cast<const R*>(h->aux), static_cast<R*>(qn), h->L, prm(h), a, h->ds);
     h->launches++;
     if (FUSED) {
       // tile-border edges of the new state, into the next step's slot

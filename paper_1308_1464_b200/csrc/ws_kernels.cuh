@@ -202,6 +202,11 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   __shared__ int s_skip;
   // warp index via lane-0 broadcast = known warp-uniform (see k_update_w)
   const int tid = threadIdx.x, lane = tid & 31, wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const unsigned long long t_start = L.trace ? gtimer() : 0ull;
+  // everything below reads the previous update's output; the next update may
+  // launch only after that update completed, i.e. after this wait returned
+  pdl_wait();
+  pdl_trigger();
   if (tid == 0) s_skip = __ldcg(&ds->err) | __ldcg(&ds->finished);
   __syncthreads();
   if (s_skip) return;
@@ -310,6 +315,7 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
     }
     atomicMax(&ds->slot[cur][0], bx);
     atomicMax(&ds->slot[cur][1], by);
+    if (L.trace) trace_cta(L, 0, t_start);
   }
 }
 
@@ -1069,7 +1075,17 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   __shared__ Ctl s_ctl;
   __shared__ R s_dtd[2];
   const int i0 = blockIdx.x * LW, j0 = blockIdx.y * LW;
+  const unsigned long long t_start = L.trace ? gtimer() : 0ull;
+  // PDL: the next step's pre-pass may launch once every CTA of this grid has
+  // started (it waits for this grid's completion before reading anything).
+  // With a pre-pass in front (!CHECKS), the tile staging below reads only the
+  // state of the PREVIOUS update, which had completed before the pre-pass
+  // triggered this launch, so only the thread reading the pre-pass's maxima
+  // waits; without one (CHECKS: static speeds) everyone waits first.
+  pdl_trigger();
+  if (CHECKS) pdl_wait();
   if (tid == 0) {
+    if (!CHECKS) pdl_wait();
     const Ctl c0 = step_control<R>(A, ds, !CHECKS);
     s_ctl = c0;
     s_dtd[0] = (R)(c0.dt / A.dx);
@@ -1084,12 +1100,17 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       if (!inner) { gi = map_i(gi, L); gj = map_j(gj, L); }
       R qc[NEQ], ac[NA1], pc[NP1];
       const R* src = q + row_off(gj, L) + gi;
+      // L2 loads (ld.global.cg): this grid may have launched before the
+      // pre-pass finished, so nothing is taken from a possibly stale L1 line
 #pragma unroll
-      for (int c = 0; c < NEQ; ++c) { qc[c] = src[c * L.pitch]; sQ[c * HC + idx] = qc[c]; }
+      for (int c = 0; c < NEQ; ++c) {
+        qc[c] = __ldcg(src + c * L.pitch);
+        sQ[c * HC + idx] = qc[c];
+      }
       if (NAUX > 0) {
         const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
 #pragma unroll
-        for (int c = 0; c < NAUX; ++c) { ac[c] = asrc[c * L.pitch]; sA[c * HC + idx] = ac[c]; }
+        for (int c = 0; c < NAUX; ++c) { ac[c] = __ldcg(asrc + c * L.pitch); sA[c * HC + idx] = ac[c]; }
       }
       if (NPR > 0) {
         prims_fast<S>(qc, ac, P, pc);
@@ -1263,6 +1284,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       __threadfence();
       commit_step<R>(ds, A, ctl, L);
     }
+    if (L.trace) trace_cta(L, 1, t_start);
   }
 }
 
