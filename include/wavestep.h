@@ -134,6 +134,12 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* stream);
  * slot (MAX) between the two phases and exchanges halo rows before phase 1.
  * ws_step == ws_phase_speeds + ws_phase_update on one shard. */
 int ws_phase_speeds(ws_handle* h, void* stream);
+/* ws_phase_speeds in two parts, so a shard overlaps the pre-pass with its
+ * halo exchange: part 1 = every edge except the y-edges that read received
+ * ghost rows (local row 0, and row ny of a top shard whose high ghost rows
+ * come from a periodic neighbour), enqueued while the halo rows are in
+ * flight; part 2 = those y-edges, after they arrived.  part 0 = both. */
+int ws_phase_speeds_part(ws_handle* h, int32_t part, void* stream);
 int ws_phase_update(ws_handle* h, const ws_ctl* c, void* stream);
 /* device pointer of the current step's 3 x uint64 reduction slot */
 void* ws_slot_ptr(ws_handle* h);

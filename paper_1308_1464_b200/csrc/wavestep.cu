@@ -216,7 +216,7 @@ void enqueue_step(ws_handle* h, const ws_ctl* c, int cur, cudaStream_t st) {
   StepArgs a = make_args(h, c, cur);
   if (!a.static_speeds) {
     // fused mode: the pre-pass only for a state the epilogue has not probed
-    if (!h->fused || h->need_prepass) h->ops.speeds(h, h->q[cur], cur, st);
+    if (!h->fused || h->need_prepass) h->ops.speeds(h, h->q[cur], cur, 0, st);
     h->need_prepass = false;
   }
   h->ops.update(h, h->q[cur], h->q[cur ^ 1], a, st);
@@ -288,7 +288,6 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   h->line_kernel = h->neq <= 3;   // 4-component systems exceed 1 CTA/SM of line smem
   if (const char* v = std::getenv("WS_KERNEL")) h->line_kernel = std::strcmp(v, "tile") != 0;
   if (const char* v = std::getenv("WS_SPEEDS")) h->speeds_smem = std::strcmp(v, "smem") == 0;
-  if (const char* v = std::getenv("WS_SPW")) h->spw = std::atoi(v);
   if (const char* v = std::getenv("WS_PDL")) h->pdl = std::atoi(v) != 0;
   {
     const char* v = std::getenv("WS_FUSE");
@@ -464,12 +463,20 @@ int ws_step(ws_handle* h, const ws_ctl* c, void* s) {
   return WS_OK;
 }
 
-int ws_phase_speeds(ws_handle* h, void* s) {
+int ws_phase_speeds(ws_handle* h, void* s) { return ws_phase_speeds_part(h, 0, s); }
+
+int ws_phase_speeds_part(ws_handle* h, int32_t part, void* s) {
   if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (part < 0 || part > 2) return fail(h, WS_ERR_CONFIG, "part must be 0, 1 or 2");
   cudaStream_t st = pick(h, s);
+  if (part != 0 && (h->fused || (h->ops.static_speeds && !h->multi))) {
+    // split pre-pass only exists for the dynamic-speed, unfused path (shards)
+    return fail(h, WS_ERR_CONFIG, "split CFL pre-pass needs a dynamic-speed, unfused handle");
+  }
   // single-shard dynamic solvers probe the next state in the update epilogue
-  if (!h->fused || h->need_prepass) h->ops.speeds(h, h->q[h->enq & 1], (int)(h->enq & 1), st);
-  h->need_prepass = false;
+  if (!h->fused || h->need_prepass)
+    h->ops.speeds(h, h->q[h->enq & 1], (int)(h->enq & 1), part, st);
+  if (part != 1) h->need_prepass = false;
   WS_CUDA(h, cudaGetLastError());
   return WS_OK;
 }

@@ -34,7 +34,7 @@ template <class S, class R> constexpr int spd_ty() {
 }
 
 struct Ops {
-  void (*speeds)(ws_handle*, const void* q, int cur, cudaStream_t);
+  void (*speeds)(ws_handle*, const void* q, int cur, int part, cudaStream_t);
   void (*update)(ws_handle*, const void* q, void* qn, const StepArgs&, cudaStream_t);
   void (*to_soa)(ws_handle*, const void* stage, void* dst, int ncomp, cudaStream_t);
   void (*to_aos)(ws_handle*, const void* cur, const void* gsrc, void* stage, cudaStream_t);
@@ -81,7 +81,6 @@ struct ws_handle {
   int exp = 0;                  // WS_EXP timing-study switches
   bool line_kernel = true;      // warp-per-line k_update_w (else the smem-tile k_update)
   bool speeds_smem = false;     // shared-memory tile pre-pass (else the register k_speeds_w)
-  int spw = 0;                  // register pre-pass geometry variant (experiments)
   bool pdl = true;              // programmatic dependent launch of the step kernels
   size_t border_bytes = 0;
   std::string err;
@@ -199,31 +198,21 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
 
   static const P& prm(ws_handle* h) { return *reinterpret_cast<const P*>(h->params.data()); }
 
-  // edge rows [0, ny+1) in warp strips of KC rows, 31 edge columns per warp
-  template <int KC, int NW, int UNR, int MINB>
-  static void speeds_w(ws_handle* h, const void* q, int cur, cudaStream_t st) {
-    dim3 grid((h->L.nx + 1 + 30) / 31, (h->L.ny + 1 + KC * NW - 1) / (KC * NW));
-    launch(h, k_speeds_w<S, R, KC, NW, UNR, MINB>, grid, dim3(NW * 32), 0, st,
-           static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
-  }
-
-  static void speeds(ws_handle* h, const void* q, int cur, cudaStream_t st) {
-    if (h->speeds_smem) {
+  static void speeds(ws_handle* h, const void* q, int cur, int part, cudaStream_t st) {
+    if (h->speeds_smem && part == 0) {
       constexpr int TY = spd_ty<S, R>();
       dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + TY - 1) / TY);
       k_speeds<S, R, SPD_TX, TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(
           static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
     } else {
-      constexpr int MB = S::NEQ <= 3 ? 8 : 4;   // CTAs/SM the register budget targets
-      switch (h->spw) {
-        case 1: speeds_w<16, 4, 1, MB>(h, q, cur, st); break;
-        case 2: speeds_w<8, 8, 1, MB / 2>(h, q, cur, st); break;
-        case 3: speeds_w<8, 4, 2, MB>(h, q, cur, st); break;
-        case 4: speeds_w<8, 4, 1, MB * 3 / 4>(h, q, cur, st); break;
-        case 5: speeds_w<8, 1, 1, MB * 4>(h, q, cur, st); break;
-        case 6: speeds_w<16, 1, 1, MB * 4>(h, q, cur, st); break;
-        default: speeds_w<8, 4, 1, MB>(h, q, cur, st); break;
-      }
+      // register pre-pass: 8 edge rows per warp, 4 warps per CTA (the best of
+      // the geometries measured in round 1, DESIGN.md perf log)
+      constexpr int KC = 8, NW = 4, MB = S::NEQ <= 3 ? 8 : 4;
+      dim3 grid((h->L.nx + 1 + 30) / 31,
+                part == 2 ? 2 : (h->L.ny + 1 + KC * NW - 1) / (KC * NW));
+      launch(h, k_speeds_w<S, R, KC, NW, 1, MB>, grid, dim3(NW * 32), 0, st,
+             static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, part,
+             h->ds);
     }
     h->launches++;
   }

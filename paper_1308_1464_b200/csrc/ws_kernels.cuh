@@ -195,7 +195,8 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
 template <class S, class R, int KC, int NWS, int UNR, int MINB>
 __global__ void __launch_bounds__(NWS * 32, MINB)
 k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
-           const typename S::template Params<R> P, const int cur, DevState* __restrict__ ds) {
+           const typename S::template Params<R> P, const int cur, const int part,
+           DevState* __restrict__ ds) {
   constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   __shared__ unsigned long long sred[2][NWS];
@@ -212,9 +213,15 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   if (s_skip) return;
   const int ci = blockIdx.x * 31 - 1 + lane;                 // this lane's cell column
   const int gi = map_i(ci < L.nx ? ci : L.nx, L);
-  const int jb = (blockIdx.y * NWS + wid) * KC;              // first edge row of the warp
-  const bool xcol = lane >= 1 && ci <= L.nx;                  // owns x-edge ci
+  // part 2 runs two CTA rows: the first, and the one holding edge row ny
+  const int brow = (part == 2 && blockIdx.y == 1) ? (L.ny_edges_y - 1) / (KC * NWS) : blockIdx.y;
+  const int jb = (brow * NWS + wid) * KC;                      // first edge row of the warp
+  // part (see Impl::speeds): the y-edges that read received ghost rows are
+  // those of row 0 and, on a top shard whose high ghost rows come from a
+  // (periodic) neighbour, of row ny; part 1 skips them, part 2 keeps only them
+  const bool xcol = lane >= 1 && ci <= L.nx && part != 2;     // owns x-edge ci
   const bool ycol = lane >= 1 && ci < L.nx;                   // owns y-edge column ci
+  const int ytop = (L.hi == ROWS_MEMORY && L.ny_edges_y > L.ny) ? L.ny : -1;
 
   auto load = [&](int r, R (&qc)[NEQ], R (&ac)[NA1]) {
     const int gj = map_j(r < L.ny ? r : L.ny, L);
@@ -285,7 +292,8 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
       const bool okl = __shfl_up_sync(0xffffffffu, okc, 1);
       if (xcol && r < L.ny)
         mx = nmax(mx, probe(NX{}, ql, qc, pl, pc, al, ac, okl && okc, 0, ci, r));
-      if (ycol && r < L.ny_edges_y)
+      const bool ghost_edge = r == 0 || r == ytop;
+      if (ycol && r < L.ny_edges_y && (part == 0 || (part == 2) == ghost_edge))
         my = nmax(my, probe(NY{}, qp, qc, pp, pc, ap, ac, okp && okc, 1, ci, r));
 #pragma unroll
       for (int c = 0; c < NEQ; ++c) qp[c] = qc[c];

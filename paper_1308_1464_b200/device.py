@@ -147,8 +147,10 @@ class DeviceGrid:
     def run(self, nsteps: int, ctl: _abi.WsCtl, stream=None):
         self._check(self.lib.ws_run(self.h, int(nsteps), ctypes.byref(ctl), stream))
 
-    def phase_speeds(self, stream=None):
-        self._check(self.lib.ws_phase_speeds(self.h, stream))
+    def phase_speeds(self, stream=None, part: int = 0):
+        """CFL pre-pass; part 1/2 = before/after the low halo rows arrive
+        (ws_phase_speeds_part), 0 = whole."""
+        self._check(self.lib.ws_phase_speeds_part(self.h, int(part), stream))
 
     def phase_update(self, ctl: _abi.WsCtl, stream=None):
         self._check(self.lib.ws_phase_update(self.h, ctypes.byref(ctl), stream))

@@ -9,7 +9,8 @@ one C-ABI handle on its GPU.  Per time step:
      to the neighbours' ghost rows (one contiguous block each way, the SoA
      row layout makes 2 rows x all components contiguous); with periodic y
      and P > 1 ranks 0 and P-1 are neighbours;
-  2. ws_phase_speeds — local CFL max + admissibility key into a 3 x u64 slot;
+  2. ws_phase_speeds — local CFL max + admissibility key into a 3 x u64 slot
+     (split around the exchange, below);
   3. all_reduce(slot, MAX) — speeds are non-negative IEEE bit patterns and
      the slot stores NKEY_MAX - key, so int64 MAX gives the global max speed
      and the globally first inadmissible interface (reference order);
@@ -19,9 +20,13 @@ Because the max is order independent and the update is local, an N-rank run
 is bitwise identical to the 1-GPU run (the reference's serial-twin guard,
 bench.py:181-185, becomes the 1-vs-N test).
 
+The pre-pass is split so the halo transfer overlaps it: every edge that
+does not read the incoming ghost rows is probed while they are in flight
+(ws_phase_speeds_part 1), the y-edges of local row 0 after they land (part 2).
+
 The orchestration is generic over a *shard executor*: ``CudaShard`` (the
 product: device buffers borrowed from torch, NCCL collectives) or any test
-double with the same five methods (tests use a numpy one over gloo).
+double with the same methods (tests use a numpy one over gloo).
 """
 
 from __future__ import annotations
@@ -76,6 +81,17 @@ def shard_block(global_field: np.ndarray, j0: int, j1: int) -> np.ndarray:
 
 def exchange_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=None):
     """Send the 2 boundary rows to each neighbour, receive its rows into ghosts."""
+    finish_halos(shard, post_halos(dist, shard, strips, rank, periodic, group))
+
+
+def finish_halos(shard, reqs):
+    for req in reqs:
+        req.wait()
+    shard.halo_received()
+
+
+def post_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=None):
+    """Issue the halo sends/receives; returns the requests (finish_halos waits)."""
     lo, hi = strips.neighbours(rank, periodic)
     send_lo, send_hi, recv_lo, recv_hi = shard.halo_views()
     # Fixed per-peer order (NCCL matches point-to-point ops to one peer in
@@ -91,16 +107,21 @@ def exchange_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, gr
         ops.append(dist.P2POp(dist.irecv, recv_lo, lo, group=group, tag=1))
     if hi is not None:
         ops.append(dist.P2POp(dist.irecv, recv_hi, hi, group=group, tag=2))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-    shard.halo_received()
+    return dist.batch_isend_irecv(ops) if ops else []
 
 
 def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl, group=None):
-    """One globally consistent time step (halo, speeds, MAX all-reduce, update)."""
-    exchange_halos(dist, shard, strips, rank, periodic, group)
-    shard.phase_speeds()
+    """One globally consistent time step.
+
+    The halo rows travel while the pre-pass runs on everything that does not
+    read them (all x-edges, y-edges of rows >= 1: part 1); the y-edges of row
+    0 follow once the low ghost rows are in (part 2), then the MAX all-reduce
+    of the slot and the update (which reads both ghost-row pairs).
+    """
+    reqs = post_halos(dist, shard, strips, rank, periodic, group)
+    shard.phase_speeds_interior()
+    finish_halos(shard, reqs)
+    shard.phase_speeds_boundary()
     slot = shard.slot_view()
     dist.all_reduce(slot, op=dist.ReduceOp.MAX, group=group)
     shard.slot_reduced()
@@ -179,6 +200,14 @@ class CudaShard:
 
     def phase_speeds(self):
         self.grid.phase_speeds(stream=self.stream)
+
+    def phase_speeds_interior(self):
+        """Pre-pass edges that do not read the ghost rows being received."""
+        self.grid.phase_speeds(stream=self.stream, part=1)
+
+    def phase_speeds_boundary(self):
+        """The y-edges that read the received ghost rows (row 0, periodic row ny)."""
+        self.grid.phase_speeds(stream=self.stream, part=2)
 
     def slot_view(self):
         off = self.grid.slot_ptr() - self.slots.data_ptr()

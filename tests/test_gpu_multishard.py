@@ -34,6 +34,10 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc):
                        stream=sh.stream)
     ctl = _abi.make_ctl(0.9)
     for _ in range(steps):
+        # part 1 of the pre-pass runs BEFORE the halo rows are refreshed (the
+        # ghost rows still hold the previous step's values): it must not read them
+        for sh in shards:
+            sh.phase_speeds_interior()
         views = [sh.halo_views() for sh in shards]
         for r in range(P):
             lo, hi = strips.neighbours(r, periodic)
@@ -42,7 +46,7 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc):
             if lo is not None:
                 views[lo][3].copy_(views[r][0])     # my bottom rows -> lower neighbour's high ghosts
         for sh in shards:
-            sh.phase_speeds()
+            sh.phase_speeds_boundary()
         slot = shards[0].slot_view().clone()
         for sh in shards[1:]:
             slot = torch.maximum(slot, sh.slot_view())
@@ -95,3 +99,17 @@ def test_fake_shards_report_the_global_first_error():
     for e in errs:
         assert e.code == _abi.WS_ERR_KERNEL
         assert f"{'xy'[e.direction]}-interface (i={e.i}, j={e.j})" == str(oe.value).split(":")[0]
+
+
+def test_split_prepass_needs_a_prepass():
+    # single-domain constant-coefficient acoustics has static speeds (no
+    # pre-pass at all): asking for half of one is a configuration error
+    from helpers import device_grid
+    g = device_grid("acoustics-const", 16, 16, 1 / 16, 1 / 16)
+    try:
+        with pytest.raises(ValueError, match="split CFL pre-pass"):
+            g.phase_speeds(part=1)
+        with pytest.raises(ValueError, match="part must be"):
+            g.phase_speeds(part=3)
+    finally:
+        g.close()
