@@ -307,7 +307,7 @@ def gpu_arm(args):
                 "peak_kind": peak_kind, "kernel_ms": upd_ms,
                 "speeds_kernel_ms": statistics.mean(t_spd) if dyn else 0.0,
                 "algorithmic_bytes_per_cell": bpc}
-    roofline["kernel"] = "k_update_w" if case.kernel not in ("euler", "euler-hlle") else "k_update"
+    roofline["kernel"] = "k_update_w"
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:

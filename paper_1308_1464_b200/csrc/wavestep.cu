@@ -285,7 +285,7 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   // faster than the k_speeds pre-pass on B200 (profiles/r1_exp_fused.md):
   // opt-in with WS_FUSE=1
   if (const char* v = std::getenv("WS_EXP")) h->exp = std::atoi(v);
-  h->line_kernel = h->neq <= 3;   // 4-component systems exceed 1 CTA/SM of line smem
+  h->line_kernel = true;          // warp-line kernel for every solver (WS_KERNEL=tile: tile kernel)
   if (const char* v = std::getenv("WS_KERNEL")) h->line_kernel = std::strcmp(v, "tile") != 0;
   if (const char* v = std::getenv("WS_SPEEDS")) h->speeds_smem = std::strcmp(v, "smem") == 0;
   if (const char* v = std::getenv("WS_PDL")) h->pdl = std::atoi(v) != 0;

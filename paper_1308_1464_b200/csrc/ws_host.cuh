@@ -243,7 +243,9 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     h->launches++;
   }
 
-  static constexpr int LNW = 10;  // warps per CTA of the warp-line kernel (29 lines / 10 ~ 97%)
+  // warps per CTA of the warp-line kernel: 29 lines / 10 ~ 97 % at 2 CTAs/SM;
+  // 4-component systems stage 141 KB (fp64) -> 1 CTA/SM of 15 warps (97 %)
+  static constexpr int LNW = (S::NEQ >= 4 && sizeof(R) == 8) ? 15 : 10;
   static constexpr bool CAN_FUSE = !S::STATIC_SPEEDS && S::NAUX == 0 && S::NPR <= S::NEQ;
   template <bool CHECKS, bool FUSED> static auto kern_w() {
     return k_update_w<S, R, ORDER, LIM, LNW, CHECKS, FUSED>;
