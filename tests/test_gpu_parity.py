@@ -262,3 +262,12 @@ def test_device_error_text_matches_reference(key):
     with pytest.raises(SweepError) as e:
         step(st, ax, cfg, TimestepController(0.9))
     assert str(e.value) == c["message"]
+
+
+@pytest.mark.parametrize("name", ["euler-hlle", "shallow-water-roe", "acoustics-var"])
+def test_tile_kernel_alternative_bitwise(monkeypatch, name):
+    # the shared-memory tile kernel (WS_KERNEL=tile; the default is the
+    # warp-line kernel for every solver) stays bitwise equal to the oracle
+    monkeypatch.setenv("WS_KERNEL", "tile")
+    _compare(name, 67, 53, 4, 2, "mc", ("periodic", "extrapolate"), seed=14)
+    _compare(name, 67, 53, 3, 2, "minmod", ("extrapolate", "periodic"), seed=15, use_run=True)
