@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the row-strip (NCCL) path even with one rank (tests it on 1 GPU)")
     ap.add_argument("--size", type=int, default=None,
                     help="override the grid edge (c2/c5 only; size sweeps, not a bench line)")
     return ap.parse_args()
@@ -223,7 +225,7 @@ def gpu_arm(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.force_sharded:
         return gpu_arm_sharded(args, rank, world, local)
 
     from paper_1308_1464_b200 import DeviceGrid, _abi, make_kernel, configs

@@ -228,6 +228,11 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     import torch.distributed as dist
 
     from . import configs
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
+    torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     base = build_case(args.config, precision=args.precision)
@@ -236,15 +241,24 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     ny_g = base.ny * world
     strips = RowStrips(ny_g, world)
     j0, j1 = strips.bounds(rank)
-    glob = np.zeros((base.q.shape[0], base.nx + 4, ny_g + 4), order="F")
-    for k in range(world):
-        glob[:, :, 2 + k * base.ny:2 + (k + 1) * base.ny] = base.q[:, :, 2:-2]
+
+    def stack(f):
+        if f is None:
+            return None
+        g = np.zeros((f.shape[0], base.nx + 4, ny_g + 4), order="F")
+        for r in range(world):
+            g[:, :, 2 + r * base.ny:2 + (r + 1) * base.ny] = f[:, :, 2:-2]
+        return g
+
+    glob, gaux = stack(base.q), stack(base.aux)
     case = base
     periodic = base.bc == "periodic"
     shard = CudaShard(case, strips, rank, dev, periodic, prec)
     npdt = np.float64 if prec == "f64" else np.float32
-    shard.grid.upload(np.asfortranarray(shard_block(glob, j0, j1), dtype=npdt),
-                      stream=shard.stream)
+    host_q = np.asfortranarray(shard_block(glob, j0, j1), dtype=npdt)
+    host_aux = (np.asfortranarray(shard_block(gaux, j0, j1), dtype=npdt)
+                if gaux is not None else None)
+    shard.grid.upload(host_q, host_aux, stream=shard.stream)
     ctl = _abi.make_ctl(case.cfl)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
@@ -259,6 +273,9 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
+        # queued GPU sleep: the host enqueues the whole loop (every op is
+        # asynchronous, NCCL included) so event gaps are device time
+        torch.cuda._sleep(int(2e6 + 6e5 * k))
         for i in range(k):
             flush.zero_()
             evs[i][0].record()
@@ -275,6 +292,10 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     launches = shard.grid.launches() - l0
     cells = case.nx * ny_g
     value = cells * k / (ms_max / 1e3)
+    e2e = None
+    if not getattr(args, "no_e2e", False):
+        e2e = sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, cells,
+                          UNIT, dev)
     if rank == 0:
         peak, kind = peak_fn()
         bpc = configs.bytes_per_cell(case.kernel, prec)
@@ -292,7 +313,7 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
                          "frac": achieved / peak, "traffic": None, "kernel": "whole step",
                          "peak_kind": kind},
             "cpu_baseline": None,
-            "e2e": None,
+            "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
@@ -300,3 +321,37 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     shard.grid.close()
     dist.destroy_process_group()
     return 0
+
+
+def sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, cells, unit, dev):
+    """Whole-job e2e at N ranks through the public API: per step every rank
+    uploads its strip from pinned host memory, the sharded step runs, every
+    rank downloads its strip; wall time max over ranks."""
+    import torch
+    pin = lambda a: (None if a is None else  # noqa: E731
+                     torch.from_numpy(np.ascontiguousarray(a.ravel(order="F")))
+                     .pin_memory().numpy().reshape(a.shape, order="F"))
+    pq, pa = pin(host_q), pin(host_aux)
+    out = pin(np.zeros_like(host_q))
+    n = max(3, min(k, 10))
+    for _ in range(2):
+        shard.grid.upload(pq, pa, stream=shard.stream)
+        sharded_step(dist, shard, strips, rank, periodic, ctl)
+        shard.grid.download(out, stream=shard.stream)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        shard.grid.upload(pq, pa, stream=shard.stream)
+        sharded_step(dist, shard, strips, rank, periodic, ctl)
+        shard.grid.download(out, stream=shard.stream)
+    el = time.perf_counter() - t0
+    t = torch.tensor([el], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    res = shard.grid.poll()
+    shard.grid.raise_for(res.error)
+    hb = pq.nbytes + (pa.nbytes if pa is not None else 0)
+    return {"value": cells * n / float(t.item()), "unit": unit,
+            "h2d_bytes_per_step": hb * dist.get_world_size(),
+            "d2h_bytes_per_step": out.nbytes * dist.get_world_size(),
+            "api": "per rank: DeviceGrid.upload(strip) / sharded_step / DeviceGrid.download "
+                   "(pinned host), wall time max over ranks"}

@@ -1,0 +1,77 @@
+"""The NCCL row-strip path on the one GPU this pool has: world_size 1 (no
+halo peers, the slot all-reduce goes through NCCL), via the production
+orchestration and via `bench.py --force-sharded`.  Bitwise equal to the
+single-domain oracle, like every other path."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from helpers import PARAMS, oracle_run, random_state
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("name,bc", [("shallow-water-roe", "extrapolate"),
+                                     ("euler-hlle", "periodic")])
+def test_nccl_world1_sharded_step_bitwise(name, bc):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1308_1464_b200 import _abi
+    from paper_1308_1464_b200 import parallel as PL
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+                      WORLD_SIZE="1")
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", device_id=dev)
+    try:
+        nx, ny, steps = 53, 47, 4
+        gq, gaux = random_state(name, nx, ny, 31)
+        ref, oreps = oracle_run(name, gq, gaux, nx, ny, 1 / nx, 1 / ny, steps=steps, order=2,
+                                limiter="mc", bc_x=bc, bc_y=bc)
+        case = SimpleNamespace(kernel=name, kernel_params=PARAMS[name], nx=nx, dx=1 / nx,
+                               dy=1 / ny, order=2, limiter="mc", bc=bc)
+        strips = PL.RowStrips(ny, 1)
+        sh = PL.CudaShard(case, strips, 0, dev, bc == "periodic")
+        sh.grid.upload(PL.shard_block(gq, 0, ny), None, stream=sh.stream)
+        ctl = _abi.make_ctl(0.9)
+        for _ in range(steps):
+            PL.sharded_step(dist, sh, strips, 0, bc == "periodic", ctl)
+        torch.cuda.synchronize()
+        res = sh.grid.poll()
+        assert res.error.code == 0
+        assert [r[0] for r in res.reports] == [o.dt for o in oreps]
+        out = sh.grid.download()
+        assert np.array_equal(out[:, 2:-2, 2:-2], ref[:, 2:-2, 2:-2])
+        sh.grid.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_force_sharded_line():
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+               WORLD_SIZE="1", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-sharded",
+                        "--steps", "4", "--warmup", "3"], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0
+    assert line["config"]["parallelism"] == "row-strips1"
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+    assert line["gpu_launches"] > 0
