@@ -31,6 +31,7 @@ double with the same methods (tests use a numpy one over gloo).
 
 from __future__ import annotations
 
+import contextlib
 import json
 import os
 import statistics
@@ -118,14 +119,16 @@ def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl,
     0 follow once the low ghost rows are in (part 2), then the MAX all-reduce
     of the slot and the update (which reads both ghost-row pairs).
     """
-    reqs = post_halos(dist, shard, strips, rank, periodic, group)
-    shard.phase_speeds_interior()
-    finish_halos(shard, reqs)
-    shard.phase_speeds_boundary()
-    slot = shard.slot_view()
-    dist.all_reduce(slot, op=dist.ReduceOp.MAX, group=group)
-    shard.slot_reduced()
-    shard.phase_update(ctl)
+    ctx = getattr(shard, "stream_context", None)
+    with ctx() if ctx is not None else contextlib.nullcontext():
+        reqs = post_halos(dist, shard, strips, rank, periodic, group)
+        shard.phase_speeds_interior()
+        finish_halos(shard, reqs)
+        shard.phase_speeds_boundary()
+        slot = shard.slot_view()
+        dist.all_reduce(slot, op=dist.ReduceOp.MAX, group=group)
+        shard.slot_reduced()
+        shard.phase_update(ctl)
 
 
 def decode_slot(slot_words) -> tuple[float, float, int | None]:
@@ -145,7 +148,7 @@ class CudaShard:
     (NCCL) without copies."""
 
     def __init__(self, case, strips: RowStrips, rank: int, device, periodic_y: bool,
-                 precision: str = "f64"):
+                 precision: str = "f64", stream=None):
         import torch
 
         from .device import DeviceGrid
@@ -182,7 +185,17 @@ class CudaShard:
                                         "q1": self.bufs[1].data_ptr(),
                                         "aux": self.aux_buf.data_ptr() if ab.value else None,
                                         "slots": self.slots.data_ptr()})
-        self.stream = torch.cuda.current_stream(device).cuda_stream
+        # one torch stream carries the shard's kernels AND its collectives:
+        # sharded_step makes it current, so NCCL (which orders itself after
+        # the current stream) and the C ABI calls (given its handle) are in
+        # one stream order.  A null handle would select the library's own
+        # non-blocking stream, which nothing on the torch side waits for.
+        self.torch_stream = stream if stream is not None else torch.cuda.Stream(device)
+        self.stream = self.torch_stream.cuda_stream
+        assert self.stream, "CudaShard needs a non-default torch stream"
+
+    def stream_context(self):
+        return self.torch.cuda.stream(self.torch_stream)
 
     def _current(self):
         ptr, pitch, row = self.grid.state_ptr()
@@ -272,9 +285,10 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     l0 = shard.grid.launches()
     dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    with Clocks(local) as clk, shard.stream_context():
         # queued GPU sleep: the host enqueues the whole loop (every op is
-        # asynchronous, NCCL included) so event gaps are device time
+        # asynchronous, NCCL included) so event gaps are device time; flush,
+        # events, kernels and collectives all on the shard's stream
         torch.cuda._sleep(int(2e6 + 6e5 * k))
         for i in range(k):
             flush.zero_()

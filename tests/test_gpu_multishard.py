@@ -26,13 +26,17 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc):
                            order=order, limiter=limiter, bc=bc)
     periodic = bc == "periodic"
     strips = PL.RowStrips(ny, P)
-    shards = [PL.CudaShard(case, strips, r, dev, periodic) for r in range(P)]
+    # one shared stream: the torch copies standing in for NCCL are ordered
+    # with every shard's kernels
+    stream = torch.cuda.Stream(dev)
+    shards = [PL.CudaShard(case, strips, r, dev, periodic, stream=stream) for r in range(P)]
     for r, sh in enumerate(shards):
         j0, j1 = strips.bounds(r)
         sh.grid.upload(PL.shard_block(gq, j0, j1),
                        PL.shard_block(gaux, j0, j1) if gaux is not None else None,
                        stream=sh.stream)
     ctl = _abi.make_ctl(0.9)
+    torch.cuda.set_stream(stream)
     for _ in range(steps):
         # part 1 of the pre-pass runs BEFORE the halo rows are refreshed (the
         # ghost rows still hold the previous step's values): it must not read them
@@ -54,6 +58,7 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc):
             sh.slot_view().copy_(slot)
             sh.phase_update(ctl)
     torch.cuda.synchronize()
+    torch.cuda.set_stream(torch.cuda.default_stream(dev))
     out, reps, errs = [], [], []
     for sh in shards:
         res = sh.grid.poll()
