@@ -121,6 +121,20 @@ int ws_download(ws_handle* h, double* q_host, void* stream);
 /* fp32 handles: same calls with float arrays */
 int ws_upload_f32(ws_handle* h, const float* q_host, const float* aux_host, void* stream);
 int ws_download_f32(ws_handle* h, float* q_host, void* stream);
+/* Enqueue-only download (array of the handle's precision): no host sync and
+ * no device error check — valid after the stream completes and ws_poll
+ * reports no error.  With a pinned destination it overlaps the next
+ * ws_upload's host-to-device copy issued on another stream.
+ *
+ * Streams: a null stream selects the handle's own stream.  Operations on one
+ * handle execute in issue order whatever streams they are issued on (a call
+ * on a different stream than the previous one waits for it), with two
+ * relaxations that let transfers overlap: ws_upload's host-to-device copy
+ * may start before earlier work finishes, and work issued after a download
+ * on another stream does not wait for that download's device-to-host copy
+ * (wait for the stream, or use the synchronous ws_download, before reading
+ * the host array). */
+int ws_download_async(ws_handle* h, void* q_host, void* stream);
 
 /* One step, enqueued only (no host sync): fill ghosts (implicit, by index
  * mapping) -> sweep -> choose_dt on device -> update.

@@ -79,6 +79,7 @@ SIGNATURES = [
     ("ws_download_f32", C.c_int, [_P, _P, _P]),
     ("ws_step", C.c_int, [_P, C.POINTER(WsCtl), _P]),
     ("ws_run", C.c_int, [_P, C.c_int32, C.POINTER(WsCtl), _P]),
+    ("ws_download_async", C.c_int, [_P, _P, _P]),
     ("ws_phase_speeds", C.c_int, [_P, _P]),
     ("ws_phase_speeds_part", C.c_int, [_P, C.c_int32, _P]),
     ("ws_phase_update", C.c_int, [_P, C.POINTER(WsCtl), _P]),

@@ -273,7 +273,10 @@ int ws_create(const ws_desc* d, ws_handle** out) {
       (e = get(d->ext_q1, qb, &h->q[1], &h->own_q[1])) != cudaSuccess ||
       (e = get(d->ext_aux, ab, &h->aux, &h->own_aux)) != cudaSuccess ||
       (e = get(d->ext_slots, sb, &dsp, &h->own_ds)) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+      (e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev_order, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming)) != cudaSuccess) {
     ws_destroy(h);
     return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
   }
@@ -336,6 +339,10 @@ void ws_destroy(ws_handle* h) {
   if (h->own_aux && h->aux) cudaFree(h->aux);
   if (h->own_ds && h->ds) cudaFree(h->ds);
   if (h->stage) cudaFree(h->stage);
+  if (h->stage_out) cudaFree(h->stage_out);
+  if (h->ev_order) cudaEventDestroy(h->ev_order);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->borders) cudaFree(h->borders);
   if (h->trace) cudaFree(h->trace);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -346,29 +353,40 @@ const char* ws_last_error(const ws_handle* h) {
   return h ? h->err.c_str() : g_create_error.c_str();
 }
 
-static int ensure_stage(ws_handle* h, size_t bytes) {
-  if (h->stage_bytes >= bytes) return WS_OK;
-  if (h->stage) { cudaStreamSynchronize(h->stream); cudaFree(h->stage); h->stage = nullptr; }
-  WS_CUDA(h, cudaMalloc(&h->stage, bytes));
-  h->stage_bytes = bytes;
+static int ensure_buf(ws_handle* h, void** buf, size_t* have, size_t bytes) {
+  if (*have >= bytes) return WS_OK;
+  if (*buf) { cudaDeviceSynchronize(); cudaFree(*buf); *buf = nullptr; }
+  WS_CUDA(h, cudaMalloc(buf, bytes));
+  *have = bytes;
   return WS_OK;
+}
+
+static int ensure_stage(ws_handle* h, size_t bytes) {
+  return ensure_buf(h, &h->stage, &h->stage_bytes, bytes);
 }
 
 static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz, void* s) {
   if (!h || !qh) return fail(h, WS_ERR_CONFIG, "null argument");
   if (hesz != h->esz) return fail(h, WS_ERR_CONFIG, "host precision does not match the handle");
   if (h->naux > 0 && !ah) return fail(h, WS_ERR_CONFIG, "this solver needs aux data");
-  cudaStream_t st = pick(h, s);
   const size_t cells = (size_t)(h->d.nx + 4) * (h->d.ny + 4);
   int ncmax = h->neq > h->naux ? h->neq : h->naux;
   int rc = ensure_stage(h, cells * ncmax * h->esz);
   if (rc) return rc;
-  WS_CUDA(h, cudaMemcpyAsync(h->stage, qh, cells * h->neq * h->esz, cudaMemcpyHostToDevice, st));
+  // The H2D copy only needs the upload staging buffer free (the previous
+  // upload's conversion done), so it is issued BEFORE the handle's
+  // issue-order wait: it overlaps a download still in flight on another
+  // stream.  The conversion into the state then waits for everything before.
+  cudaStream_t st0 = s ? reinterpret_cast<cudaStream_t>(s) : h->stream;
+  WS_CUDA(h, cudaStreamWaitEvent(st0, h->ev_in, 0));
+  WS_CUDA(h, cudaMemcpyAsync(h->stage, qh, cells * h->neq * h->esz, cudaMemcpyHostToDevice, st0));
+  cudaStream_t st = pick(h, s);
   h->ops.to_soa(h, h->stage, h->q[0], h->neq, st);
   if (h->naux > 0) {
     WS_CUDA(h, cudaMemcpyAsync(h->stage, ah, cells * h->naux * h->esz, cudaMemcpyHostToDevice, st));
     h->ops.to_soa(h, h->stage, h->aux, h->naux, st);
   }
+  WS_CUDA(h, cudaEventRecord(h->ev_in, st));
   WS_CUDA(h, cudaMemsetAsync(h->ds, 0, offsetof(DevState, rep), st));
   WS_CUDA(h, cudaMemsetAsync(h->borders, 0, h->border_bytes, st));
   h->need_prepass = true;
@@ -428,27 +446,45 @@ static int resync(ws_handle* h, const HostState& hs, cudaStream_t st) {
   return WS_OK;
 }
 
-static int download_impl(ws_handle* h, void* qh, size_t hesz, void* s) {
+static int download_impl(ws_handle* h, void* qh, size_t hesz, void* s, bool wait) {
   if (!h || !qh) return fail(h, WS_ERR_CONFIG, "null argument");
   if (hesz != h->esz) return fail(h, WS_ERR_CONFIG, "host precision does not match the handle");
   cudaStream_t st = pick(h, s);
-  HostState hs;
-  int rc = read_state(h, &hs, st);
-  if (rc) return rc;
-  if ((rc = resync(h, hs, st))) return rc;
-  const int cur = (int)(hs.steps & 1);
+  long long steps = h->enq;
+  bool err = false;
+  int rc;
+  if (wait) {
+    HostState hs;
+    if ((rc = read_state(h, &hs, st))) return rc;
+    if ((rc = resync(h, hs, st))) return rc;
+    steps = hs.steps;
+    err = hs.err != 0;
+  }
+  // (async: the host's count of enqueued steps stands in for the device's;
+  // the caller checks ws_poll before trusting the array)
+  const int cur = (int)(steps & 1);
   // ghosts hold the BC fill of the state the last (attempted) step started from
-  const void* gsrc = (hs.steps == 0 || hs.err) ? h->q[cur] : h->q[cur ^ 1];
+  const void* gsrc = (steps == 0 || err) ? h->q[cur] : h->q[cur ^ 1];
   const size_t bytes = (size_t)(h->d.nx + 4) * (h->d.ny + 4) * h->neq * h->esz;
-  if ((rc = ensure_stage(h, bytes))) return rc;
-  h->ops.to_aos(h, h->q[cur], gsrc, h->stage, st);
-  WS_CUDA(h, cudaMemcpyAsync(qh, h->stage, bytes, cudaMemcpyDeviceToHost, st));
-  WS_CUDA(h, cudaStreamSynchronize(st));
+  if ((rc = ensure_buf(h, &h->stage_out, &h->stage_out_bytes, bytes))) return rc;
+  WS_CUDA(h, cudaStreamWaitEvent(st, h->ev_out, 0));   // previous copy-out done
+  h->ops.to_aos(h, h->q[cur], gsrc, h->stage_out, st);
+  // later operations on other streams order after the conversion, not after
+  // the copy to the host (only the next download reuses stage_out, and it is
+  // stream-ordered behind this copy when issued on the same stream)
+  WS_CUDA(h, cudaEventRecord(h->ev_order, st));
+  WS_CUDA(h, cudaMemcpyAsync(qh, h->stage_out, bytes, cudaMemcpyDeviceToHost, st));
+  WS_CUDA(h, cudaEventRecord(h->ev_out, st));
+  h->order_recorded = true;
+  if (wait) WS_CUDA(h, cudaStreamSynchronize(st));
   return WS_OK;
 }
 
-int ws_download(ws_handle* h, double* q, void* s) { return download_impl(h, q, 8, s); }
-int ws_download_f32(ws_handle* h, float* q, void* s) { return download_impl(h, q, 4, s); }
+int ws_download(ws_handle* h, double* q, void* s) { return download_impl(h, q, 8, s, true); }
+int ws_download_f32(ws_handle* h, float* q, void* s) { return download_impl(h, q, 4, s, true); }
+int ws_download_async(ws_handle* h, void* q, void* s) {
+  return download_impl(h, q, h ? h->esz : 8, s, false);
+}
 
 int ws_step(ws_handle* h, const ws_ctl* c, void* s) {
   if (!h || !c) return fail(h, WS_ERR_CONFIG, "null argument");

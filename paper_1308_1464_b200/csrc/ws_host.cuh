@@ -56,10 +56,16 @@ struct ws_handle {
   void* aux = nullptr;
   DevState* ds = nullptr;
   bool own_q[2] = {false, false}, own_aux = false, own_ds = false;
-  void* stage = nullptr;
+  void* stage = nullptr;         // upload staging (host layout)
   size_t stage_bytes = 0;
+  void* stage_out = nullptr;     // download staging: a download and the next upload overlap
+  size_t stage_out_bytes = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t last_stream = nullptr;
+  cudaEvent_t ev_order = nullptr;  // issue-order hand-off between streams (pick)
+  bool order_recorded = false;     // ev_order already marks the last ordering point
+  cudaEvent_t ev_in = nullptr;     // upload staging consumed (next upload's H2D may start)
+  cudaEvent_t ev_out = nullptr;    // download staging copied out (next download may refill it)
   long long enq = 0;            // steps enqueued since upload (== committed after a poll)
   long long nrep_seen = 0;
   bool multi = false;           // row-strip shard with memory ghost rows
@@ -102,8 +108,16 @@ inline int cuda_fail(ws_handle* h, cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail((h), e_, #call); \
   } while (0)
 
+// Stream of an ABI call (null: the handle's own stream).  Operations on one
+// handle run in issue order whatever streams they are issued on: switching
+// streams makes the new stream wait for everything issued before.
 inline cudaStream_t pick(ws_handle* h, void* s) {
   cudaStream_t st = s ? reinterpret_cast<cudaStream_t>(s) : h->stream;
+  if (h->last_stream && h->last_stream != st && h->ev_order) {
+    if (!h->order_recorded) cudaEventRecord(h->ev_order, h->last_stream);
+    cudaStreamWaitEvent(st, h->ev_order, 0);
+  }
+  h->order_recorded = false;
   h->last_stream = st;
   return st;
 }

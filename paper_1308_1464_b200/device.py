@@ -129,8 +129,19 @@ class DeviceGrid:
         fn = self.lib.ws_upload if self.precision == "f64" else self.lib.ws_upload_f32
         self._check(fn(self.h, q.ctypes.data, ap, stream))
 
-    def download(self, out: np.ndarray | None = None, stream=None) -> np.ndarray:
+    def download(self, out: np.ndarray | None = None, stream=None, wait: bool = True
+                 ) -> np.ndarray:
+        """State with its ghost frame, host layout.  ``wait=False`` only
+        enqueues the copy into ``out`` (ws_download_async): read it after the
+        stream completes and ``poll`` shows no error."""
         shape = self.host_shape(self.desc.num_eqn)
+        if not wait:
+            if out is None or out.dtype != self.dtype or not out.flags.f_contiguous \
+                    or out.shape != shape:
+                raise ValueError(f"an async download needs a Fortran-ordered {shape} "
+                                 f"{np.dtype(self.dtype).name} destination")
+            self._check(self.lib.ws_download_async(self.h, out.ctypes.data, stream))
+            return out
         buf = out if (out is not None and out.dtype == self.dtype and out.flags.f_contiguous
                       and out.shape == shape) else np.zeros(shape, dtype=self.dtype, order="F")
         fn = self.lib.ws_download if self.precision == "f64" else self.lib.ws_download_f32

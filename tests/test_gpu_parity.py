@@ -271,3 +271,33 @@ def test_tile_kernel_alternative_bitwise(monkeypatch, name):
     monkeypatch.setenv("WS_KERNEL", "tile")
     _compare(name, 67, 53, 4, 2, "mc", ("periodic", "extrapolate"), seed=14)
     _compare(name, 67, 53, 3, 2, "minmod", ("extrapolate", "periodic"), seed=15, use_run=True)
+
+
+def test_async_download_and_cross_stream_order():
+    # uploads on one stream, steps + enqueue-only downloads on another: the
+    # handle keeps issue order, so every downloaded state is the oracle's
+    import torch
+    from paper_1308_1464_b200 import _abi
+    from helpers import device_grid
+    name, nx, ny = "shallow-water-roe", 61, 43
+    q, _ = random_state(name, nx, ny, 17)
+    oq, _ = oracle_run(name, q, None, nx, ny, 1 / nx, 1.3 / ny, steps=2, order=2, limiter="mc")
+    g = device_grid(name, nx, ny, 1 / nx, 1.3 / ny, order=2, limiter="mc")
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = [torch.empty(3 * (nx + 4) * (ny + 4), dtype=torch.float64).pin_memory().numpy()
+            .reshape((3, nx + 4, ny + 4), order="F") for _ in range(4)]
+    try:
+        ctl = _abi.make_ctl(0.9)
+        for k in range(4):
+            g.upload(q, None, stream=a.cuda_stream)
+            g.step(ctl, stream=b.cuda_stream)
+            g.step(ctl, stream=b.cuda_stream)
+            g.download(outs[k], stream=b.cuda_stream, wait=False)
+        torch.cuda.synchronize()
+        assert g.poll().error.code == 0
+        for o in outs:
+            assert same_bits(oq, o)
+        with pytest.raises(ValueError, match="async download needs"):
+            g.download(np.zeros((3, nx + 4, ny + 4)), wait=False)
+    finally:
+        g.close()
