@@ -404,7 +404,7 @@ static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz
       WS_CUDA(h, cudaStreamSynchronize(st));
     }
   }
-  WS_CUDA(h, cudaGetLastError());
+  WS_CUDA(h, launch_status(h));
   h->enq = 0;
   h->nrep_seen = 0;
   h->uploaded = true;
@@ -495,7 +495,7 @@ int ws_step(ws_handle* h, const ws_ctl* c, void* s) {
   if (!std::isnan(c->t_final)) WS_CUDA(h, cudaMemsetAsync(&h->ds->finished, 0, sizeof(int), st));
   enqueue_step(h, c, (int)(h->enq & 1), st);
   h->enq++;
-  WS_CUDA(h, cudaGetLastError());
+  WS_CUDA(h, launch_status(h));
   return WS_OK;
 }
 
@@ -513,7 +513,7 @@ int ws_phase_speeds_part(ws_handle* h, int32_t part, void* s) {
   if (!h->fused || h->need_prepass)
     h->ops.speeds(h, h->q[h->enq & 1], (int)(h->enq & 1), part, st);
   if (part != 1) h->need_prepass = false;
-  WS_CUDA(h, cudaGetLastError());
+  WS_CUDA(h, launch_status(h));
   return WS_OK;
 }
 
@@ -526,7 +526,7 @@ int ws_phase_update(ws_handle* h, const ws_ctl* c, void* s) {
   StepArgs a = make_args(h, c, cur);
   h->ops.update(h, h->q[cur], h->q[cur ^ 1], a, st);
   h->enq++;
-  WS_CUDA(h, cudaGetLastError());
+  WS_CUDA(h, launch_status(h));
   return WS_OK;
 }
 
@@ -592,7 +592,7 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
     }
   }
   while (left > 0) { enqueue_step(h, c, (int)(h->enq & 1), st); h->enq++; left--; }
-  WS_CUDA(h, cudaGetLastError());
+  WS_CUDA(h, launch_status(h));
   return WS_OK;
 }
 

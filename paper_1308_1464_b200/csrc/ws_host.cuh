@@ -88,6 +88,7 @@ struct ws_handle {
   bool line_kernel = true;      // warp-per-line k_update_w (else the smem-tile k_update)
   bool speeds_smem = false;     // shared-memory tile pre-pass (else the register k_speeds_w)
   bool pdl = true;              // programmatic dependent launch of the step kernels
+  cudaError_t launch_err = cudaSuccess;  // first failed cudaLaunchKernelEx (reported once)
   size_t border_bytes = 0;
   std::string err;
 };
@@ -107,6 +108,15 @@ inline int cuda_fail(ws_handle* h, cudaError_t e, const char* where) {
     cudaError_t e_ = (call);                               \
     if (e_ != cudaSuccess) return cuda_fail((h), e_, #call); \
   } while (0)
+
+// launch status of everything enqueued since the last check: a failed
+// cudaLaunchKernelEx (returned, not necessarily sticky) or the runtime's last error
+inline cudaError_t launch_status(ws_handle* h) {
+  cudaError_t e = h->launch_err;
+  h->launch_err = cudaSuccess;
+  const cudaError_t l = cudaGetLastError();
+  return e != cudaSuccess ? e : l;
+}
 
 // Stream of an ABI call (null: the handle's own stream).  Operations on one
 // handle run in issue order whatever streams they are issued on: switching
@@ -201,7 +211,8 @@ inline void launch(ws_handle* h, void (*k)(KArgs...), dim3 grid, dim3 block, siz
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = h->pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k, args...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
+  if (e != cudaSuccess && h->launch_err == cudaSuccess) h->launch_err = e;
 }
 
 // ---- typed launchers -----------------------------------------------------
