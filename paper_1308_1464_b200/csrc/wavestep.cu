@@ -195,7 +195,6 @@ StepArgs make_args(ws_handle* h, const ws_ctl* c, int cur) {
   a.cur = cur;
   a.static_speeds = (h->ops.static_speeds && !h->multi) ? 1 : 0;
   a.borders = h->borders;
-  a.exp = h->exp;
   return a;
 }
 
@@ -287,7 +286,6 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   // kernel; tile kernel: shared-border counters) are bitwise correct but not
   // faster than the k_speeds pre-pass on B200 (profiles/r1_exp_fused.md):
   // opt-in with WS_FUSE=1
-  if (const char* v = std::getenv("WS_EXP")) h->exp = std::atoi(v);
   h->line_kernel = true;          // warp-line kernel for every solver (WS_KERNEL=tile: tile kernel)
   if (const char* v = std::getenv("WS_KERNEL")) h->line_kernel = std::strcmp(v, "tile") != 0;
   if (const char* v = std::getenv("WS_SPEEDS")) h->speeds_smem = std::strcmp(v, "smem") == 0;
@@ -319,7 +317,6 @@ int ws_create(const ws_desc* d, ws_handle** out) {
       }
     }
   }
-  if (const char* v = std::getenv("WS_TILE")) h->variant = std::atoi(v);
   // zero everything once so ghost rows / padding are defined
   cudaMemsetAsync(h->q[0], 0, qb, h->stream);
   cudaMemsetAsync(h->q[1], 0, qb, h->stream);

@@ -92,7 +92,6 @@ struct StepArgs {
   int cur;              // slot parity of this step
   int static_speeds;    // 1: max speeds come from DevState::static_bits
   int* borders;         // tile-border counters of the fused CFL epilogue
-  int exp;              // experiment switches (WS_EXP, timing studies only)
 };
 
 __device__ __forceinline__ int map_i(int i, const Layout& L) {

@@ -79,12 +79,10 @@ struct ws_handle {
   cudaStream_t gstream = nullptr;
   long long launches = 0;
   long long graph_launches = 0;  // kernels per replay of the 2-step graph
-  int variant = 0;              // WS_TILE experiment selector (0 = default tiles)
   bool fused = false;           // next-step CFL maxima computed in the update epilogue
   bool need_prepass = true;     // fused mode: slot of the current state not yet filled
   int* borders = nullptr;       // tile-border counters of the fused epilogue
   unsigned long long* trace = nullptr;   // CTA timeline buffer (WS_TRACE=1)
-  int exp = 0;                  // WS_EXP timing-study switches
   bool line_kernel = true;      // warp-per-line k_update_w (else the smem-tile k_update)
   bool speeds_smem = false;     // shared-memory tile pre-pass (else the register k_speeds_w)
   bool pdl = true;              // programmatic dependent launch of the step kernels
@@ -156,44 +154,6 @@ int persistent_grid(K kernel, int nt, size_t smem, int nx, int ny, int tx, int t
   const long long tiles = (long long)((nx + tx - 1) / tx) * ((ny + ty - 1) / ty);
   const long long g = (long long)per_sm * sms;
   return (int)(tiles < g ? tiles : g);
-}
-
-// ---- tile-shape experiments (WS_TILE=k selects variant k; SW fp64 order 2 MC)
-template <class S, class R, int ORDER, int LIM, int TX, int TY, int NT>
-void launch_variant(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
-  using G = TileGeom<S, ORDER, TX, TY>;
-  const size_t smem = G::template smem_bytes<R>();
-  auto go = [&](auto k) {
-    static bool done = false;
-    if (!done) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); done = true; }
-    dim3 grid(persistent_grid(k, NT, smem, h->L.nx, h->L.ny, TX, TY));
-    k<<<grid, NT, smem, st>>>(static_cast<const R*>(q), static_cast<const R*>(h->aux),
-                              static_cast<R*>(qn), h->L,
-                              *reinterpret_cast<const typename S::template Params<R>*>(h->params.data()),
-                              a, h->ds);
-  };
-  if (h->fused) go(k_update<S, R, ORDER, LIM, TX, TY, NT, false, true>);
-  else go(k_update<S, R, ORDER, LIM, TX, TY, NT, false, false>);
-  h->launches++;
-}
-
-template <class S, class R, int ORDER, int LIM>
-bool variant_update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
-  if constexpr (std::is_same<S, ShallowRoe>::value && std::is_same<R, double>::value &&
-                ORDER == 2 && LIM == LIM_MC) {
-    switch (h->variant) {
-      case 1: launch_variant<S, R, 2, LIM_MC, 32, 8, 256>(h, q, qn, a, st); return true;
-      case 2: launch_variant<S, R, 2, LIM_MC, 32, 13, 256>(h, q, qn, a, st); return true;
-      case 3: launch_variant<S, R, 2, LIM_MC, 64, 8, 256>(h, q, qn, a, st); return true;
-      case 4: launch_variant<S, R, 2, LIM_MC, 32, 16, 128>(h, q, qn, a, st); return true;
-      case 5: launch_variant<S, R, 2, LIM_MC, 16, 16, 256>(h, q, qn, a, st); return true;
-      case 6: launch_variant<S, R, 2, LIM_MC, 32, 8, 128>(h, q, qn, a, st); return true;
-      case 7: launch_variant<S, R, 2, LIM_MC, 64, 6, 256>(h, q, qn, a, st); return true;
-      case 8: launch_variant<S, R, 2, LIM_MC, 32, 12, 192>(h, q, qn, a, st); return true;
-      default: return false;
-    }
-  }
-  return false;
 }
 
 // kernel launch, with programmatic dependent launch when enabled (the two
@@ -292,7 +252,6 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   }
 
   static void update(ws_handle* h, const void* q, void* qn, const StepArgs& a, cudaStream_t st) {
-    if (h->variant > 0 && variant_update<S, R, ORDER, LIM>(h, q, qn, a, st)) return;
     if (h->line_kernel) {
       if (S::STATIC_SPEEDS && !h->multi) update_w<true, false>(h, q, qn, a, st);
       else if constexpr (CAN_FUSE) {

@@ -466,10 +466,8 @@ __device__ __forceinline__ void next_step_speeds(
   }
 
   // shared borders: left/right = vertical border ids, bottom/top = horizontal
-  if (A.exp & 1) return;   // timing study: interior edges only (NOT a valid CFL max)
   __syncthreads();
   if (tid == 0) {
-    if (A.exp & 2) __threadfence();
     int* vb = A.borders;                 // [nty][ntx]: left border of tile column c
     int* hb = A.borders + ntx * nty;     // [nty][ntx]: bottom border of tile row r
     int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
@@ -817,7 +815,7 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
         }
       }
       if (FUSED) {
-        if (!(A.exp & 2)) __threadfence();   // q_new visible device-wide before the border counters
+        __threadfence();   // q_new visible device-wide before the border counters
         next_step_speeds<S, R, TX, TY, NT, H>(sQ, sA, sP, qn, aux, L, P, A, i0, j0, t % ntx,
                                            t / ntx, ntx, nty, s_second, nmx, nmy, nkey);
       }

@@ -1,6 +1,6 @@
-# pytest -m gpu, then C2 bench per pre-pass variant (WS_SPW / WS_SPEEDS)
+# pytest -m gpu, then the bench per environment variant (VARIANTS, CFG)
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? ; tail -2 gpurun_out/pytest_gpu.log
-for v in ${VARIANTS:-"WS_SPW=0" "WS_SPW=1" "WS_SPW=2" "WS_SPW=3" "WS_SPEEDS=smem" "WS_SPW=0"}; do
+for v in ${VARIANTS:-"WS_PDL=1" "WS_SPEEDS=smem" "WS_PDL=0"}; do
 env $v timeout 600 python bench.py --config ${CFG:-c2} --steps 30 --warmup 5 --no-e2e --no-cpu > gpurun_out/b8.log 2>&1
 python -c "
 import json

@@ -301,3 +301,18 @@ def test_async_download_and_cross_stream_order():
             g.download(np.zeros((3, nx + 4, ny + 4)), wait=False)
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("kernel_env,name", [("line", "shallow-water-roe"),
+                                             ("line", "advection"),
+                                             ("tile", "euler-hlle"),
+                                             ("tile", "shallow-water-roe")])
+def test_fused_cfl_epilogue_bitwise(monkeypatch, kernel_env, name):
+    # opt-in WS_FUSE=1: the next step's CFL maxima come from the update
+    # kernel's epilogue (+ tile-border pass) instead of the pre-pass; every dt
+    # and the state must not change
+    monkeypatch.setenv("WS_FUSE", "1")
+    monkeypatch.setenv("WS_KERNEL", kernel_env)
+    for bc in ("periodic", "extrapolate"):
+        _compare(name, 131, 75, 5, 2, "mc", (bc, bc), seed=19)
+        _compare(name, 131, 75, 5, 2, "superbee", (bc, bc), seed=20, use_run=True)
