@@ -83,6 +83,15 @@ def _desc(**kw):
     ({"num_ghost": 1}, "num_ghost=2"),
     ({"order": 3}, "order must be 1 or 2"),
     ({"bc_x": 0, "nx": 1, "ny_global": 8}, "periodic boundary needs at least num_ghost=2"),
+    ({"nx": 1 << 19}, "grid too large for the interface indices"),
+    ({"ny": 1 << 18, "ny_global": 1 << 18}, "grid too large for the interface indices"),
+    ({"ny": 8, "ny_global": 4}, "inconsistent row-strip geometry"),
+    ({"j_offset": 3}, "inconsistent row-strip geometry"),
+    ({"rows_lo": 0, "ny": 1, "ny_global": 8}, "a row-strip shard needs at least 2 rows"),
+    ({"limiter": 7}, "unknown limiter"),
+    ({"precision": 5}, "unknown precision"),
+    ({"bc_y": 4}, "unknown boundary condition"),
+    ({"solver": 42}, "unknown solver id 42"),
 ])
 def test_create_validates_before_touching_the_device(kw, msg):
     lib = _abi.lib()
@@ -90,6 +99,16 @@ def test_create_validates_before_touching_the_device(kw, msg):
     rc = lib.ws_create(ctypes.byref(_desc(**kw)), ctypes.byref(h))
     assert rc == _abi.WS_ERR_CONFIG
     assert msg in lib.ws_last_error(None).decode()
+
+
+def test_largest_accepted_grid_sizes_its_buffers():
+    # the error key holds i < 2^19, j < 2^18: the largest grid the ABI takes
+    lib = _abi.lib()
+    qb, ab, sb = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    d = _desc(nx=(1 << 19) - 1, ny=(1 << 18) - 1, ny_global=(1 << 18) - 1)
+    assert lib.ws_buffer_bytes(ctypes.byref(d), ctypes.byref(qb), ctypes.byref(ab),
+                               ctypes.byref(sb)) == 0
+    assert qb.value == ((1 << 18) - 1 + 4) * 3 * (1 << 19) * 8   # 3.3 TB: sizes in 64 bits
 
 
 def test_buffer_bytes_layout():

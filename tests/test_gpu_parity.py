@@ -316,3 +316,25 @@ def test_fused_cfl_epilogue_bitwise(monkeypatch, kernel_env, name):
     for bc in ("periodic", "extrapolate"):
         _compare(name, 131, 75, 5, 2, "mc", (bc, bc), seed=19)
         _compare(name, 131, 75, 5, 2, "superbee", (bc, bc), seed=20, use_run=True)
+
+
+def test_fp32_c5_recipe_within_stated_bound():
+    # configs[4] (C5) recipe at 256^2, 20 steps, MC: fp32 device vs the fp64
+    # device run (itself bitwise the oracle) — the stated fp32 bound
+    from paper_1308_1464_b200 import configs
+    c = configs.c5_bumps(256, steps=20)
+    q64, r64, _ = device_run(c.kernel, c.q, None, c.nx, c.ny, c.dx, c.dy, steps=20, order=2,
+                             limiter="mc")
+    q32, r32, _ = device_run(c.kernel, np.asfortranarray(c.q, dtype=np.float32), None, c.nx,
+                             c.ny, c.dx, c.dy, steps=20, order=2, limiter="mc",
+                             precision="f32")
+    assert r64.error.code == 0 and r32.error.code == 0
+    h64 = q64[0, 2:-2, 2:-2]
+    h32 = q32[0, 2:-2, 2:-2].astype(np.float64)
+    rel = np.abs(h32 - h64).max() / np.abs(h64).max()
+    dts64 = np.array([r[0] for r in r64.reports])
+    dts32 = np.array([r[0] for r in r32.reports])
+    print(f"C5 recipe 256^2 x 20: fp32 max rel err on h {rel:.3e}, "
+          f"max rel dt diff {np.abs(dts32 / dts64 - 1).max():.3e}")
+    assert rel <= 1e-5, rel
+    assert np.abs(dts32 / dts64 - 1).max() <= 1e-5
