@@ -1100,28 +1100,43 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   {
     // ---- stage tile + 2-cell halo (BC by index mapping), per-cell primitives
     const bool inner = i0 >= 2 && i0 + LW + 2 <= L.nx && j0 >= 2 && j0 + LW + 2 <= L.ny;
-    for (int idx = tid; idx < HC; idx += NT) {
-      const int lx = idx % HW, ly = idx / HW;
-      int gi = i0 - 2 + lx, gj = j0 - 2 + ly;
-      if (!inner) { gi = map_i(gi, L); gj = map_j(gj, L); }
-      R qc[NEQ], ac[NA1], pc[NP1];
-      const R* src = q + row_off(gj, L) + gi;
-      // L2 loads (ld.global.cg): this grid may have launched before the
-      // pre-pass finished, so nothing is taken from a possibly stale L1 line
+    // all of this thread's loads first (NSTG cells in flight), then the
+    // primitives: the loads' latency is paid once per tile, not per cell.
+    // L2 loads (ld.global.cg): this grid may have launched before the
+    // pre-pass finished, so nothing is taken from a possibly stale L1 line
+    constexpr int NSTG = (HC + NT - 1) / NT;
+    R qs[NSTG][NEQ], as[NSTG][NA1];
 #pragma unroll
-      for (int c = 0; c < NEQ; ++c) {
-        qc[c] = __ldcg(src + c * L.pitch);
-        sQ[c * HC + idx] = qc[c];
+    for (int k = 0; k < NSTG; ++k) {
+      const int idx = tid + k * NT;
+      if (idx < HC) {
+        const int lx = idx % HW, ly = idx / HW;
+        int gi = i0 - 2 + lx, gj = j0 - 2 + ly;
+        if (!inner) { gi = map_i(gi, L); gj = map_j(gj, L); }
+        const R* src = q + row_off(gj, L) + gi;
+#pragma unroll
+        for (int c = 0; c < NEQ; ++c) qs[k][c] = __ldcg(src + c * L.pitch);
+        if (NAUX > 0) {
+          const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+#pragma unroll
+          for (int c = 0; c < NAUX; ++c) as[k][c] = __ldcg(asrc + c * L.pitch);
+        }
       }
-      if (NAUX > 0) {
-        const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+    }
 #pragma unroll
-        for (int c = 0; c < NAUX; ++c) { ac[c] = __ldcg(asrc + c * L.pitch); sA[c * HC + idx] = ac[c]; }
-      }
-      if (NPR > 0) {
-        prims_fast<S>(qc, ac, P, pc);
+    for (int k = 0; k < NSTG; ++k) {
+      const int idx = tid + k * NT;
+      if (idx < HC) {
 #pragma unroll
-        for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
+        for (int c = 0; c < NEQ; ++c) sQ[c * HC + idx] = qs[k][c];
+#pragma unroll
+        for (int c = 0; c < NAUX; ++c) sA[c * HC + idx] = as[k][c];
+        if (NPR > 0) {
+          R pc[NP1];
+          prims_fast<S>(qs[k], as[k], P, pc);
+#pragma unroll
+          for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
+        }
       }
     }
   }
