@@ -208,9 +208,6 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   // launch only after that update completed, i.e. after this wait returned
   pdl_wait();
   pdl_trigger();
-  if (tid == 0) s_skip = __ldcg(&ds->err) | __ldcg(&ds->finished);
-  __syncthreads();
-  if (s_skip) return;
   const int ci = blockIdx.x * 31 - 1 + lane;                 // this lane's cell column
   const int gi = map_i(ci < L.nx ? ci : L.nx, L);
   // part 2 runs two CTA rows: the first, and the one holding edge row ny
@@ -234,6 +231,15 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
       for (int c = 0; c < NAUX; ++c) ac[c] = asrc[c * L.pitch];
     }
   };
+  // the first rows' loads go out before the run-flag barrier (they are
+  // in-bounds whatever the flags say; a skipped step just drops them)
+  R qp[NEQ], ap[NA1], qn[NEQ], an[NA1], qn2[NEQ], an2[NA1];
+  load(jb - 1, qp, ap);
+  load(jb, qn, an);
+  load(jb + 1, qn2, an2);                   // two rows in flight ahead of the compute
+  if (tid == 0) s_skip = __ldcg(&ds->err) | __ldcg(&ds->finished);
+  __syncthreads();
+  if (s_skip) return;
   auto cell = [&](const R (&qc)[NEQ], const R (&ac)[NA1], R (&pc)[NP1]) -> bool {
     if (NPR > 0) prims_fast<S>(qc, ac, P, pc);
     return S::cell_ok(qc, ac, pc, P);
@@ -266,9 +272,7 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   const int rows = L.ny > L.ny_edges_y ? L.ny : L.ny_edges_y;
   const int nk = rows - jb < KC ? rows - jb : KC;
   if (nk > 0) {
-    R qp[NEQ], ap[NA1], pp[NP1], qn[NEQ], an[NA1];
-    load(jb - 1, qp, ap);
-    load(jb, qn, an);                       // next row in flight while this one computes
+    R pp[NP1];
     bool okp = cell(qp, ap, pp);
 #pragma unroll UNR
     for (int k = 0; k < KC; ++k) {
@@ -276,10 +280,10 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
       const int r = jb + k;
       R qc[NEQ], ac[NA1], pc[NP1];
 #pragma unroll
-      for (int c = 0; c < NEQ; ++c) qc[c] = qn[c];
+      for (int c = 0; c < NEQ; ++c) { qc[c] = qn[c]; qn[c] = qn2[c]; }
 #pragma unroll
-      for (int c = 0; c < NAUX; ++c) ac[c] = an[c];
-      load(r + 1, qn, an);
+      for (int c = 0; c < NAUX; ++c) { ac[c] = an[c]; an[c] = an2[c]; }
+      load(r + 2, qn2, an2);
       const bool okc = cell(qc, ac, pc);
       // left neighbour (lane - 1) of the current row
       R ql[NEQ], al[NA1], pl[NP1];
