@@ -1079,9 +1079,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   // warp-uniform, so the line loops below (trip count depends on it) keep
   // their shuffles plain instead of divergent-warp collectives
   const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  // thread 0 evaluates the step control (dt from this step's maxima, 5
-  // dependent divisions) while the other threads stage the tile; the result
-  // is handed over at the post-staging barrier
+  // one thread evaluates the step control (dt from this step's maxima, 5
+  // dependent divisions) while the others stage the tile; the result is
+  // handed over at the post-staging barrier
   __shared__ Ctl s_ctl;
   __shared__ R s_dtd[2];
   const int i0 = blockIdx.x * LW, j0 = blockIdx.y * LW;
@@ -1094,13 +1094,6 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   // waits; without one (CHECKS: static speeds) everyone waits first.
   pdl_trigger();
   if (CHECKS) pdl_wait();
-  if (tid == 0) {
-    if (!CHECKS) pdl_wait();
-    const Ctl c0 = step_control<R>(A, ds, !CHECKS);
-    s_ctl = c0;
-    s_dtd[0] = (R)(c0.dt / A.dx);
-    s_dtd[1] = (R)(c0.dt / A.dy);
-  }
   {
     // ---- stage tile + 2-cell halo (BC by index mapping), per-cell primitives
     const bool inner = i0 >= 2 && i0 + LW + 2 <= L.nx && j0 >= 2 && j0 + LW + 2 <= L.ny;
@@ -1126,6 +1119,15 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
           for (int c = 0; c < NAUX; ++c) as[k][c] = __ldcg(asrc + c * L.pitch);
         }
       }
+    }
+    // step control by lane 0 of the last warp (one staged cell fewer than
+    // the first warps) while its loads are in flight
+    if (tid == NT - 32) {
+      if (!CHECKS) pdl_wait();
+      const Ctl c0 = step_control<R>(A, ds, !CHECKS);
+      s_ctl = c0;
+      s_dtd[0] = (R)(c0.dt / A.dx);
+      s_dtd[1] = (R)(c0.dt / A.dy);
     }
 #pragma unroll
     for (int k = 0; k < NSTG; ++k) {
