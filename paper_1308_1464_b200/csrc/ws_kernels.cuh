@@ -1301,10 +1301,13 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     if (CHECKS && key != ~0ull) atomicMax(&ds->slot[A.cur][2], NKEY_MAX - key);
   }
 
-  // ---- last CTA commits the step
+  // ---- last CTA commits the step.  The fence only orders this CTA's
+  // error-key atomics (CHECKS) before its count; the state stores need none
+  // (the next kernel reads them after this grid completes), and a fence per
+  // CTA holds the SM's slot for its whole latency.
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
+    if (CHECKS) __threadfence();
     const int nblk = gridDim.x * gridDim.y;
     const int prev = atomicAdd(&ds->done, 1);
     if (prev == nblk - 1) {

@@ -1,5 +1,6 @@
 // Bitwise check of ws::FastMath against the IEEE operations on a B200:
-// for random operands over wide exponent ranges plus special values, every
+// for random operands over wide exponent ranges, special values and signed
+// zero numerators, every
 // result whose range flag is set must equal `x / y`, `1.0 / y`, `sqrt(x)`
 // bit for bit.  Prints one JSON line; exit code 1 on any mismatch.
 // Built and run by tests/test_gpu_fastmath.py (same flags as the library).
@@ -42,8 +43,10 @@ __global__ void k_check(unsigned long long seed, long long n, unsigned long long
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
        t += (long long)gridDim.x * blockDim.x) {
     const unsigned long long r1 = mix(seed ^ (2 * t)), r2 = mix(seed ^ (2 * t + 1));
-    const int mode = (int)(t % 3);
-    const double x = operand(r1, mode), y = operand(r2, mode);
+    const int mode = (int)(t % 4);
+    // mode 3: a signed-zero numerator over any bit pattern (zero-jump path)
+    const double x = mode == 3 ? ((r1 & 1) ? -0.0 : 0.0) : operand(r1, mode);
+    const double y = operand(r2, mode == 3 ? (int)((r2 >> 7) % 3) : mode);
     bool ok = true;
     double q = FastMath::div(x, y, ok);
     if (ok) {
