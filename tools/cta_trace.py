@@ -1,8 +1,8 @@
-"""CTA timeline of one C2 time step (diagnostics; needs WS_TRACE=1 support in
+"""CTA timeline of one time step (C2 by default) (diagnostics; needs WS_TRACE=1 support in
 the library).  Prints, per kernel: span, CTA duration stats, and the number
 of resident CTAs over time — where the small-grid overhead goes.
 
-    WS_TRACE=1 python tools/cta_trace.py [--size 1024] [--flush]
+    python tools/cta_trace.py [--config c2|c3|c5] [--size 1024] [--flush]
 """
 import argparse
 import ctypes
@@ -17,16 +17,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--size", type=int, default=1024)
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
     ap.add_argument("--flush", action="store_true")
     a = ap.parse_args()
     os.environ["WS_TRACE"] = "1"
     import torch
 
     from paper_1308_1464_b200 import DeviceGrid, _abi, configs, make_kernel
-    c = configs.c2_shallow_water(a.size)
+    c = configs.BUILDERS[a.config](a.size)
     g = DeviceGrid(c.nx, c.ny, c.dx, c.dy, make_kernel(c.kernel, **c.kernel_params),
-                   order=2, limiter="mc", bc_x=c.bc, bc_y=c.bc)
-    g.upload(c.q)
+                   order=c.order, limiter=c.limiter, bc_x=c.bc, bc_y=c.bc)
+    g.upload(c.q, c.aux)
     ctl = _abi.make_ctl(c.cfl)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device="cuda")
     for _ in range(5):
