@@ -86,6 +86,7 @@ struct ws_handle {
   bool line_kernel = true;      // warp-per-line k_update_w (else the smem-tile k_update)
   bool speeds_smem = false;     // shared-memory tile pre-pass (else the register k_speeds_w)
   bool pdl = true;              // programmatic dependent launch of the step kernels
+  bool persist = true;          // persistent prefetching line kernel where it applies
   cudaError_t launch_err = cudaSuccess;  // first failed cudaLaunchKernelEx (reported once)
   size_t border_bytes = 0;
   std::string err;
@@ -210,6 +211,11 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     const int lsmem = (int)LineGeom<S>::template smem_bytes<R>();
     cudaFuncSetAttribute(kern_w<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
     cudaFuncSetAttribute(kern_w<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+    if constexpr (PERSIST_W) {
+      const int psmem = (int)LineGeom<S>::template smem_bytes<R>(true);
+      cudaFuncSetAttribute(kern_w<true, false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
+      cudaFuncSetAttribute(kern_w<false, false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
+    }
     if constexpr (CAN_FUSE)
       cudaFuncSetAttribute(kern_w<false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
     const int smem = (int)G::template smem_bytes<R>();
@@ -232,11 +238,24 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   // 4-component systems stage 141 KB (fp64) -> 1 CTA/SM of 15 warps (97 %)
   static constexpr int LNW = (S::NEQ >= 4 && sizeof(R) == 8) ? 15 : 10;
   static constexpr bool CAN_FUSE = !S::STATIC_SPEEDS && S::NAUX == 0 && S::NPR <= S::NEQ;
-  template <bool CHECKS, bool FUSED> static auto kern_w() {
-    return k_update_w<S, R, ORDER, LIM, LNW, CHECKS, FUSED>;
+  template <bool CHECKS, bool FUSED, bool PERSIST = false> static auto kern_w() {
+    return k_update_w<S, R, ORDER, LIM, LNW, CHECKS, FUSED, PERSIST>;
   }
+  // one CTA per SM (4-component fp64): persistent CTAs prefetch the next tile
+  static constexpr bool PERSIST_W = S::NEQ >= 4 && sizeof(R) == 8;
   template <bool CHECKS, bool FUSED> static void update_w(ws_handle* h, const void* q, void* qn,
                                                           const StepArgs& a, cudaStream_t st) {
+    if constexpr (PERSIST_W && !FUSED) {
+      if (h->persist) {
+        auto k = kern_w<CHECKS, false, true>();
+        const size_t smem = LineGeom<S>::template smem_bytes<R>(true);
+        dim3 grid(persistent_grid(k, LNW * 32, smem, h->L.nx, h->L.ny, 29, 29));
+        launch(h, k, grid, dim3(LNW * 32), smem, st, static_cast<const R*>(q),
+               static_cast<const R*>(h->aux), static_cast<R*>(qn), h->L, prm(h), a, h->ds);
+        h->launches++;
+        return;
+      }
+    }
     auto k = kern_w<CHECKS, FUSED>();
     const size_t smem = LineGeom<S>::template smem_bytes<R>();
     dim3 grid((h->L.nx + 28) / 29, (h->L.ny + 28) / 29);

@@ -1059,7 +1059,8 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
 // shared memory; the y pass adds the y term and both correction fluxes in
 // the reference order and writes q_new back to shared memory, from which
 // the tile is stored row-coalesced.
-template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUSED>
+template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUSED,
+          bool PERSIST = false>
 __global__ void __launch_bounds__(NWARP * 32, (20 / NWARP > 0 ? 20 / NWARP : 1))
 k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
            const Layout L, const typename S::template Params<R> P, const StepArgs A,
@@ -1074,6 +1075,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   R* sA = sQ + NEQ * HC;
   R* sP = sA + NAUX * HC;
   R* sX = sP + NPR * HC;          // [2*NEQ][LW*LW]: q1 and dFx, later q_new
+  R* sR = sX + 2 * NEQ * LW * LW;  // PERSIST: raw q (+aux) of the next tile, cp.async
+  static_assert(!(PERSIST && FUSED), "persistent form has no fused epilogue");
 
   // warp index through a lane-0 broadcast: the compiler then treats it as
   // warp-uniform, so the line loops below (trip count depends on it) keep
@@ -1084,7 +1087,35 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   // handed over at the post-staging barrier
   __shared__ Ctl s_ctl;
   __shared__ R s_dtd[2];
-  const int i0 = blockIdx.x * LW, j0 = blockIdx.y * LW;
+  // PERSIST (one CTA per SM, 4-component fp64): CTAs walk the tiles and
+  // prefetch the next tile's raw state with cp.async while the current tile
+  // computes; otherwise one tile per CTA (blockIdx)
+  const int ntx = (L.nx + LW - 1) / LW, ntiles = ntx * ((L.ny + LW - 1) / LW);
+  int t = PERSIST ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+  auto tile_origin = [&](int tt, int& a, int& b) { a = (tt % ntx) * LW; b = (tt / ntx) * LW; };
+  // raw tile + halo -> sR (BC by index mapping), one cp.async group
+  auto prefetch = [&](int tt) {
+    int a, b;
+    tile_origin(tt, a, b);
+    const bool in = a >= 2 && a + LW + 2 <= L.nx && b >= 2 && b + LW + 2 <= L.ny;
+    for (int idx = tid; idx < HC; idx += NT) {
+      const int lx = idx % HW, ly = idx / HW;
+      int gi = a - 2 + lx, gj = b - 2 + ly;
+      if (!in) { gi = map_i(gi, L); gj = map_j(gj, L); }
+      const R* src = q + row_off(gj, L) + gi;
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) cp_async(&sR[c * HC + idx], src + c * L.pitch);
+      if (NAUX > 0) {
+        const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+#pragma unroll
+        for (int c = 0; c < NAUX; ++c) cp_async(&sR[(NEQ + c) * HC + idx], asrc + c * L.pitch);
+      }
+    }
+    cp_commit();
+  };
+  int i0, j0;
+  tile_origin(t, i0, j0);
+  Ctl ctl;
   const unsigned long long t_start = L.trace ? gtimer() : 0ull;
   // PDL: the next step's pre-pass may launch once every CTA of this grid has
   // started (it waits for this grid's completion before reading anything).
@@ -1094,7 +1125,37 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   // waits; without one (CHECKS: static speeds) everyone waits first.
   pdl_trigger();
   if (CHECKS) pdl_wait();
-  {
+  if (PERSIST) {
+    if (t < ntiles) prefetch(t);
+    if (tid == NT - 32) {
+      if (!CHECKS) pdl_wait();
+      const Ctl c0 = step_control<R>(A, ds, !CHECKS);
+      s_ctl = c0;
+      s_dtd[0] = (R)(c0.dt / A.dx);
+      s_dtd[1] = (R)(c0.dt / A.dy);
+    }
+  }
+  for (;;) {
+  if (PERSIST) {
+    if (t >= ntiles) break;
+    cp_wait<0>();
+    __syncthreads();   // raw tile landed for every thread; previous tile fully stored
+#pragma unroll 4
+    for (int idx = tid; idx < HC; idx += NT) {
+      R qc[NEQ], ac[NA1], pc[NP1];
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) { qc[c] = sR[c * HC + idx]; sQ[c * HC + idx] = qc[c]; }
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) { ac[c] = sR[(NEQ + c) * HC + idx]; sA[c * HC + idx] = ac[c]; }
+      if (NPR > 0) {
+        prims_fast<S>(qc, ac, P, pc);
+#pragma unroll
+        for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
+      }
+    }
+    __syncthreads();   // sR consumed: the next tile's copies may land
+    if (t + (int)gridDim.x < ntiles) prefetch(t + (int)gridDim.x);
+  } else {
     // ---- stage tile + 2-cell halo (BC by index mapping), per-cell primitives
     const bool inner = i0 >= 2 && i0 + LW + 2 <= L.nx && j0 >= 2 && j0 + LW + 2 <= L.ny;
     // all of this thread's loads first (NSTG cells in flight), then the
@@ -1147,8 +1208,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
   }
   __syncthreads();
-  const Ctl ctl = s_ctl;
-  if (!ctl.skip) {
+  ctl = s_ctl;
+  if (ctl.skip) break;
+  {
     const R dtdx = s_dtd[0];
     const R dtdy = s_dtd[1];
     unsigned long long key = ~0ull;
@@ -1300,6 +1362,13 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
     if (CHECKS && key != ~0ull) atomicMax(&ds->slot[A.cur][2], NKEY_MAX - key);
   }
+  if (!PERSIST) break;
+  t += gridDim.x;
+  tile_origin(t, i0, j0);
+  }   // tile loop
+  if (PERSIST) cp_wait<0>();   // no copy outstanding at exit
+  __syncthreads();
+  ctl = s_ctl;
 
   // ---- last CTA commits the step.  The fence only orders this CTA's
   // error-key atomics (CHECKS) before its count; the state stores need none
@@ -1320,8 +1389,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 
 template <class S> struct LineGeom {
   static constexpr int LW = 29, HC = 33 * 33;
-  template <class R> static constexpr size_t smem_bytes() {
-    return sizeof(R) * (size_t)((S::NEQ + S::NAUX + S::NPR) * HC + 2 * S::NEQ * LW * LW);
+  template <class R> static constexpr size_t smem_bytes(bool persist = false) {
+    return sizeof(R) * (size_t)((S::NEQ + S::NAUX + S::NPR) * HC + 2 * S::NEQ * LW * LW +
+                                (persist ? (S::NEQ + S::NAUX) * HC : 0));
   }
 };
 

@@ -338,3 +338,10 @@ def test_fp32_c5_recipe_within_stated_bound():
           f"max rel dt diff {np.abs(dts32 / dts64 - 1).max():.3e}")
     assert rel <= 1e-5, rel
     assert np.abs(dts32 / dts64 - 1).max() <= 1e-5
+
+
+@pytest.mark.parametrize("name,bc", [("euler-hlle", "periodic"), ("euler", "extrapolate")])
+def test_persistent_line_kernel_walks_tiles_bitwise(name, bc):
+    # 4-component fp64 systems run persistent CTAs (one per SM) that prefetch
+    # the next tile with cp.async: > 148 tiles so CTAs walk several tiles
+    _compare(name, 610, 331, 3, 2, "mc", (bc, bc), seed=23)
