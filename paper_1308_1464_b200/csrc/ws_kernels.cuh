@@ -220,8 +220,10 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   const bool ycol = lane >= 1 && ci < L.nx;                   // owns y-edge column ci
   const int ytop = (L.hi == ROWS_MEMORY && L.ny_edges_y > L.ny) ? L.ny : -1;
 
+  // warps whose rows jb-1 .. jb+KC+1 are all interior skip the y mapping
+  const bool inner_rows = jb >= 1 && jb + KC + 1 < L.ny;
   auto load = [&](int r, R (&qc)[NEQ], R (&ac)[NA1]) {
-    const int gj = map_j(r < L.ny ? r : L.ny, L);
+    const int gj = inner_rows ? r : map_j(r < L.ny ? r : L.ny, L);
     const R* src = q + row_off(gj, L) + gi;
 #pragma unroll
     for (int c = 0; c < NEQ; ++c) qc[c] = src[c * L.pitch];
