@@ -72,8 +72,9 @@ def test_tiny_grids():
     _compare("euler-hlle", 2, 2, 3, 2, "minmod", ("periodic", "periodic"), seed=5)
 
 
-def test_fp32_bitwise_vs_fp32_oracle():
-    name, nx, ny = "shallow-water-roe", 50, 42
+@pytest.mark.parametrize("name", SOLVERS)
+def test_fp32_bitwise_vs_fp32_oracle(name):
+    nx, ny = 50, 42
     dx = dy = 1.0 / 50
     q, aux = random_state(name, nx, ny, 6, dtype=np.float32)
     oq, oreps = oracle_run(name, q, aux, nx, ny, dx, dy, steps=5, order=2, limiter="mc")
@@ -345,3 +346,67 @@ def test_persistent_line_kernel_walks_tiles_bitwise(name, bc):
     # 4-component fp64 systems run persistent CTAs (one per SM) that prefetch
     # the next tile with cp.async: > 148 tiles so CTAs walk several tiles
     _compare(name, 610, 331, 3, 2, "mc", (bc, bc), seed=23)
+
+
+@pytest.mark.parametrize("name,order,limiter", [("shallow-water-roe", 2, "mc"),
+                                                ("euler-hlle", 2, "minmod"),
+                                                ("acoustics-var", 1, "none")])
+def test_run_to_t_final_matches_oracle(name, order, limiter):
+    # device-resident run with the t_final truncation decided on the GPU
+    # (remaining = t_final - t, tolerance 1e-14 max(1, t_final), reference
+    # driver.py:508-530): same number of steps, same dts (the last one
+    # truncated), same state; the graph path is used (> 4 steps)
+    from paper_1308_1464_b200 import _abi
+    from helpers import device_grid
+    nx, ny = 48, 37
+    dx, dy = 1.0 / nx, 1.0 / ny
+    q, aux = random_state(name, nx, ny, 24)
+    oq = np.asfortranarray(q.copy())
+    oa = np.asfortranarray(aux.copy()) if aux is not None else None
+    solver = O.make_solver(name, **PARAMS[name])
+    spec = O.Spec(nx, ny, dx, dy)
+    probe = O.step(np.asfortranarray(q.copy()), oa, spec, solver, O.Controller(0.9),
+                   bc_x="periodic", bc_y="periodic", order=order, limiter=limiter)
+    t_final = 11.37 * probe.dt                 # ~12 steps, the last one truncated
+    oreps = O.run(oq, oa, spec, solver, O.Controller(0.9), t_final=t_final,
+                  bc_x="periodic", bc_y="periodic", order=order, limiter=limiter)
+    g = device_grid(name, nx, ny, dx, dy, order=order, limiter=limiter, bc_x="periodic",
+                    bc_y="periodic")
+    try:
+        g.upload(q, aux)
+        g.run(50, _abi.make_ctl(0.9, t_final=t_final))   # more than needed: stops itself
+        res = g.poll()
+        assert res.error.code == 0
+        assert res.steps_done == len(oreps)
+        assert [r[0] for r in res.reports] == [r.dt for r in oreps]
+        assert abs(res.t - t_final) <= 1e-14 * max(1.0, t_final)
+        assert same_bits(oq, g.download())
+    finally:
+        g.close()
+
+
+def test_driver_run_t_final_and_remaining():
+    # the public driver API: run(config with t_final) and step(remaining=...)
+    from paper_1308_1464_b200 import (BoundaryCondition, GridSpec, SimulationConfig,
+                                      TimestepController, initial_condition, run, step)
+    spec = GridSpec(nx=40, ny=30, dx=1 / 40, dy=1 / 30, num_eqn=3, num_aux=0)
+    cfg = SimulationConfig(spec=spec, kernel="shallow-water-roe", ic="sw-dam-break",
+                           t_final=0.05, order=2, limiter="mc",
+                           bc_x=BoundaryCondition.EXTRAPOLATE, bc_y=BoundaryCondition.EXTRAPOLATE)
+    state, reps = run(cfg, TimestepController(0.9))
+    assert abs(sum(r.dt for r in reps) - 0.05) <= 1e-14
+    st, aux, _ = initial_condition("sw-dam-break", spec)
+    oq = np.asfortranarray(st.data.copy())
+    solver = O.make_solver("shallow-water-roe", **PARAMS["shallow-water-roe"])
+    oreps = O.run(oq, None, O.Spec(40, 30, 1 / 40, 1 / 30), solver, O.Controller(0.9),
+                  t_final=0.05, bc_x="extrapolate", bc_y="extrapolate", order=2, limiter="mc")
+    assert [r.dt for r in reps] == [r.dt for r in oreps]
+    assert same_bits(oq, state.data)
+    # one step with remaining smaller than the CFL dt takes exactly `remaining`
+    cfg1 = SimulationConfig(spec=spec, kernel="shallow-water-roe", ic="sw-dam-break",
+                            num_steps=1, order=2, limiter="mc",
+                            bc_x=BoundaryCondition.EXTRAPOLATE,
+                            bc_y=BoundaryCondition.EXTRAPOLATE)
+    st, aux, _ = initial_condition("sw-dam-break", spec)
+    _, rep = step(st, aux, cfg1, TimestepController(0.9), remaining=1e-5)
+    assert rep.dt == 1e-5
