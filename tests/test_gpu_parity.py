@@ -410,3 +410,15 @@ def test_driver_run_t_final_and_remaining():
     st, aux, _ = initial_condition("sw-dam-break", spec)
     _, rep = step(st, aux, cfg1, TimestepController(0.9), remaining=1e-5)
     assert rep.dt == 1e-5
+
+
+@pytest.mark.parametrize("env", ["WS_PDL=0", "WS_PERSIST=0", "WS_SPEEDS=smem"])
+def test_alternative_launch_paths_bitwise(monkeypatch, env):
+    # the non-default execution paths (plain launches, non-persistent 4-component
+    # line kernel, shared-memory pre-pass) give the same bits
+    k, v = env.split("=")
+    monkeypatch.setenv(k, v)
+    for name in ("shallow-water-roe", "euler-hlle", "acoustics-var"):
+        _compare(name, 610, 97, 3, 2, "mc", ("periodic", "extrapolate"), seed=25)
+    _compare("euler", 131, 75, 4, 2, "superbee", ("extrapolate", "extrapolate"), seed=26,
+             use_run=True)
