@@ -1118,6 +1118,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   int i0, j0;
   tile_origin(t, i0, j0);
   Ctl ctl;
+  bool stage_ok = true;   // CHECKS: every staged cell admissible (per thread)
   const unsigned long long t_start = L.trace ? gtimer() : 0ull;
   // PDL: the next step's pre-pass may launch once every CTA of this grid has
   // started (it waits for this grid's completion before reading anything).
@@ -1200,16 +1201,19 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         for (int c = 0; c < NEQ; ++c) sQ[c * HC + idx] = qs[k][c];
 #pragma unroll
         for (int c = 0; c < NAUX; ++c) sA[c * HC + idx] = as[k][c];
+        R pc[NP1];
         if (NPR > 0) {
-          R pc[NP1];
           prims_fast<S>(qs[k], as[k], P, pc);
 #pragma unroll
           for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
         }
+        if (CHECKS) stage_ok = stage_ok && S::cell_ok(qs[k], as[k], pc, P);
       }
     }
   }
-  __syncthreads();
+  // CHECKS (static speeds, no pre-pass): a tile whose staged cells are all
+  // admissible cannot report an error, so its edges skip the checked probe
+  const bool tile_clean = CHECKS ? (__syncthreads_and(stage_ok) != 0) : (__syncthreads(), true);
   ctl = s_ctl;
   if (ctl.skip) break;
   {
@@ -1226,8 +1230,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       const int ei = i0 - 1 + lane;
       R ap[NEQ], amn[NEQ], fl[NEQ], fr[NEQ];
       line_edge<S, R, ORDER, LIM, CHECKS, 1, HC>(sQ, sA, sP, P, L, cl, cr, ei, j0 + r,
-                                                  lane >= 1 && lane <= 30 && ei <= L.nx, dtdx,
-                                                  key, ap, amn, fl, fr);
+                                                  !tile_clean && lane >= 1 && lane <= 30 &&
+                                                      ei <= L.nx,
+                                                  dtdx, key, ap, amn, fl, fr);
       if (cell_lane) {
         const int c = lane - 1;
 #pragma unroll
@@ -1250,7 +1255,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       const int ej = j0 - 1 + lane;
       R ap[NEQ], amn[NEQ], fl[NEQ], fr[NEQ];
       line_edge<S, R, ORDER, LIM, CHECKS, 2, HC>(sQ, sA, sP, P, L, cl, cr, i0 + c, ej,
-                                                  lane >= 1 && lane <= 30 && ej < L.ny_edges_y,
+                                                  !tile_clean && lane >= 1 && lane <= 30 &&
+                                                      ej < L.ny_edges_y,
                                                   dtdy, key, ap, amn, fl, fr);
       R qnew[NEQ];
       const int rr = lane - 1, o = rr * LW + c;
