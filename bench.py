@@ -308,7 +308,10 @@ def gpu_arm(args):
                 "frac": achieved / peak, "traffic": None, "kernel": "k_update",
                 "peak_kind": peak_kind, "kernel_ms": upd_ms,
                 "speeds_kernel_ms": statistics.mean(t_spd) if dyn else 0.0,
-                "algorithmic_bytes_per_cell": bpc}
+                "algorithmic_bytes_per_cell": bpc,
+                "timing": "CUDA events on the launching stream around each kernel, in a second "
+                          "loop of the same K steps (an event between the two kernels costs the "
+                          "programmatic overlap, so the headline loop has none)"}
     roofline["kernel"] = "k_update_w"
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):

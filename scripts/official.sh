@@ -5,9 +5,11 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/o_smoke.log 2>&1
 ./tools/fp64_peak > gpurun_out/o_fp64_peak.json 2>&1
 python bench.py > gpurun_out/o_bench.json 2> gpurun_out/o_bench.err; echo bench_rc=$?
 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/o_bench_ref.json 2> gpurun_out/o_bench_ref.err; echo ref_rc=$?
-CMD="python bench.py --steps 6 --warmup 3 --no-e2e --no-cpu"
-$CMD > gpurun_out/o_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/o_launches.csv $CMD > gpurun_out/o_ncu_launch.log 2>&1
+# launch list of the exact default bench command (it exited 0 just above)
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/o_launches.csv python bench.py > gpurun_out/o_ncu_launch.log 2>&1
 echo launch_rc=$?
+CMD="python bench.py --steps 6 --warmup 3 --no-e2e --no-cpu"
+$CMD > gpurun_out/o_plain.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_update_w|k_speeds" -s 8 -c 2 -o gpurun_out/o_prof $CMD > gpurun_out/o_ncu_full.log 2>&1
 echo full_rc=$?
 ncu -i gpurun_out/o_prof.ncu-rep --page raw --csv > gpurun_out/o_raw.csv 2>/dev/null
