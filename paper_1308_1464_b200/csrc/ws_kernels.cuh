@@ -1155,6 +1155,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 #pragma unroll
         for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
       }
+      if (CHECKS) stage_ok = stage_ok && S::cell_ok(qc, ac, pc, P);
     }
     __syncthreads();   // sR consumed: the next tile's copies may land
     if (t + (int)gridDim.x < ntiles) prefetch(t + (int)gridDim.x);
