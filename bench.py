@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--device-reduce", action="store_true",
+                    help="row-strip path: CFL reduction by the kernels over peer memory "
+                         "(symmetric memory) instead of an NCCL all-reduce")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the row-strip (NCCL) path even with one rank (tests it on 1 GPU)")
     ap.add_argument("--size", type=int, default=None,

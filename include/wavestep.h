@@ -192,6 +192,19 @@ int ws_fill_ghost(double* data, int32_t ncomp, int32_t nx, int32_t ny, int32_t b
 /* number of kernel launches this handle has issued (bench evidence) */
 int64_t ws_launch_count(const ws_handle* h);
 
+/* Device-side CFL reduction across row-strip shards (replaces the host
+ * all-reduce of the slot between ws_phase_speeds and ws_phase_update): with
+ * npeers > 0, the last CTA of each pre-pass (part 0 or 2) max-reduces this
+ * shard's 3-word slot into every table entry's slot (64-bit system-scope
+ * atomics; peers reached through P2P / symmetric-memory mappings) and
+ * increments their arrival counters; the update waits until npeers pushes
+ * for the step arrived.  peer_states[r] = ws_devstate_ptr of shard r as
+ * mapped on this GPU (self included); npeers = 0 turns it off.  All shards
+ * must ws_upload before any shard steps. */
+#define WS_MAX_PEERS 8
+int ws_set_peers(ws_handle* h, int32_t npeers, void* const* peer_states);
+void* ws_devstate_ptr(ws_handle* h);
+
 /* Diagnostics (no reference counterpart): with WS_TRACE=1 in the environment
  * at ws_create, every CTA of the CFL pre-pass (region 0) and of the update
  * kernel (region 1) writes {start ns, end ns, smid, block} (%globaltimer) on

@@ -178,6 +178,8 @@ void compute_layout(ws_handle* h) {
   L.nx_glob = d.nx;
   L.trace = nullptr;
   L.trace_cap = 0;
+  L.peers = nullptr;
+  L.npeers = 0;
   L.pitch = pitch_for(d.nx, h->esz);
   L.rstride = (long long)h->neq * L.pitch;
   L.astride = (long long)h->naux * L.pitch;
@@ -193,6 +195,7 @@ StepArgs make_args(ws_handle* h, const ws_ctl* c, int cur) {
   a.has_t_final = !std::isnan(c->t_final); a.t_final = c->t_final;
   a.tol = a.has_t_final ? 1e-14 * std::fmax(1.0, c->t_final) : 0.0;   // driver.py:525
   a.cur = cur;
+  a.seq = h->enq;
   a.static_speeds = (h->ops.static_speeds && !h->multi) ? 1 : 0;
   a.borders = h->borders;
   return a;
@@ -338,6 +341,7 @@ void ws_destroy(ws_handle* h) {
   if (h->own_ds && h->ds) cudaFree(h->ds);
   if (h->stage) cudaFree(h->stage);
   if (h->stage_out) cudaFree(h->stage_out);
+  if (h->peers_dev) cudaFree(h->peers_dev);
   if (h->ev_order) cudaEventDestroy(h->ev_order);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
@@ -651,6 +655,25 @@ int ws_sync(ws_handle* h) {
 }
 
 int64_t ws_launch_count(const ws_handle* h) { return h ? h->launches : 0; }
+
+void* ws_devstate_ptr(ws_handle* h) { return h ? (void*)h->ds : nullptr; }
+
+int ws_set_peers(ws_handle* h, int32_t npeers, void* const* peer_states) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (npeers < 0 || npeers > WS_MAX_PEERS || (npeers > 0 && !peer_states))
+    return fail(h, WS_ERR_CONFIG, "npeers must lie in [0, 8] with a pointer table");
+  if (npeers > 0 && (!h->line_kernel || h->fused || (h->ops.static_speeds && !h->multi)))
+    return fail(h, WS_ERR_CONFIG,
+                "device-side reduction needs the warp-line update with a CFL pre-pass");
+  if (!h->peers_dev) WS_CUDA(h, cudaMalloc(&h->peers_dev, sizeof(void*) * WS_MAX_PEERS));
+  if (npeers > 0) {
+    WS_CUDA(h, cudaMemcpy(h->peers_dev, peer_states, sizeof(void*) * npeers,
+                          cudaMemcpyHostToDevice));
+  }
+  h->L.peers = reinterpret_cast<DevState* const*>(h->peers_dev);
+  h->L.npeers = npeers;
+  return WS_OK;
+}
 
 int ws_trace(ws_handle* h, uint64_t* out, int64_t cap, int64_t* n) {
   if (!h || !out || !n) return WS_ERR_CONFIG;

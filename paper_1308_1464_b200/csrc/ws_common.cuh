@@ -23,6 +23,9 @@ enum : int { LIM_NONE = 0, LIM_MINMOD = 1, LIM_SUPERBEE = 2, LIM_MC = 3 };
 constexpr int REPCAP = 4096;          // device report ring (steps between polls)
 constexpr int ERR_KERNEL = 1;
 constexpr int ERR_STATIONARY = 4;
+constexpr int ERR_WAIT_TIMEOUT = 3;   // a device-side wait gave up (reported as WS_ERR_CUDA)
+
+struct DevState;
 
 struct Layout {
   int nx, ny;             // local interior
@@ -36,6 +39,8 @@ struct Layout {
   long long astride;      // elements per grid row of aux (num_aux * pitch)
   unsigned long long* trace;  // CTA timeline (WS_TRACE=1 diagnostics) or null
   int trace_cap;              // CTAs per traced kernel
+  struct DevState* const* peers;  // device-side slot reduce: every shard's state (or null)
+  int npeers;
 };
 
 // Programmatic dependent launch (sm_90+): a kernel launched with the
@@ -46,6 +51,13 @@ struct Layout {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// system-scope acquire load (peer GPUs write the counter over NVLink)
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // CTA timeline record (diagnostics): {start ns, end ns, smid, linear block}
@@ -80,13 +92,15 @@ struct DevState {
   unsigned long long err_key;
   double t;                           // simulated time since upload
   int finished;                       // t_final reached
-  int pad_;
+  int pdone;                          // pre-pass CTA counter (device-side slot push)
   long long nrep;                     // reports written (ring index)
+  unsigned long long arrive;          // slot pushes received from the shards (device reduce)
   Report rep[REPCAP];
 };
 
 struct StepArgs {
   double dx, dy;
+  long long seq;        // steps enqueued since upload (device reduce: arrivals to await)
   double cfl, dt_max, fixed_dt, remaining, t_final, tol;
   int has_dt_max, has_fixed, has_remaining, has_t_final;
   int cur;              // slot parity of this step

@@ -88,6 +88,7 @@ struct ws_handle {
   bool pdl = true;              // programmatic dependent launch of the step kernels
   bool persist = true;          // persistent prefetching line kernel where it applies
   cudaError_t launch_err = cudaSuccess;  // first failed cudaLaunchKernelEx (reported once)
+  void* peers_dev = nullptr;    // device table of the shards' DevState (device-side reduce)
   size_t border_bytes = 0;
   std::string err;
 };
@@ -185,7 +186,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   static const P& prm(ws_handle* h) { return *reinterpret_cast<const P*>(h->params.data()); }
 
   static void speeds(ws_handle* h, const void* q, int cur, int part, cudaStream_t st) {
-    if (h->speeds_smem && part == 0) {
+    if (h->speeds_smem && part == 0 && h->L.npeers == 0) {
       constexpr int TY = spd_ty<S, R>();
       dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + TY - 1) / TY);
       k_speeds<S, R, SPD_TX, TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(

@@ -329,6 +329,27 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
     }
     atomicMax(&ds->slot[cur][0], bx);
     atomicMax(&ds->slot[cur][1], by);
+    if (L.npeers > 0 && part != 1) {
+      // device-side reduction across shards: the last CTA pushes this
+      // shard's slot into every shard's slot (64-bit MAX, over NVLink for
+      // peers) and then announces the push with a release increment
+      __threadfence();
+      if (atomicAdd(&ds->pdone, 1) == (int)(gridDim.x * gridDim.y) - 1) {
+        __threadfence();
+        ds->pdone = 0;
+        const unsigned long long v0 = atomicOr(&ds->slot[cur][0], 0ull);
+        const unsigned long long v1 = atomicOr(&ds->slot[cur][1], 0ull);
+        const unsigned long long v2 = atomicOr(&ds->slot[cur][2], 0ull);
+        for (int r = 0; r < L.npeers; ++r) {
+          DevState* pr = L.peers[r];
+          atomicMax_system(&pr->slot[cur][0], v0);
+          atomicMax_system(&pr->slot[cur][1], v1);
+          if (v2) atomicMax_system(&pr->slot[cur][2], v2);
+        }
+        __threadfence_system();
+        for (int r = 0; r < L.npeers; ++r) atomicAdd_system(&L.peers[r]->arrive, 1ull);
+      }
+    }
     if (L.trace) trace_cta(L, 0, t_start);
   }
 }
@@ -1046,6 +1067,17 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
   }
 }
 
+// device-side reduction across shards: wait until every shard pushed its
+// slot for this step (release/acquire through the arrival counter)
+__device__ __forceinline__ void wait_arrivals(DevState* ds, unsigned long long need) {
+  long long spins = 0;
+  while (ld_acquire_sys(&ds->arrive) < need) {
+    if (__ldcg(&ds->err)) return;
+    __nanosleep(128);
+    if (++spins > (1ll << 24)) { atomicCAS(&ds->err, 0, ERR_WAIT_TIMEOUT); return; }
+  }
+}
+
 // --------------------------------------------------------------------------
 // Warp-per-line fused update (default for 3-component systems).
 //
@@ -1132,6 +1164,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     if (t < ntiles) prefetch(t);
     if (tid == NT - 32) {
       if (!CHECKS) pdl_wait();
+      if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (A.seq + 1));
       const Ctl c0 = step_control<R>(A, ds, !CHECKS);
       s_ctl = c0;
       s_dtd[0] = (R)(c0.dt / A.dx);
@@ -1189,6 +1222,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     // the first warps) while its loads are in flight
     if (tid == NT - 32) {
       if (!CHECKS) pdl_wait();
+      if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (A.seq + 1));
       const Ctl c0 = step_control<R>(A, ds, !CHECKS);
       s_ctl = c0;
       s_dtd[0] = (R)(c0.dt / A.dx);

@@ -187,6 +187,16 @@ class DeviceGrid:
     def sync(self):
         self._check(self.lib.ws_sync(self.h))
 
+    def devstate_ptr(self) -> int:
+        return self.lib.ws_devstate_ptr(self.h)
+
+    def set_peers(self, state_ptrs):
+        """Device-side CFL reduction across shards (ws_set_peers): the
+        DevState pointers of every shard as mapped on this GPU, self
+        included; [] turns it off."""
+        arr = (ctypes.c_void_p * max(1, len(state_ptrs)))(*state_ptrs)
+        self._check(self.lib.ws_set_peers(self.h, len(state_ptrs), arr))
+
     def launches(self) -> int:
         return int(self.lib.ws_launch_count(self.h))
 

@@ -111,13 +111,16 @@ def post_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=
     return dist.batch_isend_irecv(ops) if ops else []
 
 
-def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl, group=None):
+def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl, group=None,
+                 device_reduce: bool = False):
     """One globally consistent time step.
 
     The halo rows travel while the pre-pass runs on everything that does not
     read them (all x-edges, y-edges of rows >= 1: part 1); the y-edges of row
     0 follow once the low ghost rows are in (part 2), then the MAX all-reduce
-    of the slot and the update (which reads both ghost-row pairs).
+    of the slot and the update (which reads both ghost-row pairs).  With
+    ``device_reduce`` (shards set up with ``set_peers``) the all-reduce is
+    done by the kernels themselves over peer memory.
     """
     ctx = getattr(shard, "stream_context", None)
     with ctx() if ctx is not None else contextlib.nullcontext():
@@ -125,9 +128,12 @@ def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl,
         shard.phase_speeds_interior()
         finish_halos(shard, reqs)
         shard.phase_speeds_boundary()
-        slot = shard.slot_view()
-        dist.all_reduce(slot, op=dist.ReduceOp.MAX, group=group)
-        shard.slot_reduced()
+        if not device_reduce:
+            slot = shard.slot_view()
+            dist.all_reduce(slot, op=dist.ReduceOp.MAX, group=group)
+            shard.slot_reduced()
+        # (device_reduce: the pre-pass pushed the slot into every shard's and
+        # the update waits for all pushes on the device — no host collective)
         shard.phase_update(ctl)
 
 
@@ -148,7 +154,7 @@ class CudaShard:
     (NCCL) without copies."""
 
     def __init__(self, case, strips: RowStrips, rank: int, device, periodic_y: bool,
-                 precision: str = "f64", stream=None):
+                 precision: str = "f64", stream=None, symmetric: bool = False):
         import torch
 
         from .device import DeviceGrid
@@ -175,7 +181,13 @@ class CudaShard:
         u8 = dict(dtype=torch.uint8, device=device)
         self.bufs = [torch.zeros(qb.value, **u8), torch.zeros(qb.value, **u8)]
         self.aux_buf = torch.zeros(max(ab.value, 8), **u8)
-        self.slots = torch.zeros((sb.value + 7) // 8 * 8, **u8)
+        nslot = (sb.value + 7) // 8 * 8
+        if symmetric:
+            import torch.distributed._symmetric_memory as symm
+            self.slots = symm.empty(nslot, dtype=torch.uint8, device=device)
+            self.slots.zero_()
+        else:
+            self.slots = torch.zeros(nslot, **u8)
         self.grid = DeviceGrid(case.nx, self.ny, case.dx, case.dy, kernel, order=case.order,
                                limiter=case.limiter, bc_x=case.bc, bc_y=case.bc,
                                precision=precision, device=device.index or 0,
@@ -196,6 +208,23 @@ class CudaShard:
 
     def stream_context(self):
         return self.torch.cuda.stream(self.torch_stream)
+
+    def set_peers(self, state_ptrs):
+        """Device-side slot reduction: DevState pointers of all shards (this
+        shard's slots buffer is its DevState), as mapped on this GPU."""
+        self.grid.set_peers(state_ptrs)
+
+    def enable_device_reduce(self, group=None):
+        """Map every rank's DevState through torch symmetric memory and hand
+        the table to the library (multi-GPU, one process per GPU).  The
+        shard's slots buffer must have been allocated symmetric
+        (``CudaShard(..., symmetric=True)``)."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        grp = group if group is not None else dist.group.WORLD
+        hdl = symm.rendezvous(self.slots, grp)
+        ptrs = [int(hdl.buffer_ptrs[r]) for r in range(hdl.world_size)]
+        self.set_peers(ptrs)
 
     def _current(self):
         ptr, pitch, row = self.grid.state_ptr()
@@ -266,16 +295,22 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     glob, gaux = stack(base.q), stack(base.aux)
     case = base
     periodic = base.bc == "periodic"
-    shard = CudaShard(case, strips, rank, dev, periodic, prec)
+    dred = bool(getattr(args, "device_reduce", False))
+    shard = CudaShard(case, strips, rank, dev, periodic, prec, symmetric=dred)
+    if dred:
+        shard.enable_device_reduce()
     npdt = np.float64 if prec == "f64" else np.float32
     host_q = np.asfortranarray(shard_block(glob, j0, j1), dtype=npdt)
     host_aux = (np.asfortranarray(shard_block(gaux, j0, j1), dtype=npdt)
                 if gaux is not None else None)
     shard.grid.upload(host_q, host_aux, stream=shard.stream)
+    if dred:
+        torch.cuda.synchronize()
+        dist.barrier()      # every arrival counter reset before the first push
     ctl = _abi.make_ctl(case.cfl)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
-        sharded_step(dist, shard, strips, rank, periodic, ctl)
+        sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
     torch.cuda.synchronize()
     res = shard.grid.poll()
     shard.grid.raise_for(res.error)
@@ -293,7 +328,7 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
         for i in range(k):
             flush.zero_()
             evs[i][0].record()
-            sharded_step(dist, shard, strips, rank, periodic, ctl)
+            sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
             evs[i][1].record()
         torch.cuda.synchronize()
     dist.barrier()
@@ -309,7 +344,7 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     e2e = None
     if not getattr(args, "no_e2e", False):
         e2e = sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, cells,
-                          UNIT, dev)
+                          UNIT, dev, dred)
     if rank == 0:
         peak, kind = peak_fn()
         bpc = configs.bytes_per_cell(case.kernel, prec)
@@ -322,7 +357,9 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
                        "nx": case.nx, "ny": ny_g, "limiter": case.limiter, "order": case.order,
                        "cfl": case.cfl, "parallelism": f"row-strips{world}",
                        "l2": "flushed between timed steps (512 MiB write)",
-                       "timed_step": "halo exchange + CFL pre-pass + MAX all-reduce + update"},
+                       "timed_step": ("halo exchange + CFL pre-pass + device-side slot reduction over "
+                           "peer memory + update") if dred else
+                          "halo exchange + CFL pre-pass + MAX all-reduce + update"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "whole step",
                          "peak_kind": kind},
@@ -337,7 +374,8 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     return 0
 
 
-def sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, cells, unit, dev):
+def sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, cells, unit, dev,
+                dred=False):
     """Whole-job e2e at N ranks through the public API: per step every rank
     uploads its strip from pinned host memory, the sharded step runs, every
     rank downloads its strip; wall time max over ranks."""
@@ -348,16 +386,21 @@ def sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, c
     pq, pa = pin(host_q), pin(host_aux)
     out = pin(np.zeros_like(host_q))
     n = max(3, min(k, 10))
-    for _ in range(2):
+    def one():
         shard.grid.upload(pq, pa, stream=shard.stream)
-        sharded_step(dist, shard, strips, rank, periodic, ctl)
+        if dred:
+            # every rank's upload resets its arrival counter before anyone pushes
+            torch.cuda.synchronize()
+            dist.barrier()
+        sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
         shard.grid.download(out, stream=shard.stream)
+
+    for _ in range(2):
+        one()
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(n):
-        shard.grid.upload(pq, pa, stream=shard.stream)
-        sharded_step(dist, shard, strips, rank, periodic, ctl)
-        shard.grid.download(out, stream=shard.stream)
+        one()
     el = time.perf_counter() - t0
     t = torch.tensor([el], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)

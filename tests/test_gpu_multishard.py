@@ -16,7 +16,8 @@ from oracle import wavestep_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc):
+def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
+                 device_reduce=False):
     import torch
 
     from paper_1308_1464_b200 import _abi
@@ -35,6 +36,12 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc):
         sh.grid.upload(PL.shard_block(gq, j0, j1),
                        PL.shard_block(gaux, j0, j1) if gaux is not None else None,
                        stream=sh.stream)
+    if device_reduce:
+        # every shard's DevState (its slots buffer) in every shard's table:
+        # the pre-passes push their slots, the updates wait for P arrivals
+        ptrs = [sh.slots.data_ptr() for sh in shards]
+        for sh in shards:
+            sh.set_peers(ptrs)
     ctl = _abi.make_ctl(0.9)
     torch.cuda.set_stream(stream)
     for _ in range(steps):
@@ -51,11 +58,13 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc):
                 views[lo][3].copy_(views[r][0])     # my bottom rows -> lower neighbour's high ghosts
         for sh in shards:
             sh.phase_speeds_boundary()
-        slot = shards[0].slot_view().clone()
-        for sh in shards[1:]:
-            slot = torch.maximum(slot, sh.slot_view())
+        if not device_reduce:
+            slot = shards[0].slot_view().clone()
+            for sh in shards[1:]:
+                slot = torch.maximum(slot, sh.slot_view())
+            for sh in shards:
+                sh.slot_view().copy_(slot)
         for sh in shards:
-            sh.slot_view().copy_(slot)
             sh.phase_update(ctl)
     torch.cuda.synchronize()
     torch.cuda.set_stream(torch.cuda.default_stream(dev))
@@ -116,5 +125,51 @@ def test_split_prepass_needs_a_prepass():
             g.phase_speeds(part=1)
         with pytest.raises(ValueError, match="part must be"):
             g.phase_speeds(part=3)
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("name,P,bc", [("shallow-water-roe", 3, "periodic"),
+                                       ("euler-hlle", 2, "extrapolate"),
+                                       ("acoustics-var", 4, "extrapolate")])
+def test_device_side_reduction_bitwise(name, P, bc):
+    # ws_set_peers: no host collective at all — the pre-pass kernels push
+    # their slots into every shard's and the updates wait for all pushes
+    nx, ny, steps = 45, 70, 5
+    dx, dy = 1 / nx, 1 / ny
+    gq, gaux = random_state(name, nx, ny, 27)
+    ref, oreps = oracle_run(name, gq, gaux, nx, ny, dx, dy, steps=steps, order=2,
+                            limiter="mc", bc_x=bc, bc_y=bc)
+    out, reps, errs, strips = fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, 2, "mc",
+                                           bc, device_reduce=True)
+    for r in range(P):
+        j0, j1 = strips.bounds(r)
+        assert errs[r].code == 0
+        assert reps[r] == [o.dt for o in oreps]
+        assert np.array_equal(out[r], ref[:, 2:-2, 2 + j0:2 + j1]), f"shard {r}"
+
+
+def test_device_side_reduction_reports_the_global_first_error():
+    from paper_1308_1464_b200 import _abi
+    name, nx, ny = "shallow-water-roe", 20, 24
+    gq, _ = random_state(name, nx, ny, 22)
+    gq[0, 2 + 7, 2 + 19] = -1.0            # lives on strip 2 of 3
+    with pytest.raises(O.OracleError) as oe:
+        oracle_run(name, gq, None, nx, ny, 1 / nx, 1 / ny, steps=1, order=2, limiter="mc")
+    _, _, errs, _ = fake_sharded(name, gq, None, nx, ny, 1 / nx, 1 / ny, 3, 1, 2, "mc",
+                                 "extrapolate", device_reduce=True)
+    for e in errs:
+        assert e.code == _abi.WS_ERR_KERNEL
+        assert f"{'xy'[e.direction]}-interface (i={e.i}, j={e.j})" == str(oe.value).split(":")[0]
+
+
+def test_set_peers_validation():
+    from helpers import device_grid
+    g = device_grid("acoustics-const", 16, 16, 1 / 16, 1 / 16)
+    try:
+        with pytest.raises(ValueError, match="device-side reduction needs"):
+            g.set_peers([g.devstate_ptr()])
+        with pytest.raises(ValueError, match="npeers must lie"):
+            g.set_peers([g.devstate_ptr()] * 9)
     finally:
         g.close()

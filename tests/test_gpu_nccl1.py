@@ -27,9 +27,10 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,bc", [("shallow-water-roe", "extrapolate"),
-                                     ("euler-hlle", "periodic")])
-def test_nccl_world1_sharded_step_bitwise(name, bc):
+@pytest.mark.parametrize("name,bc,device_reduce", [("shallow-water-roe", "extrapolate", False),
+                                                   ("euler-hlle", "periodic", False),
+                                                   ("shallow-water-roe", "periodic", True)])
+def test_nccl_world1_sharded_step_bitwise(name, bc, device_reduce):
     import torch
     import torch.distributed as dist
 
@@ -47,11 +48,16 @@ def test_nccl_world1_sharded_step_bitwise(name, bc):
         case = SimpleNamespace(kernel=name, kernel_params=PARAMS[name], nx=nx, dx=1 / nx,
                                dy=1 / ny, order=2, limiter="mc", bc=bc)
         strips = PL.RowStrips(ny, 1)
-        sh = PL.CudaShard(case, strips, 0, dev, bc == "periodic")
+        sh = PL.CudaShard(case, strips, 0, dev, bc == "periodic", symmetric=device_reduce)
+        if device_reduce:
+            # symmetric-memory rendezvous of the DevState buffers (the
+            # multi-GPU path of ws_set_peers), here with one rank
+            sh.enable_device_reduce()
         sh.grid.upload(PL.shard_block(gq, 0, ny), None, stream=sh.stream)
         ctl = _abi.make_ctl(0.9)
         for _ in range(steps):
-            PL.sharded_step(dist, sh, strips, 0, bc == "periodic", ctl)
+            PL.sharded_step(dist, sh, strips, 0, bc == "periodic", ctl,
+                            device_reduce=device_reduce)
         torch.cuda.synchronize()
         res = sh.grid.poll()
         assert res.error.code == 0
@@ -75,3 +81,15 @@ def test_bench_force_sharded_line():
     assert line["config"]["parallelism"] == "row-strips1"
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
     assert line["gpu_launches"] > 0
+
+
+def test_bench_force_sharded_device_reduce_line():
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+               WORLD_SIZE="1", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-sharded",
+                        "--device-reduce", "--steps", "4", "--warmup", "3"], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert "device-side slot reduction" in line["config"]["timed_step"]
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
