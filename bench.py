@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--device-reduce", action="store_true",
                     help="row-strip path: CFL reduction by the kernels over peer memory "
                          "(symmetric memory) instead of an NCCL all-reduce")
+    ap.add_argument("--device-halo", action="store_true",
+                    help="row-strip path: halo rows pushed by the update kernel into the "
+                         "neighbours' ghost rows over peer memory (implies --device-reduce)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the row-strip (NCCL) path even with one rank (tests it on 1 GPU)")
     ap.add_argument("--size", type=int, default=None,

@@ -204,6 +204,17 @@ int64_t ws_launch_count(const ws_handle* h);
 #define WS_MAX_PEERS 8
 int ws_set_peers(ws_handle* h, int32_t npeers, void* const* peer_states);
 void* ws_devstate_ptr(ws_handle* h);
+/* Device-side halo exchange (replaces the host halo send/recv): the update
+ * kernel stores this shard's two first / last rows straight into the low /
+ * high neighbour's ghost rows (lo_q / hi_q = the neighbour's two state
+ * buffers, ping-pong order, as mapped on this GPU; ny_lo = the low
+ * neighbour's row count) and releases the neighbour's arrival counter
+ * (lo_state / hi_state = its DevState); the pre-pass (part 2 / 0) waits for
+ * the pushes it is owed before reading ghost rows.  Null state = that side
+ * has no neighbour.  Use with ws_set_peers (the slot reduction orders the
+ * buffer reuse across shards). */
+int ws_set_halo_peers(ws_handle* h, void* const* lo_q, void* lo_state, int32_t ny_lo,
+                      void* const* hi_q, void* hi_state);
 
 /* Diagnostics (no reference counterpart): with WS_TRACE=1 in the environment
  * at ws_create, every CTA of the CFL pre-pass (region 0) and of the update

@@ -96,6 +96,8 @@ SIGNATURES = [
     ("ws_trace", C.c_int, [_P, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     ("ws_set_peers", C.c_int, [_P, C.c_int32, C.POINTER(C.c_void_p)]),
     ("ws_devstate_ptr", C.c_void_p, [_P]),
+    ("ws_set_halo_peers", C.c_int, [_P, C.POINTER(C.c_void_p), C.c_void_p, C.c_int32,
+                                    C.POINTER(C.c_void_p), C.c_void_p]),
     ("ws_riemann", C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int32, C.c_int64,
                              _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int32]),
     ("ws_fill_ghost", C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

@@ -180,6 +180,10 @@ void compute_layout(ws_handle* h) {
   L.trace_cap = 0;
   L.peers = nullptr;
   L.npeers = 0;
+  L.nq_lo[0] = L.nq_lo[1] = L.nq_hi[0] = L.nq_hi[1] = nullptr;
+  L.nds_lo = L.nds_hi = nullptr;
+  L.ny_lo = 0;
+  L.hsides = 0;
   L.pitch = pitch_for(d.nx, h->esz);
   L.rstride = (long long)h->neq * L.pitch;
   L.astride = (long long)h->naux * L.pitch;
@@ -657,6 +661,26 @@ int ws_sync(ws_handle* h) {
 int64_t ws_launch_count(const ws_handle* h) { return h ? h->launches : 0; }
 
 void* ws_devstate_ptr(ws_handle* h) { return h ? (void*)h->ds : nullptr; }
+
+int ws_set_halo_peers(ws_handle* h, void* const* lo_q, void* lo_state, int32_t ny_lo,
+                      void* const* hi_q, void* hi_state) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  const bool lo = lo_state != nullptr, hi = hi_state != nullptr;
+  if ((lo && (!lo_q || !lo_q[0] || !lo_q[1] || ny_lo < 2)) || (hi && (!hi_q || !hi_q[0] || !hi_q[1])))
+    return fail(h, WS_ERR_CONFIG, "halo peer: both state buffers, its DevState and ny >= 2");
+  if ((lo && h->L.lo != ROWS_MEMORY) || (hi && h->L.hi != ROWS_MEMORY))
+    return fail(h, WS_ERR_CONFIG, "halo peers only on sides whose ghost rows are in memory");
+  if ((lo || hi) && (!h->line_kernel || h->fused))
+    return fail(h, WS_ERR_CONFIG, "device-side halos need the warp-line update");
+  h->L.nq_lo[0] = lo ? lo_q[0] : nullptr; h->L.nq_lo[1] = lo ? lo_q[1] : nullptr;
+  h->L.nq_hi[0] = hi ? hi_q[0] : nullptr; h->L.nq_hi[1] = hi ? hi_q[1] : nullptr;
+  h->L.nds_lo = static_cast<DevState*>(lo_state);
+  h->L.nds_hi = static_cast<DevState*>(hi_state);
+  h->L.ny_lo = lo ? ny_lo : 0;
+  // pushes this shard receives per step: one per neighbour side it has
+  h->L.hsides = (h->L.lo == ROWS_MEMORY && lo ? 1 : 0) + (h->L.hi == ROWS_MEMORY && hi ? 1 : 0);
+  return WS_OK;
+}
 
 int ws_set_peers(ws_handle* h, int32_t npeers, void* const* peer_states) {
   if (!h) return fail(h, WS_ERR_CONFIG, "null argument");

@@ -41,6 +41,14 @@ struct Layout {
   int trace_cap;              // CTAs per traced kernel
   struct DevState* const* peers;  // device-side slot reduce: every shard's state (or null)
   int npeers;
+  // device-side halo push: the neighbours' two state buffers (this GPU's
+  // mapping), their DevState, the low neighbour's row count; null = none
+  void* nq_lo[2];
+  void* nq_hi[2];
+  struct DevState* nds_lo;
+  struct DevState* nds_hi;
+  int ny_lo;
+  int hsides;                 // ghost-row sides this shard receives by push (0..2)
 };
 
 // Programmatic dependent launch (sm_90+): a kernel launched with the
@@ -95,6 +103,8 @@ struct DevState {
   int pdone;                          // pre-pass CTA counter (device-side slot push)
   long long nrep;                     // reports written (ring index)
   unsigned long long arrive;          // slot pushes received from the shards (device reduce)
+  unsigned long long harrive;         // halo-row pushes received from the neighbours
+  int hsent[2];                       // this step's boundary tiles pushed (low / high side)
   Report rep[REPCAP];
 };
 

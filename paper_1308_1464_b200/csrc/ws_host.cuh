@@ -186,7 +186,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   static const P& prm(ws_handle* h) { return *reinterpret_cast<const P*>(h->params.data()); }
 
   static void speeds(ws_handle* h, const void* q, int cur, int part, cudaStream_t st) {
-    if (h->speeds_smem && part == 0 && h->L.npeers == 0) {
+    if (h->speeds_smem && part == 0 && h->L.npeers == 0 && h->L.hsides == 0) {
       constexpr int TY = spd_ty<S, R>();
       dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + TY - 1) / TY);
       k_speeds<S, R, SPD_TX, TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(
@@ -199,7 +199,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
                 part == 2 ? 2 : (h->L.ny + 1 + KC * NW - 1) / (KC * NW));
       launch(h, k_speeds_w<S, R, KC, NW, 1, MB>, grid, dim3(NW * 32), 0, st,
              static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, part,
-             h->ds);
+             (long long)h->enq, h->ds);
     }
     h->launches++;
   }

@@ -182,6 +182,18 @@ k_speeds(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   }
 }
 
+// spin (acquire, system scope) until a device counter written by other
+// shards reaches `need`; gives up with ERR_WAIT_TIMEOUT (never in a healthy run)
+__device__ __forceinline__ void wait_counter(const unsigned long long* cnt, unsigned long long need,
+                                             DevState* ds) {
+  long long spins = 0;
+  while (ld_acquire_sys(cnt) < need) {
+    if (__ldcg(&ds->err)) return;
+    __nanosleep(128);
+    if (++spins > (1ll << 24)) { atomicCAS(&ds->err, 0, ERR_WAIT_TIMEOUT); return; }
+  }
+}
+
 // --------------------------------------------------------------------------
 // CFL / admissibility pre-pass, register form (the default).  One warp owns a
 // strip of 31 edge columns x KC edge rows: lane l holds cell column
@@ -196,7 +208,7 @@ template <class S, class R, int KC, int NWS, int UNR, int MINB>
 __global__ void __launch_bounds__(NWS * 32, MINB)
 k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
            const typename S::template Params<R> P, const int cur, const int part,
-           DevState* __restrict__ ds) {
+           const long long seq, DevState* __restrict__ ds) {
   constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   __shared__ unsigned long long sred[2][NWS];
@@ -207,6 +219,13 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   // everything below reads the previous update's output; the next update may
   // launch only after that update completed, i.e. after this wait returned
   pdl_wait();
+  if (L.hsides > 0 && part != 1) {
+    // device-side halos: the neighbours' updates pushed this step's ghost
+    // rows; wait for all of them (the update launched after us stages ghost
+    // rows too, so the trigger comes after this wait)
+    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * seq, ds);
+    __syncthreads();
+  }
   pdl_trigger();
   const int ci = blockIdx.x * 31 - 1 + lane;                 // this lane's cell column
   const int gi = map_i(ci < L.nx ? ci : L.nx, L);
@@ -1070,12 +1089,7 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
 // device-side reduction across shards: wait until every shard pushed its
 // slot for this step (release/acquire through the arrival counter)
 __device__ __forceinline__ void wait_arrivals(DevState* ds, unsigned long long need) {
-  long long spins = 0;
-  while (ld_acquire_sys(&ds->arrive) < need) {
-    if (__ldcg(&ds->err)) return;
-    __nanosleep(128);
-    if (++spins > (1ll << 24)) { atomicCAS(&ds->err, 0, ERR_WAIT_TIMEOUT); return; }
-  }
+  wait_counter(&ds->arrive, need, ds);
 }
 
 // --------------------------------------------------------------------------
@@ -1393,7 +1407,10 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       }
     }
 
-    // ---- row-coalesced store of the tile
+    // ---- row-coalesced store of the tile; the strip's two first / last rows
+    // also go straight into the low / high neighbour's ghost rows (P2P
+    // stores into its buffer of the same parity) when halos are pushed
+    const int par = A.cur ^ 1;
     for (int idx = tid; idx < LW * LW; idx += NT) {
       const int rr = idx / LW, c = idx % LW;
       const int gi = i0 + c, gj = j0 + rr;
@@ -1401,6 +1418,36 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         R* dst = qn + row_off(gj, L) + gi;
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = sX[m * (LW * LW) + idx];
+        if (L.nds_lo && gj < 2) {
+          R* rd = static_cast<R*>(L.nq_lo[par]) + (long long)(L.ny_lo + 2 + gj) * L.rstride + gi;
+#pragma unroll
+          for (int m = 0; m < NEQ; ++m) rd[m * L.pitch] = sX[m * (LW * LW) + idx];
+        }
+        if (L.nds_hi && gj >= L.ny - 2) {
+          R* rd = static_cast<R*>(L.nq_hi[par]) + (long long)(gj - (L.ny - 2)) * L.rstride + gi;
+#pragma unroll
+          for (int m = 0; m < NEQ; ++m) rd[m * L.pitch] = sX[m * (LW * LW) + idx];
+        }
+      }
+    }
+    if ((L.nds_lo && j0 < 2) || (L.nds_hi && j0 + LW > L.ny - 2)) {
+      // boundary tile: once every such tile of a side stored, release the
+      // neighbour (system fence, then one increment of its arrival counter)
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        const int ntxl = (L.nx + LW - 1) / LW;
+        if (L.nds_lo && j0 < 2 && atomicAdd(&ds->hsent[0], 1) == ntxl - 1) {
+          ds->hsent[0] = 0;
+          atomicAdd_system(&L.nds_lo->harrive, 1ull);
+        }
+        if (L.nds_hi && j0 + LW > L.ny - 2) {
+          const int rows = ((L.ny - 1) / LW != (L.ny - 2) / LW) ? 2 : 1;   // tile rows holding ny-2, ny-1
+          if (atomicAdd(&ds->hsent[1], 1) == rows * ntxl - 1) {
+            ds->hsent[1] = 0;
+            atomicAdd_system(&L.nds_hi->harrive, 1ull);
+          }
+        }
       }
     }
     if (CHECKS && key != ~0ull) atomicMax(&ds->slot[A.cur][2], NKEY_MAX - key);

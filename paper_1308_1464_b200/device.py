@@ -190,6 +190,16 @@ class DeviceGrid:
     def devstate_ptr(self) -> int:
         return self.lib.ws_devstate_ptr(self.h)
 
+    def set_halo_peers(self, lo=None, hi=None):
+        """Device-side halo push (ws_set_halo_peers): lo = (q0, q1, state,
+        ny) of the low neighbour, hi = (q0, q1, state) of the high one, as
+        device pointers mapped on this GPU; None = no neighbour."""
+        lq = (ctypes.c_void_p * 2)(*(lo[:2] if lo else (None, None)))
+        hq = (ctypes.c_void_p * 2)(*(hi[:2] if hi else (None, None)))
+        self._check(self.lib.ws_set_halo_peers(self.h, lq, lo[2] if lo else None,
+                                               int(lo[3]) if lo else 0, hq,
+                                               hi[2] if hi else None))
+
     def set_peers(self, state_ptrs):
         """Device-side CFL reduction across shards (ws_set_peers): the
         DevState pointers of every shard as mapped on this GPU, self

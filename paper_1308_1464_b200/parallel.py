@@ -74,6 +74,10 @@ class RowStrips:
                 _abi.ROWS_MEMORY if hi is not None else _abi.ROWS_BC)
 
 
+def periodic_rows(bc: str) -> bool:
+    return bc == "periodic"
+
+
 def shard_block(global_field: np.ndarray, j0: int, j1: int) -> np.ndarray:
     """Rows [j0-2, j1+2) of a global (ncomp, nx+4, ny+4) F-order field: the
     shard's host block, its ghost rows being the neighbours' interior rows."""
@@ -112,7 +116,7 @@ def post_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=
 
 
 def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl, group=None,
-                 device_reduce: bool = False):
+                 device_reduce: bool = False, device_halo: bool = False):
     """One globally consistent time step.
 
     The halo rows travel while the pre-pass runs on everything that does not
@@ -124,9 +128,20 @@ def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl,
     """
     ctx = getattr(shard, "stream_context", None)
     with ctx() if ctx is not None else contextlib.nullcontext():
-        reqs = post_halos(dist, shard, strips, rank, periodic, group)
-        shard.phase_speeds_interior()
-        finish_halos(shard, reqs)
+        if device_halo and not getattr(shard, "halos_primed", True):
+            # first step after an upload: the ghost rows come from the host
+            # exchange once; every later step's are pushed by the kernels
+            exchange_halos(dist, shard, strips, rank, periodic, group)
+            shard.halos_primed = True
+            shard.phase_speeds_interior()
+        elif device_halo:
+            # the neighbours' update kernels already stored our ghost rows;
+            # part 2 of the pre-pass waits for them on the device
+            shard.phase_speeds_interior()
+        else:
+            reqs = post_halos(dist, shard, strips, rank, periodic, group)
+            shard.phase_speeds_interior()
+            finish_halos(shard, reqs)
         shard.phase_speeds_boundary()
         if not device_reduce:
             slot = shard.slot_view()
@@ -179,7 +194,12 @@ class CudaShard:
         _abi.check(_abi.lib().ws_buffer_bytes(ctypes.byref(desc), ctypes.byref(qb),
                                               ctypes.byref(ab), ctypes.byref(sb)))
         u8 = dict(dtype=torch.uint8, device=device)
-        self.bufs = [torch.zeros(qb.value, **u8), torch.zeros(qb.value, **u8)]
+        if symmetric:
+            import torch.distributed._symmetric_memory as symm
+            self.bufs = [symm.empty(qb.value, dtype=torch.uint8, device=device).zero_()
+                         for _ in range(2)]
+        else:
+            self.bufs = [torch.zeros(qb.value, **u8), torch.zeros(qb.value, **u8)]
         self.aux_buf = torch.zeros(max(ab.value, 8), **u8)
         nslot = (sb.value + 7) // 8 * 8
         if symmetric:
@@ -213,6 +233,34 @@ class CudaShard:
         """Device-side slot reduction: DevState pointers of all shards (this
         shard's slots buffer is its DevState), as mapped on this GPU."""
         self.grid.set_peers(state_ptrs)
+
+    def upload(self, q_block, aux_block=None):
+        """Host block of this strip (ghost rows included); with device halos
+        the next step primes the ghost rows through the host exchange."""
+        self.grid.upload(q_block, aux_block, stream=self.stream)
+        self.halos_primed = False
+
+    def set_halo_peers(self, lo=None, hi=None):
+        """Device-side halos: lo = (q0, q1, state, ny) / hi = (q0, q1, state)
+        device pointers of the neighbour shards as mapped here."""
+        self.grid.set_halo_peers(lo, hi)
+
+    def enable_device_halo(self, strips, rank, periodic, group=None):
+        """Symmetric-memory rendezvous of the state buffers; hand the
+        neighbours' buffers and DevState to the library (the DevState table
+        comes from enable_device_reduce, which must run first)."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        grp = group if group is not None else dist.group.WORLD
+        h0 = symm.rendezvous(self.bufs[0], grp)
+        h1 = symm.rendezvous(self.bufs[1], grp)
+        hs = symm.rendezvous(self.slots, grp)
+        lo, hi = strips.neighbours(rank, periodic)
+        arg = lambda r: (int(h0.buffer_ptrs[r]), int(h1.buffer_ptrs[r]),  # noqa: E731
+                         int(hs.buffer_ptrs[r]))
+        self.set_halo_peers(None if lo is None else arg(lo) + (strips.bounds(lo)[1] -
+                                                                strips.bounds(lo)[0],),
+                            None if hi is None else arg(hi))
 
     def enable_device_reduce(self, group=None):
         """Map every rank's DevState through torch symmetric memory and hand
@@ -293,24 +341,35 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
         return g
 
     glob, gaux = stack(base.q), stack(base.aux)
+    if periodic_rows(base.bc):
+        # periodic y: the outermost strips' memory ghost rows wrap around
+        # (static aux rows are never exchanged, so they must be right here)
+        for g in (glob, gaux):
+            if g is not None:
+                g[:, :, 0:2] = g[:, :, ny_g:ny_g + 2]
+                g[:, :, ny_g + 2:ny_g + 4] = g[:, :, 2:4]
     case = base
     periodic = base.bc == "periodic"
-    dred = bool(getattr(args, "device_reduce", False))
+    dhalo = bool(getattr(args, "device_halo", False))
+    dred = bool(getattr(args, "device_reduce", False)) or dhalo
     shard = CudaShard(case, strips, rank, dev, periodic, prec, symmetric=dred)
     if dred:
         shard.enable_device_reduce()
+    if dhalo:
+        shard.enable_device_halo(strips, rank, periodic)
     npdt = np.float64 if prec == "f64" else np.float32
     host_q = np.asfortranarray(shard_block(glob, j0, j1), dtype=npdt)
     host_aux = (np.asfortranarray(shard_block(gaux, j0, j1), dtype=npdt)
                 if gaux is not None else None)
-    shard.grid.upload(host_q, host_aux, stream=shard.stream)
+    shard.upload(host_q, host_aux)
     if dred:
         torch.cuda.synchronize()
         dist.barrier()      # every arrival counter reset before the first push
     ctl = _abi.make_ctl(case.cfl)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
-        sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
+        sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred,
+                     device_halo=dhalo)
     torch.cuda.synchronize()
     res = shard.grid.poll()
     shard.grid.raise_for(res.error)
@@ -328,7 +387,8 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
         for i in range(k):
             flush.zero_()
             evs[i][0].record()
-            sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
+            sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred,
+                     device_halo=dhalo)
             evs[i][1].record()
         torch.cuda.synchronize()
     dist.barrier()
@@ -344,7 +404,7 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     e2e = None
     if not getattr(args, "no_e2e", False):
         e2e = sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, cells,
-                          UNIT, dev, dred)
+                          UNIT, dev, dred, dhalo)
     if rank == 0:
         peak, kind = peak_fn()
         bpc = configs.bytes_per_cell(case.kernel, prec)
@@ -357,7 +417,9 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
                        "nx": case.nx, "ny": ny_g, "limiter": case.limiter, "order": case.order,
                        "cfl": case.cfl, "parallelism": f"row-strips{world}",
                        "l2": "flushed between timed steps (512 MiB write)",
-                       "timed_step": ("halo exchange + CFL pre-pass + device-side slot reduction over "
+                       "timed_step": ("CFL pre-pass + update with halo rows and the slot reduction "
+                           "done by the kernels over peer memory") if dhalo else
+                          ("halo exchange + CFL pre-pass + device-side slot reduction over "
                            "peer memory + update") if dred else
                           "halo exchange + CFL pre-pass + MAX all-reduce + update"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -375,7 +437,7 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
 
 
 def sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, cells, unit, dev,
-                dred=False):
+                dred=False, dhalo=False):
     """Whole-job e2e at N ranks through the public API: per step every rank
     uploads its strip from pinned host memory, the sharded step runs, every
     rank downloads its strip; wall time max over ranks."""
@@ -387,12 +449,13 @@ def sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, c
     out = pin(np.zeros_like(host_q))
     n = max(3, min(k, 10))
     def one():
-        shard.grid.upload(pq, pa, stream=shard.stream)
+        shard.upload(pq, pa)
         if dred:
             # every rank's upload resets its arrival counter before anyone pushes
             torch.cuda.synchronize()
             dist.barrier()
-        sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
+        sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred,
+                     device_halo=dhalo)
         shard.grid.download(out, stream=shard.stream)
 
     for _ in range(2):

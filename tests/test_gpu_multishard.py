@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 
 def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
-                 device_reduce=False):
+                 device_reduce=False, device_halo=False):
     import torch
 
     from paper_1308_1464_b200 import _abi
@@ -26,6 +26,13 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
     case = SimpleNamespace(kernel=name, kernel_params=PARAMS[name], nx=nx, dx=dx, dy=dy,
                            order=order, limiter=limiter, bc=bc)
     periodic = bc == "periodic"
+    # the global ghost frame as the single domain sees it (static aux rows of
+    # a periodic strip boundary included)
+    gq = np.asfortranarray(gq.copy())
+    O.fill_ghost(gq, bc, bc)
+    if gaux is not None:
+        gaux = np.asfortranarray(gaux.copy())
+        O.fill_ghost(gaux, bc, bc)
     strips = PL.RowStrips(ny, P)
     # one shared stream: the torch copies standing in for NCCL are ordered
     # with every shard's kernels
@@ -42,20 +49,32 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
         ptrs = [sh.slots.data_ptr() for sh in shards]
         for sh in shards:
             sh.set_peers(ptrs)
+    if device_halo:
+        # each shard's update stores its boundary rows into the neighbours'
+        # ghost rows; their pre-pass part 2 waits for the pushes
+        for r, sh in enumerate(shards):
+            lo, hi = strips.neighbours(r, periodic)
+            info = lambda k: (shards[k].bufs[0].data_ptr(), shards[k].bufs[1].data_ptr(),  # noqa: E731
+                              shards[k].slots.data_ptr())
+            sh.set_halo_peers(None if lo is None else info(lo) + (shards[lo].ny,),
+                              None if hi is None else info(hi))
     ctl = _abi.make_ctl(0.9)
     torch.cuda.set_stream(stream)
-    for _ in range(steps):
+    for it in range(steps):
         # part 1 of the pre-pass runs BEFORE the halo rows are refreshed (the
         # ghost rows still hold the previous step's values): it must not read them
         for sh in shards:
             sh.phase_speeds_interior()
-        views = [sh.halo_views() for sh in shards]
-        for r in range(P):
-            lo, hi = strips.neighbours(r, periodic)
-            if hi is not None:
-                views[hi][2].copy_(views[r][1])     # my top rows -> upper neighbour's low ghosts
-            if lo is not None:
-                views[lo][3].copy_(views[r][0])     # my bottom rows -> lower neighbour's high ghosts
+        if not device_halo or it == 0:
+            # (device halos: the first step's ghost rows are primed by a copy;
+            # later ones are pushed by the neighbours' update kernels)
+            views = [sh.halo_views() for sh in shards]
+            for r in range(P):
+                lo, hi = strips.neighbours(r, periodic)
+                if hi is not None:
+                    views[hi][2].copy_(views[r][1])  # my top rows -> upper neighbour's low ghosts
+                if lo is not None:
+                    views[lo][3].copy_(views[r][0])  # my bottom rows -> lower neighbour's high ghosts
         for sh in shards:
             sh.phase_speeds_boundary()
         if not device_reduce:
@@ -129,10 +148,14 @@ def test_split_prepass_needs_a_prepass():
         g.close()
 
 
-@pytest.mark.parametrize("name,P,bc", [("shallow-water-roe", 3, "periodic"),
-                                       ("euler-hlle", 2, "extrapolate"),
-                                       ("acoustics-var", 4, "extrapolate")])
-def test_device_side_reduction_bitwise(name, P, bc):
+@pytest.mark.parametrize("name,P,bc,halo", [("shallow-water-roe", 3, "periodic", False),
+                                            ("euler-hlle", 2, "extrapolate", False),
+                                            ("acoustics-var", 4, "extrapolate", False),
+                                            ("shallow-water-roe", 3, "periodic", True),
+                                            ("shallow-water-roe", 2, "periodic", True),
+                                            ("euler-hlle", 4, "extrapolate", True),
+                                            ("acoustics-var", 3, "periodic", True)])
+def test_device_side_reduction_bitwise(name, P, bc, halo):
     # ws_set_peers: no host collective at all — the pre-pass kernels push
     # their slots into every shard's and the updates wait for all pushes
     nx, ny, steps = 45, 70, 5
@@ -141,7 +164,7 @@ def test_device_side_reduction_bitwise(name, P, bc):
     ref, oreps = oracle_run(name, gq, gaux, nx, ny, dx, dy, steps=steps, order=2,
                             limiter="mc", bc_x=bc, bc_y=bc)
     out, reps, errs, strips = fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, 2, "mc",
-                                           bc, device_reduce=True)
+                                           bc, device_reduce=True, device_halo=halo)
     for r in range(P):
         j0, j1 = strips.bounds(r)
         assert errs[r].code == 0

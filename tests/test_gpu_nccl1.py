@@ -83,13 +83,15 @@ def test_bench_force_sharded_line():
     assert line["gpu_launches"] > 0
 
 
-def test_bench_force_sharded_device_reduce_line():
+@pytest.mark.parametrize("flag,text", [("--device-reduce", "device-side slot reduction"),
+                                       ("--device-halo", "done by the kernels over peer memory")])
+def test_bench_force_sharded_device_collective_line(flag, text):
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
                WORLD_SIZE="1", LOCAL_RANK="0")
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-sharded",
-                        "--device-reduce", "--steps", "4", "--warmup", "3"], env=env,
+                        flag, "--steps", "4", "--warmup", "3"], env=env,
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     line = json.loads(p.stdout.strip().splitlines()[-1])
-    assert "device-side slot reduction" in line["config"]["timed_step"]
+    assert text in line["config"]["timed_step"]
     assert line["value"] > 0 and line["e2e"]["value"] > 0
