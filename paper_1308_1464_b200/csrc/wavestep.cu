@@ -492,9 +492,21 @@ int ws_download_async(ws_handle* h, void* q, void* s) {
   return download_impl(h, q, h ? h->esz : 8, s, false);
 }
 
+// a row-strip shard can run whole steps only when the kernels do its
+// collectives (slot reduction and every memory ghost-row side pushed)
+static bool device_collectives(const ws_handle* h) {
+  const int mem_sides = (h->L.lo == ROWS_MEMORY ? 1 : 0) + (h->L.hi == ROWS_MEMORY ? 1 : 0);
+  return h->L.npeers > 0 && h->L.hsides == mem_sides;
+}
+
+static const char* kShardStepMsg =
+    "a row-strip shard steps through ws_phase_speeds / ws_phase_update with the host "
+    "exchanging halos and reducing the slot, or with ws_set_peers + ws_set_halo_peers";
+
 int ws_step(ws_handle* h, const ws_ctl* c, void* s) {
   if (!h || !c) return fail(h, WS_ERR_CONFIG, "null argument");
   if (!h->uploaded) return fail(h, WS_ERR_CONFIG, "no state uploaded");
+  if (h->multi && !device_collectives(h)) return fail(h, WS_ERR_CONFIG, kShardStepMsg);
   int rc = check_ctl(h, c);
   if (rc) return rc;
   cudaStream_t st = pick(h, s);
@@ -562,6 +574,7 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
   if (!h || !c) return fail(h, WS_ERR_CONFIG, "null argument");
   if (!h->uploaded) return fail(h, WS_ERR_CONFIG, "no state uploaded");
   if (nsteps < 0) return fail(h, WS_ERR_CONFIG, "nsteps must be >= 0");
+  if (h->multi && !device_collectives(h)) return fail(h, WS_ERR_CONFIG, kShardStepMsg);
   int rc = check_ctl(h, c);
   if (rc) return rc;
   cudaStream_t st = pick(h, s);
@@ -573,7 +586,9 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
     enqueue_step(h, c, 0, st); h->enq++; left--;
     enqueue_step(h, c, 1, st); h->enq++; left--;
   }
-  if (left >= 4 && st != nullptr) {
+  // shards with device collectives step without graphs (the arrival counts
+  // they wait for depend on the host's step sequence number)
+  if (left >= 4 && st != nullptr && !h->multi) {
     // two-step graph (parity 0 then 1), cached per (ctl, stream)
     if (!h->gexec || std::memcmp(&h->gctl, c, sizeof(ws_ctl)) != 0 || h->gstream != st) {
       if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }

@@ -196,3 +196,23 @@ def test_set_peers_validation():
             g.set_peers([g.devstate_ptr()] * 9)
     finally:
         g.close()
+
+
+def test_shard_refuses_whole_steps_without_device_collectives():
+    import torch
+    from paper_1308_1464_b200 import _abi
+    from paper_1308_1464_b200 import parallel as PL
+    name, nx, ny = "shallow-water-roe", 20, 24
+    gq, _ = random_state(name, nx, ny, 5)
+    case = SimpleNamespace(kernel=name, kernel_params=PARAMS[name], nx=nx, dx=1 / nx,
+                           dy=1 / ny, order=2, limiter="mc", bc="extrapolate")
+    strips = PL.RowStrips(ny, 2)
+    sh = PL.CudaShard(case, strips, 0, torch.device("cuda", 0), False)
+    try:
+        sh.upload(PL.shard_block(gq, *strips.bounds(0)))
+        with pytest.raises(ValueError, match="row-strip shard steps through"):
+            sh.grid.step(_abi.make_ctl(0.9))
+        with pytest.raises(ValueError, match="row-strip shard steps through"):
+            sh.grid.run(3, _abi.make_ctl(0.9))
+    finally:
+        sh.grid.close()
