@@ -202,6 +202,7 @@ StepArgs make_args(ws_handle* h, const ws_ctl* c, int cur) {
   a.seq = h->enq;
   a.static_speeds = (h->ops.static_speeds && !h->multi) ? 1 : 0;
   a.borders = h->borders;
+  a.tmax = h->tile_prepass ? h->tmax : nullptr;
   return a;
 }
 
@@ -295,7 +296,11 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   // opt-in with WS_FUSE=1
   h->line_kernel = true;          // warp-line kernel for every solver (WS_KERNEL=tile: tile kernel)
   if (const char* v = std::getenv("WS_KERNEL")) h->line_kernel = std::strcmp(v, "tile") != 0;
-  if (const char* v = std::getenv("WS_SPEEDS")) h->speeds_smem = std::strcmp(v, "smem") == 0;
+  if (const char* v = std::getenv("WS_SPEEDS")) {
+    h->speeds_smem = std::strcmp(v, "smem") == 0;
+    h->speeds_exact = std::strcmp(v, "exact") == 0;   // no candidate filter
+    h->speeds_edge = std::strcmp(v, "edge") == 0;     // per-edge filter (k_speeds_b)
+  }
   if (const char* v = std::getenv("WS_PDL")) h->pdl = std::atoi(v) != 0;
   if (const char* v = std::getenv("WS_PERSIST")) h->persist = std::atoi(v) != 0;
   {
@@ -312,6 +317,19 @@ int ws_create(const ws_desc* d, ws_handle** out) {
     return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
   }
   cudaMemsetAsync(h->borders, 0, h->border_bytes, h->stream);
+  // whole-tile CFL pre-pass (k_speeds_t): the update stores per-tile bound
+  // maxima of the state it writes, the next pre-pass skips tiles that cannot
+  // hold the step's maximum (WS_SPEEDS=exact|edge|smem select the others)
+  h->tile_prepass = h->ops.tile_prepass && !h->multi && h->line_kernel && !h->fused &&
+                    !h->speeds_exact && !h->speeds_smem && !h->speeds_edge;
+  if (h->tile_prepass) {
+    const size_t nt = (size_t)((d->nx + 28) / 29) * ((d->ny + 28) / 29);
+    // [2][nt] int4 tile accumulators, then the [nt] candidate list
+    if ((e = cudaMalloc(&h->tmax, 2 * nt * 16 + nt * 4)) != cudaSuccess) {
+      ws_destroy(h);
+      return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+    }
+  }
   h->ops.prepare();
   if (const char* v = std::getenv("WS_TRACE")) {
     if (std::atoi(v) != 0) {
@@ -350,6 +368,7 @@ void ws_destroy(ws_handle* h) {
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->borders) cudaFree(h->borders);
+  if (h->tmax) cudaFree(h->tmax);
   if (h->trace) cudaFree(h->trace);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;

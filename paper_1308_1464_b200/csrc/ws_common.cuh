@@ -105,6 +105,15 @@ struct DevState {
   unsigned long long arrive;          // slot pushes received from the shards (device reduce)
   unsigned long long harrive;         // halo-row pushes received from the neighbours
   int hsent[2];                       // this step's boundary tiles pushed (low / high side)
+  // CFL filter hint (k_speeds_b): per direction, the edge where the previous
+  // step's max |s| was found, packed (speed bits >> 29) << 29 | edge index;
+  // hint_acc[parity] accumulates this step's (64-bit MAX), the commit moves it
+  unsigned long long hint_acc[2][2];
+  unsigned long long hint[2];
+  int tmax_ok[2];                     // tile maxima of state buffer p written by its update
+  int pq[2][2];                       // tile pre-pass: candidate tiles listed / items taken
+  unsigned long long tnext[2][2];     // exact max|s| bits of one x / y edge of state buffer p
+                                      // (the update that wrote it probed its hint edges)
   Report rep[REPCAP];
 };
 
@@ -116,6 +125,7 @@ struct StepArgs {
   int cur;              // slot parity of this step
   int static_speeds;    // 1: max speeds come from DevState::static_bits
   int* borders;         // tile-border counters of the fused CFL epilogue
+  void* tmax;           // per-tile bound maxima [2][ntiles][4] R for k_speeds_t, or null
 };
 
 __device__ __forceinline__ int map_i(int i, const Layout& L) {

@@ -42,6 +42,7 @@ struct Ops {
   void (*prepare)();   // one-time kernel attributes (never inside a capture)
   int static_speeds;   // solver has q-independent speeds
   int can_fuse_line;   // warp-line kernel has the fused next-step CFL epilogue
+  int tile_prepass;    // solver has a bound (S::HAS_BOUND) and a non-persistent line kernel
 };
 
 }  // namespace wsh
@@ -85,6 +86,10 @@ struct ws_handle {
   unsigned long long* trace = nullptr;   // CTA timeline buffer (WS_TRACE=1)
   bool line_kernel = true;      // warp-per-line k_update_w (else the smem-tile k_update)
   bool speeds_smem = false;     // shared-memory tile pre-pass (else the register k_speeds_w)
+  bool speeds_exact = false;    // probe every edge (k_speeds_w) even where a filter exists
+  bool speeds_edge = false;     // per-edge candidate filter (k_speeds_b) instead of whole tiles
+  bool tile_prepass = false;    // k_speeds_t, fed by the update's per-tile bound maxima
+  void* tmax = nullptr;         // [2][ntiles][4] R per-tile bound maxima
   bool pdl = true;              // programmatic dependent launch of the step kernels
   bool persist = true;          // persistent prefetching line kernel where it applies
   cudaError_t launch_err = cudaSuccess;  // first failed cudaLaunchKernelEx (reported once)
@@ -191,6 +196,33 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
       dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + TY - 1) / TY);
       k_speeds<S, R, SPD_TX, TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(
           static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
+    } else if (HasBound<S>::value && h->tile_prepass && part == 0) {
+      if constexpr (HasBound<S>::value) {
+        constexpr int LW = 29, NWT = 8;
+        const int nt = ((h->L.nx + LW - 1) / LW) * ((h->L.ny + LW - 1) / LW);
+        int* list = reinterpret_cast<int*>(static_cast<char*>(h->tmax) + 2 * (size_t)nt * 16);
+        launch(h, k_tiles_decide<S, R>, dim3((nt + 255) / 256), dim3(256), 0, st,
+               static_cast<const int4*>(h->tmax), h->L, prm(h), cur, list, h->ds);
+        h->launches++;
+        // persistent item loop: every warp the GPU holds at 4 CTAs per SM
+        // (fewer for small grids: 8 items per tile)
+        const long long items = (long long)nt * TILE_NG;
+        long long ctas = (items + NWT - 1) / NWT;
+        if (ctas > 148 * 4) ctas = 148 * 4;
+        launch(h, k_speeds_t<S, R, NWT>, dim3((unsigned)ctas), dim3(NWT * 32), 0, st,
+               static_cast<const R*>(q), static_cast<const R*>(h->aux),
+               static_cast<const int*>(list), h->L, prm(h), cur, h->ds);
+      }
+    } else if (HasBound<S>::value && !h->speeds_exact) {
+      // candidate-filter pre-pass (exact result, see k_speeds_b)
+      if constexpr (HasBound<S>::value) {
+        constexpr int KC = 8, NW = 4, MB = S::NEQ <= 3 ? 8 : 4;
+        dim3 grid((h->L.nx + 1 + 30) / 31,
+                  part == 2 ? 2 : (h->L.ny + 1 + KC * NW - 1) / (KC * NW));
+        launch(h, k_speeds_b<S, R, KC, NW, MB, 6>, grid, dim3(NW * 32), 0, st,
+               static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, part,
+               (long long)h->enq, h->ds);
+      }
     } else {
       // register pre-pass: 8 edge rows per warp, 4 warps per CTA (the best of
       // the geometries measured in round 1, DESIGN.md perf log)
@@ -320,6 +352,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     o.prepare = &prepare;
     o.static_speeds = S::STATIC_SPEEDS ? 1 : 0;
     o.can_fuse_line = CAN_FUSE ? 1 : 0;
+    o.tile_prepass = (HasBound<S>::value && !PERSIST_W) ? 1 : 0;
     return o;
   }
 };

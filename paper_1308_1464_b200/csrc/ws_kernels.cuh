@@ -14,6 +14,7 @@
 //               CTA to finish commits the step (report, t, counters).
 //   k_to_soa / k_to_aos / k_static_speed : layout conversion, acoustics setup.
 #pragma once
+#include <climits>
 #include <type_traits>
 
 #include "ws_solvers.cuh"
@@ -373,6 +374,523 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   }
 }
 
+// cp.async (LDGSTS): global -> shared without a register round trip, so the
+// next tile's loads are in flight while the current tile is computed
+__device__ __forceinline__ void cp_async(void* smem, const double* g) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_async(void* smem, const float* g) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// --------------------------------------------------------------------------
+// CFL / admissibility pre-pass with a candidate filter (solvers with
+// S::HAS_BOUND; the default for them).  Same warp geometry as k_speeds_w, but
+// an edge is probed exactly only if it can hold the step's maximum: every
+// edge gets a cheap upper bound B_e >= max|s|_e from per-cell seeds
+// (S::bound_cell, no IEEE division or square root), and with T any EXACT
+// max|s| of some edge of the current state (a lower bound of the step's
+// maximum M), an edge with B_e < T has max|s|_e <= B_e < T <= M and cannot
+// change the maximum.  So
+//     max over {e : B_e >= T} of max|s|_e  ==  M   (bit for bit),
+// and edges whose cells are not provably admissible are always probed
+// (checked probe: errors and their reference-order key are unchanged).
+// T per warp: the exact max|s| at the edge where the previous step's maximum
+// was found (DevState::hint, recorded by this kernel), the slot's running
+// maximum of this step, and each lane's own running maximum.
+template <class S, class = void> struct HasBound : std::false_type {};
+template <class S> struct HasBound<S, std::enable_if_t<S::HAS_BOUND>> : std::true_type {};
+
+constexpr unsigned long long HINT_IDX_MASK = (1ull << 29) - 1;
+template <class R>
+__device__ __forceinline__ unsigned long long hint_key(R s, long long idx) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong((double)s);
+  const unsigned long long ix = (idx >= 0 && idx < (long long)HINT_IDX_MASK)
+                                    ? (unsigned long long)idx : HINT_IDX_MASK;
+  return ((b >> 29) << 29) | ix;
+}
+
+// Exact max|s| on the current state at the hint edge of direction dir (0: x,
+// 1: y), or 0 when there is none, it is out of range, it reads ghost rows a
+// split step has not received yet (part 1), or it is not admissible.
+template <class S, class R>
+__device__ __forceinline__ R hint_probe(const R* __restrict__ q, const R* __restrict__ aux,
+                                        const Layout& L, const typename S::template Params<R>& P,
+                                        const DevState* ds, int dir, int part, int ytop) {
+  constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  const unsigned long long hk = __ldcg(&ds->hint[dir]);
+  const long long idx = (long long)(hk & HINT_IDX_MASK);
+  const long long w = dir == 0 ? (long long)L.nx + 1 : (long long)L.nx;
+  const long long hj = idx / w;
+  const int hi = (int)(idx - hj * w);
+  const bool use = hk != 0ull && (dir == 0 ? hj < L.ny
+                                           : (hj < L.ny_edges_y &&
+                                              (part != 1 || (hj != 0 && hj != ytop))));
+  if (!use) return (R)0;
+  R ql[NEQ], qr[NEQ], al[NA1], ar[NA1], pl[NP1], pr[NP1];
+  auto load_at = [&](int gcol, int gj, R (&qc)[NEQ], R (&ac)[NA1]) {
+    const R* src = q + row_off(gj, L) + gcol;
+#pragma unroll
+    for (int c = 0; c < NEQ; ++c) qc[c] = __ldcg(src + c * L.pitch);
+    if (NAUX > 0) {
+      const R* asrc = aux + (long long)(gj + 2) * L.astride + gcol;
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) ac[c] = __ldcg(asrc + c * L.pitch);
+    }
+  };
+  if (dir == 0) {
+    load_at(map_i(hi - 1, L), (int)hj, ql, al);
+    load_at(map_i(hi, L), (int)hj, qr, ar);
+  } else {
+    load_at(hi, map_j((int)hj - 1, L), ql, al);
+    load_at(hi, map_j((int)hj < L.ny ? (int)hj : L.ny, L), qr, ar);
+  }
+  if (NPR > 0) { prims_fast<S>(ql, al, P, pl); prims_fast<S>(qr, ar, P, pr); }
+  if (!(S::cell_ok(ql, al, pl, P) && S::cell_ok(qr, ar, pr, P))) return (R)0;
+  bool ok = true;
+  R sm;
+  int code;
+  if (dir == 0) {
+    code = S::template probe_fast<1, FastMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    if (!ok) code = S::template probe_fast<1, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+  } else {
+    code = S::template probe_fast<2, FastMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    if (!ok) code = S::template probe_fast<2, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+  }
+  return code == 0 ? sm : (R)0;   // an inadmissible edge (Euler c^2 <= 0) gives no bound
+}
+
+template <class S, class R, int KC, int NWS, int MINB, int RING>
+__global__ void __launch_bounds__(NWS * 32, MINB)
+k_speeds_b(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
+           const typename S::template Params<R> P, const int cur, const int part,
+           const long long seq, DevState* __restrict__ ds) {
+  constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  const R MARGIN = (R)BoundMath::MARGIN;
+  __shared__ unsigned long long sred[2][NWS];
+  __shared__ int s_skip;
+  const int tid = threadIdx.x, lane = tid & 31, wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const unsigned long long t_start = L.trace ? gtimer() : 0ull;
+  pdl_wait();
+  if (L.hsides > 0 && part != 1) {
+    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * seq, ds);
+    __syncthreads();
+  }
+  pdl_trigger();
+  const int ci = blockIdx.x * 31 - 1 + lane;
+  const int gi = map_i(ci < L.nx ? ci : L.nx, L);
+  const int brow = (part == 2 && blockIdx.y == 1) ? (L.ny_edges_y - 1) / (KC * NWS) : blockIdx.y;
+  const int jb = (brow * NWS + wid) * KC;
+  const bool xcol = lane >= 1 && ci <= L.nx && part != 2;
+  const bool ycol = lane >= 1 && ci < L.nx;
+  const int ytop = (L.hi == ROWS_MEMORY && L.ny_edges_y > L.ny) ? L.ny : -1;
+  const bool inner_rows = jb >= 1 && jb + KC + 1 < L.ny;
+  // per-thread ring of RING rows in shared memory, filled by cp.async: the
+  // row loop keeps RING - 1 rows in flight without holding them in registers
+  // (the pre-pass is bound by load latency once the per-edge work is gone).
+  // Each lane reads back only the elements it copied itself: no warp sync.
+  constexpr int NC = NEQ + NAUX;
+  __shared__ R ring[RING][NC][NWS * 32];
+  auto issue = [&](int t) {   // row jb - 1 + t into slot t % RING (always one group)
+    if (t <= KC) {
+      const int r = jb - 1 + t;
+      const int gj = inner_rows ? r : map_j(r < L.ny ? r : L.ny, L);
+      const R* src = q + row_off(gj, L) + gi;
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) cp_async(&ring[t % RING][c][tid], src + c * L.pitch);
+      if (NAUX > 0) {
+        const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+#pragma unroll
+        for (int c = 0; c < NAUX; ++c) cp_async(&ring[t % RING][NEQ + c][tid], asrc + c * L.pitch);
+      }
+    }
+    cp_commit();
+  };
+  auto take = [&](int t, R (&qc)[NEQ], R (&ac)[NA1]) {   // row jb - 1 + t, after its wait
+#pragma unroll
+    for (int c = 0; c < NEQ; ++c) qc[c] = ring[t % RING][c][tid];
+#pragma unroll
+    for (int c = 0; c < NAUX; ++c) ac[c] = ring[t % RING][NEQ + c][tid];
+  };
+#pragma unroll
+  for (int t = 0; t < RING; ++t) issue(t);
+
+  // the hint edges: lane 0 probes the x-edge, lane 1 the y-edge (exactly, on
+  // the current state; a hint that reads rows still in flight is skipped)
+  using NX = std::integral_constant<int, 1>;
+  using NY = std::integral_constant<int, 2>;
+  R gh = (R)0;
+  if (lane < 2) gh = hint_probe<S>(q, aux, L, P, ds, lane, part, ytop);
+  if (tid == 0) s_skip = __ldcg(&ds->err) | __ldcg(&ds->finished);
+  __syncthreads();
+  if (s_skip) { cp_wait<0>(); return; }
+  // lower bounds: the hint edges and this step's running maxima (exact |s| of
+  // current-state edges; in a sharded step possibly of other shards' edges)
+  R tx = __shfl_sync(0xffffffffu, gh, 0), ty = __shfl_sync(0xffffffffu, gh, 1);
+  tx = nmax(tx, Bits<R>::from(__ldcg(&ds->slot[cur][0])));
+  ty = nmax(ty, Bits<R>::from(__ldcg(&ds->slot[cur][1])));
+
+  R mx = (R)0, my = (R)0;
+  unsigned long long key = ~0ull, kx = 0ull, ky = 0ull;
+  auto probe = [&](auto ni_tag, const R* ql, const R* qr, const R* pl, const R* pr,
+                   const R* al, const R* ar, bool clean, int dir, int ei, int ej) -> R {
+    constexpr int NI = decltype(ni_tag)::value;
+    R sm;
+    bool ok = true;
+    int code;
+    if (clean) {
+      code = S::template probe_fast<NI, FastMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+      if (!ok) code = S::template probe_fast<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    } else {
+      code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    }
+    if (code) {
+      unsigned long long k = err_key(dir, ei, L.j_off + ej, (code & 0xff) - 1, code >> 8, L.nx);
+      key = k < key ? k : key;
+    }
+    return sm;
+  };
+
+  const int rows = L.ny > L.ny_edges_y ? L.ny : L.ny_edges_y;
+  const int nk = rows - jb < KC ? rows - jb : KC;
+  R qp[NEQ], ap[NA1];
+  if (nk > 0) {
+    cp_wait<RING - 1>();
+    take(0, qp, ap);
+    issue(RING);
+    R byp, bcp, bxd;
+    bool vp = S::bound_cell(qp, ap, P, bxd, byp, bcp);
+#pragma unroll 1
+    for (int k = 0; k < KC; ++k) {
+      if (k >= nk) break;
+      const int r = jb + k;
+      R qc[NEQ], ac[NA1];
+      cp_wait<RING - 1>();
+      take(k + 1, qc, ac);
+      issue(k + 1 + RING);
+      R bxc, byc, bcc;
+      const bool vc = S::bound_cell(qc, ac, P, bxc, byc, bcc);
+      const R bxl = __shfl_up_sync(0xffffffffu, bxc, 1);
+      const R bcl = __shfl_up_sync(0xffffffffu, bcc, 1);
+      const bool vl = __shfl_up_sync(0xffffffffu, vc, 1);
+      const R bndx = (nmax(bxl, bxc) + nmax(bcl, bcc)) * MARGIN;
+      const R bndy = (nmax(byp, byc) + nmax(bcp, bcc)) * MARGIN;
+      const bool candx = xcol && r < L.ny && (!(vl && vc) || !(bndx < nmax(tx, mx)));
+      const bool ghost_edge = r == 0 || r == ytop;
+      const bool candy = ycol && r < L.ny_edges_y && (part == 0 || (part == 2) == ghost_edge) &&
+                         (!(vp && vc) || !(bndy < nmax(ty, my)));
+      if (__any_sync(0xffffffffu, candx || candy)) {
+        R pc[NP1];
+        if (NPR > 0) prims_fast<S>(qc, ac, P, pc);
+        const bool okc = S::cell_ok(qc, ac, pc, P);
+        if (__any_sync(0xffffffffu, candx)) {
+          R ql[NEQ], al[NA1], pl[NP1];
+#pragma unroll
+          for (int c = 0; c < NEQ; ++c) ql[c] = __shfl_up_sync(0xffffffffu, qc[c], 1);
+#pragma unroll
+          for (int c = 0; c < NAUX; ++c) al[c] = __shfl_up_sync(0xffffffffu, ac[c], 1);
+#pragma unroll
+          for (int c = 0; c < NPR; ++c) pl[c] = __shfl_up_sync(0xffffffffu, pc[c], 1);
+          const bool okl = __shfl_up_sync(0xffffffffu, okc, 1);
+          if (candx) {
+            const R s = probe(NX{}, ql, qc, pl, pc, al, ac, okl && okc, 0, ci, r);
+            mx = nmax(mx, s);
+            const unsigned long long hk = hint_key(s, (long long)r * (L.nx + 1) + ci);
+            kx = hk > kx ? hk : kx;
+          }
+        }
+        if (candy) {
+          R pp[NP1];
+          if (NPR > 0) prims_fast<S>(qp, ap, P, pp);
+          const bool okp = S::cell_ok(qp, ap, pp, P);
+          const R s = probe(NY{}, qp, qc, pp, pc, ap, ac, okp && okc, 1, ci, r);
+          my = nmax(my, s);
+          const unsigned long long hk = hint_key(s, (long long)r * L.nx + ci);
+          ky = hk > ky ? hk : ky;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) qp[c] = qc[c];
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) ap[c] = ac[c];
+      byp = byc; bcp = bcc; vp = vc;
+    }
+  }
+  cp_wait<0>();
+  if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
+  // the maxima and the hint keys: warp-shuffle trees, then one atomic per
+  // CTA and value (hint keys only where some lane probed)
+  unsigned long long bx = Bits<R>::to(mx), by = Bits<R>::to(my);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long wx = __shfl_xor_sync(0xffffffffu, bx, o);
+    unsigned long long wy = __shfl_xor_sync(0xffffffffu, by, o);
+    unsigned long long hx = __shfl_xor_sync(0xffffffffu, kx, o);
+    unsigned long long hy = __shfl_xor_sync(0xffffffffu, ky, o);
+    bx = wx > bx ? wx : bx;
+    by = wy > by ? wy : by;
+    kx = hx > kx ? hx : kx;
+    ky = hy > ky ? hy : ky;
+  }
+  if (lane == 0) {
+    if (kx) atomicMax(&ds->hint_acc[cur][0], kx);
+    if (ky) atomicMax(&ds->hint_acc[cur][1], ky);
+    sred[0][wid] = bx; sred[1][wid] = by;
+  }
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int w = 1; w < NWS; ++w) {
+      bx = sred[0][w] > bx ? sred[0][w] : bx;
+      by = sred[1][w] > by ? sred[1][w] : by;
+    }
+    if (bx) atomicMax(&ds->slot[cur][0], bx);
+    if (by) atomicMax(&ds->slot[cur][1], by);
+    if (L.npeers > 0 && part != 1) {
+      __threadfence();
+      if (atomicAdd(&ds->pdone, 1) == (int)(gridDim.x * gridDim.y) - 1) {
+        __threadfence();
+        ds->pdone = 0;
+        const unsigned long long v0 = atomicOr(&ds->slot[cur][0], 0ull);
+        const unsigned long long v1 = atomicOr(&ds->slot[cur][1], 0ull);
+        const unsigned long long v2 = atomicOr(&ds->slot[cur][2], 0ull);
+        for (int r = 0; r < L.npeers; ++r) {
+          DevState* pr = L.peers[r];
+          atomicMax_system(&pr->slot[cur][0], v0);
+          atomicMax_system(&pr->slot[cur][1], v1);
+          if (v2) atomicMax_system(&pr->slot[cur][2], v2);
+        }
+        __threadfence_system();
+        for (int r = 0; r < L.npeers; ++r) atomicAdd_system(&L.peers[r]->arrive, 1ull);
+      }
+    }
+    if (L.trace) trace_cta(L, 0, t_start);
+  }
+}
+
+// --------------------------------------------------------------------------
+// CFL / admissibility pre-pass over whole tiles (single-domain solvers with
+// S::HAS_BOUND; the default for them), two kernels.
+//
+// The update kernel that wrote the state also stored, per 29x29 tile, integer
+// maxima of its new cells (S::tile_acc) and probed one x- and one y-edge of
+// the new state exactly (DevState::tnext: the edges where this step's maxima
+// were found).  Every edge a tile owns reads cells of the tile or of its 8
+// neighbours (boundary mapping included), so S::tile_bound over the 3x3
+// neighbourhood gives B_x(tile) >= max|s| of each x-edge it owns (B_y
+// likewise).  With T an exact max|s| of some edge of this state (tnext, the
+// running slot maximum), a tile with B_x * MARGIN < T cannot hold the x
+// maximum: its x-edges are not even loaded.  The others are probed exactly,
+// so the step's maxima are bit-identical to probing every edge.  A cell that
+// is inadmissible or outside the bound's range makes B infinite: its edges
+// are always probed with the checked probe (errors and their reference-order
+// key).  Without valid tile data (first step after an upload, another update
+// path) every tile is a candidate.
+//
+// k_tiles_decide: one thread per tile -> candidate list (warp-aggregated
+// atomics).  k_speeds_t: persistent warps pull (tile, 4-row group) items
+// from the list, so a few candidate tiles spread over the whole GPU.
+constexpr int TILE_RPW = 1, TILE_NG = 30;  // rows per item, items per tile (30 edge rows at most)
+
+template <class S, class R>
+__global__ void __launch_bounds__(256)
+k_tiles_decide(const int4* __restrict__ tmax, const Layout L, const typename S::template Params<R> P,
+               const int cur, int* __restrict__ list, DevState* __restrict__ ds) {
+  constexpr int LW = 29;
+  const R MARGIN = (R)BoundMath::MARGIN;
+  pdl_wait();
+  pdl_trigger();
+  const int ntx = (L.nx + LW - 1) / LW, nty = (L.ny + LW - 1) / LW;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool cx = false, cy = false;
+  if (t < ntx * nty && !(__ldcg(&ds->err) | __ldcg(&ds->finished))) {
+    cx = cy = true;
+    if (__ldcg(&ds->tmax_ok[cur])) {
+      const R tlx = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][0])),
+                         Bits<R>::from(__ldcg(&ds->slot[cur][0])));
+      const R tly = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][1])),
+                         Bits<R>::from(__ldcg(&ds->slot[cur][1])));
+      const int tx = t % ntx, ty = t / ntx;
+      const int4* tm = tmax + (long long)cur * ntx * nty;
+      // x-edges of a tile read its own cells and the left tile's last column
+      // (periodic: tile ntx-1 left of tile 0, tile 0 right of the last tile);
+      // y-edges likewise with the tile below / above
+      auto get = [&](int x, int y) { return __ldcg(tm + (long long)y * ntx + x); };
+      auto fold = [](int (&a)[4], const int4 v) {
+        a[0] = max(a[0], v.x); a[1] = max(a[1], v.y); a[2] = max(a[2], v.z); a[3] = min(a[3], v.w);
+      };
+      const int4 self = get(tx, ty);
+      int ax[4] = {self.x, self.y, self.z, self.w};
+      int ay[4] = {self.x, self.y, self.z, self.w};
+      const bool px = L.bcx == BC_PERIODIC, py = L.bcy == BC_PERIODIC;
+      if (tx > 0) fold(ax, get(tx - 1, ty));
+      else if (px) fold(ax, get(ntx - 1, ty));
+      if (px && tx == ntx - 1) fold(ax, get(0, ty));
+      if (ty > 0) fold(ay, get(tx, ty - 1));
+      else if (py) fold(ay, get(tx, nty - 1));
+      if (py && ty == nty - 1) fold(ay, get(tx, 0));
+      R bxx, byx, bcx, bxy, byy, bcy;
+      S::tile_bound(ax, P, bxx, byx, bcx);
+      S::tile_bound(ay, P, bxy, byy, bcy);
+      cx = !((bxx + bcx) * MARGIN < tlx);
+      cy = !((byy + bcy) * MARGIN < tly);
+    }
+  }
+  const bool cand = cx || cy;
+  const unsigned m = __ballot_sync(0xffffffffu, cand);
+  int base = 0;
+  if (lane == 0 && m) base = atomicAdd(&ds->pq[cur][0], __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (cand) list[base + __popc(m & ((1u << lane) - 1u))] = t | (cx ? 1 << 30 : 0) | (cy ? 1 << 31 : 0);
+}
+
+template <class S, class R, int NWT>
+__global__ void __launch_bounds__(NWT * 32, 4)
+k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int* __restrict__ list,
+           const Layout L, const typename S::template Params<R> P, const int cur,
+           DevState* __restrict__ ds) {
+  constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  constexpr int LW = 29, RPW = TILE_RPW;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long t_start = L.trace ? gtimer() : 0ull;
+  pdl_wait();
+  pdl_trigger();
+  const int ntx = (L.nx + LW - 1) / LW;
+  const int nitems = __ldcg(&ds->pq[cur][0]) * TILE_NG;
+
+  R mx = (R)0, my = (R)0;
+  unsigned long long key = ~0ull, kx = 0ull, ky = 0ull;
+  auto probe = [&](auto ni_tag, const R* ql, const R* qr, const R* pl, const R* pr,
+                   const R* al, const R* ar, bool clean, int dir, int ei, int ej) -> R {
+    constexpr int NI = decltype(ni_tag)::value;
+    R sm;
+    bool ok = true;
+    int code;
+    if (clean) {
+      code = S::template probe_fast<NI, FastMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+      if (!ok) code = S::template probe_fast<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    } else {
+      code = S::template probe<NI, IeeeMath>(ql, qr, pl, pr, al, ar, P, sm, ok);
+    }
+    if (code) {
+      unsigned long long k = err_key(dir, ei, L.j_off + ej, (code & 0xff) - 1, code >> 8, L.nx);
+      key = k < key ? k : key;
+    }
+    return sm;
+  };
+  using NX = std::integral_constant<int, 1>;
+  using NY = std::integral_constant<int, 2>;
+
+  bool worked = false;
+  // consecutive items go to different CTAs (SMs): a few candidate tiles
+  // still spread over the whole GPU
+  const int nwarps = gridDim.x * NWT;
+  const int wg = (int)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  for (int item = wg; item < nitems; item += nwarps) {
+    worked = true;
+    const int ent = __ldcg(list + item / TILE_NG), g = item % TILE_NG;
+    const int tile = ent & ((1 << 30) - 1);
+    const bool cx = (ent & (1 << 30)) != 0, cy = ent < 0;
+    const int i0 = (tile % ntx) * LW, j0 = (tile / ntx) * LW;
+    // edges owned: x-edges ei in [i0, iend) on rows [j0, min(j0+29, ny));
+    // y-edges ci in [i0, min(i0+29, nx)) on rows [j0, rend)
+    const int iend = i0 + LW >= L.nx ? L.nx + 1 : i0 + LW;
+    const int rend = j0 + LW >= L.ny ? L.ny_edges_y : j0 + LW;
+    const int ci = i0 - 1 + lane;
+    const int gi = map_i(ci < L.nx ? ci : L.nx, L);
+    const bool xcol = cx && lane >= 1 && ci < iend;
+    const bool ycol = cy && lane >= 1 && ci < (i0 + LW < L.nx ? i0 + LW : L.nx);
+    const int rb = j0 + g * RPW;
+    const int nr = rend - rb < RPW ? rend - rb : RPW;
+    if (nr <= 0) continue;
+    R qb[RPW + 1][NEQ], ab[RPW + 1][NA1];
+#pragma unroll
+    for (int k = 0; k <= RPW; ++k) {
+      if (k <= nr) {
+        const int r = rb - 1 + k;
+        const int gj = map_j(r < L.ny ? r : L.ny, L);
+        const R* src = q + row_off(gj, L) + gi;
+#pragma unroll
+        for (int c = 0; c < NEQ; ++c) qb[k][c] = __ldcg(src + c * L.pitch);
+        if (NAUX > 0) {
+          const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+#pragma unroll
+          for (int c = 0; c < NAUX; ++c) ab[k][c] = __ldcg(asrc + c * L.pitch);
+        }
+      }
+    }
+    R pp[NP1];
+    if (NPR > 0) prims_fast<S>(qb[0], ab[0], P, pp);
+    bool okp = S::cell_ok(qb[0], ab[0], pp, P);
+#pragma unroll
+    for (int k = 1; k <= RPW; ++k) {
+      if (k > nr) break;
+      const int r = rb - 1 + k;
+      R pc[NP1];
+      if (NPR > 0) prims_fast<S>(qb[k], ab[k], P, pc);
+      const bool okc = S::cell_ok(qb[k], ab[k], pc, P);
+      if (cx) {
+        R ql[NEQ], al[NA1], pl[NP1];
+#pragma unroll
+        for (int c = 0; c < NEQ; ++c) ql[c] = __shfl_up_sync(0xffffffffu, qb[k][c], 1);
+#pragma unroll
+        for (int c = 0; c < NAUX; ++c) al[c] = __shfl_up_sync(0xffffffffu, ab[k][c], 1);
+#pragma unroll
+        for (int c = 0; c < NPR; ++c) pl[c] = __shfl_up_sync(0xffffffffu, pc[c], 1);
+        const bool okl = __shfl_up_sync(0xffffffffu, okc, 1);
+        if (xcol && r < L.ny) {
+          const R sv = probe(NX{}, ql, qb[k], pl, pc, al, ab[k], okl && okc, 0, ci, r);
+          mx = nmax(mx, sv);
+          const unsigned long long hk = hint_key(sv, (long long)r * (L.nx + 1) + ci);
+          kx = hk > kx ? hk : kx;
+        }
+      }
+      if (ycol && r < L.ny_edges_y) {
+        const R sv = probe(NY{}, qb[k - 1], qb[k], pp, pc, ab[k - 1], ab[k], okp && okc, 1, ci, r);
+        my = nmax(my, sv);
+        const unsigned long long hk = hint_key(sv, (long long)r * L.nx + ci);
+        ky = hk > ky ? hk : ky;
+      }
+#pragma unroll
+      for (int c = 0; c < NPR; ++c) pp[c] = pc[c];
+      okp = okc;
+    }
+  }
+  if (worked) {
+    // per-warp results: at most one atomic per value and warp
+    if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
+    unsigned long long bxs = Bits<R>::to(mx), bys = Bits<R>::to(my);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long wx = __shfl_xor_sync(0xffffffffu, bxs, o);
+      unsigned long long wy = __shfl_xor_sync(0xffffffffu, bys, o);
+      unsigned long long hx = __shfl_xor_sync(0xffffffffu, kx, o);
+      unsigned long long hy = __shfl_xor_sync(0xffffffffu, ky, o);
+      bxs = wx > bxs ? wx : bxs;
+      bys = wy > bys ? wy : bys;
+      kx = hx > kx ? hx : kx;
+      ky = hy > ky ? hy : ky;
+    }
+    if (lane == 0) {
+      if (bxs) atomicMax(&ds->slot[cur][0], bxs);
+      if (bys) atomicMax(&ds->slot[cur][1], bys);
+      if (kx) atomicMax(&ds->hint_acc[cur][0], kx);
+      if (ky) atomicMax(&ds->hint_acc[cur][1], ky);
+    }
+  }
+  if (L.trace && threadIdx.x == 0) trace_cta(L, 0, t_start);
+}
+
 // --------------------------------------------------------------------------
 // commit: run by thread 0 of the last CTA of an update kernel
 template <class R>
@@ -399,8 +917,17 @@ __device__ __forceinline__ void commit_step(DevState* ds, const StepArgs& A, con
       v->t = v->t + c.dt;
     }
   }
+  // tile maxima of the state this step wrote: valid only after a committed
+  // step of an update that stored them (k_speeds_t probes every tile otherwise)
+  v->tmax_ok[A.cur ^ 1] = (A.tmax != nullptr && v->err == 0 && !c.finished && !c.stationary) ? 1 : 0;
+  // the filter hint of the next pre-pass: where this step's maxima were found
+  // (kept when this step's pre-pass recorded none, e.g. the exact pre-pass)
+  if (v->hint_acc[A.cur][0]) v->hint[0] = v->hint_acc[A.cur][0];
+  if (v->hint_acc[A.cur][1]) v->hint[1] = v->hint_acc[A.cur][1];
+  v->hint_acc[A.cur][0] = 0ull; v->hint_acc[A.cur][1] = 0ull;
   // this step's slot is consumed; it is the accumulator of the step after next
   v->slot[A.cur][0] = 0ull; v->slot[A.cur][1] = 0ull; v->slot[A.cur][2] = 0ull;
+  v->pq[A.cur][0] = 0; v->pq[A.cur][1] = 0;
   __threadfence();
   v->done = 0;
 }
@@ -580,20 +1107,6 @@ __device__ __forceinline__ void next_step_speeds(
   }
 }
 
-// cp.async (LDGSTS): global -> shared without a register round trip, so the
-// next tile's loads are in flight while the current tile is computed
-__device__ __forceinline__ void cp_async(void* smem, const double* g) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g));
-}
-__device__ __forceinline__ void cp_async(void* smem, const float* g) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N> __device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 // Persistent CTAs walk the tiles (t = blockIdx.x, += gridDim.x).  Per tile:
 // wait for its staged q(+aux) (issued one tile earlier), compute per-cell
@@ -990,6 +1503,35 @@ k_border(const R* __restrict__ q, const Layout L, const typename S::template Par
   }
 }
 
+// Which tile probes the next pre-pass's lower-bound edges (k_speeds_t): the
+// hint edge of each direction (where this step's maximum was found), moved
+// by at most one cell so that both of its cells are interior and lie in one
+// 29x29 tile.  pos[d] = offset of the lower / left cell in that tile (-1: not
+// this tile), any[d] = some tile owns it.
+__device__ __forceinline__ void hint_owner(unsigned long long hk, const Layout& L, int i0, int j0,
+                                           int d, int& pos, int& any) {
+  constexpr int LW = 29;
+  pos = -1; any = 0;
+  if (hk == 0ull) return;
+  const unsigned idx = (unsigned)(hk & HINT_IDX_MASK);
+  const unsigned w = d == 0 ? (unsigned)L.nx + 1u : (unsigned)L.nx;
+  const int hj = (int)(idx / w), hi = (int)(idx - (unsigned)hj * w);
+  int ci, cj;
+  if (d == 0) {
+    if (L.nx < 2 || hj >= L.ny) return;
+    ci = min(max(hi - 1, 0), L.nx - 2);
+    if (ci % LW == LW - 1) ci -= 1;
+    cj = hj;
+  } else {
+    if (L.ny < 2 || hi >= L.nx) return;
+    cj = min(max(hj - 1, 0), L.ny - 2);
+    if (cj % LW == LW - 1) cj -= 1;
+    ci = hi;
+  }
+  any = 1;
+  if (ci / LW == i0 / LW && cj / LW == j0 / LW) pos = (cj - j0) * LW + (ci - i0);
+}
+
 // one edge per lane of a grid line (see k_update_w): solve, optional
 // admissibility probe, wave limiter against lane +-1 (register shuffles),
 // correction flux; returns this lane's apdq / flux and the next lane's
@@ -1135,6 +1677,11 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   // handed over at the post-staging barrier
   __shared__ Ctl s_ctl;
   __shared__ R s_dtd[2];
+  __shared__ int s_hany[2], s_hpos[2];  // TMAX: hint edge owned by some tile / offset here (-1)
+  __shared__ int s_acc[4];              // TMAX: S::tile_acc of the tile (shared-memory atomics)
+  if (HasBound<S>::value && !PERSIST && !FUSED && tid == 0) {
+    s_acc[0] = 0; s_acc[1] = 0; s_acc[2] = INT_MIN; s_acc[3] = INT_MAX;
+  }
   // PERSIST (one CTA per SM, 4-component fp64): CTAs walk the tiles and
   // prefetch the next tile's raw state with cp.async while the current tile
   // computes; otherwise one tile per CTA (blockIdx)
@@ -1272,6 +1819,13 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 
     const bool cell_lane = lane >= 1 && lane <= LW;
 
+    // TMAX: the last warp walks one row fewer in the x pass; it fetches and
+    // decodes this step's hint edges (the pre-pass has completed: the
+    // step-control thread waited for it before the barrier above)
+    unsigned long long hk0 = 0ull, hk1 = 0ull;
+    const bool hwarp = HasBound<S>::value && !PERSIST && !FUSED && A.tmax != nullptr &&
+                       warp == NWARP - 1 && lane < 2;
+    if (hwarp) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
     // ---- x pass: warps walk rows; lane l = x-edge i0-1+l
     for (int r = warp; r < LW; r += NWARP) {
       if (j0 + r >= L.ny) break;
@@ -1291,6 +1845,11 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
           if (ORDER == 2) sX[(NEQ + m) * (LW * LW) + r * LW + c] = fr[m] - fl[m];
         }
       }
+    }
+    if (hwarp) {
+      int o, anyd;
+      hint_owner(hk0, L, i0, j0, lane, o, anyd);
+      s_hpos[lane] = o; s_hany[lane] = anyd;
     }
     __syncthreads();
 
@@ -1407,6 +1966,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       }
     }
 
+    int tb[4] = {0, 0, INT_MIN, INT_MAX};   // TMAX: this thread's S::tile_acc accumulator
     // ---- row-coalesced store of the tile; the strip's two first / last rows
     // also go straight into the low / high neighbour's ghost rows (P2P
     // stores into its buffer of the same parity) when halos are pushed
@@ -1418,6 +1978,16 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         R* dst = qn + row_off(gj, L) + gi;
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = sX[m * (LW * LW) + idx];
+        if constexpr (HasBound<S>::value && !PERSIST && !FUSED) {
+          // tile-bound ingredients of the new cell for the next pre-pass
+          // (k_speeds_t): integer maxima, no FP64 work
+          if (A.tmax) {
+            R qv[NEQ];
+#pragma unroll
+            for (int m = 0; m < NEQ; ++m) qv[m] = sX[m * (LW * LW) + idx];
+            S::tile_acc(qv, tb);
+          }
+        }
         if (L.nds_lo && gj < 2) {
           R* rd = static_cast<R*>(L.nq_lo[par]) + (long long)(L.ny_lo + 2 + gj) * L.rstride + gi;
 #pragma unroll
@@ -1427,6 +1997,16 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
           R* rd = static_cast<R*>(L.nq_hi[par]) + (long long)(gj - (L.ny - 2)) * L.rstride + gi;
 #pragma unroll
           for (int m = 0; m < NEQ; ++m) rd[m * L.pitch] = sX[m * (LW * LW) + idx];
+        }
+      }
+    }
+    if constexpr (HasBound<S>::value && !PERSIST && !FUSED) {
+      if (A.tmax) {
+        const int r0 = __reduce_max_sync(FULL, tb[0]), r1 = __reduce_max_sync(FULL, tb[1]);
+        const int r2 = __reduce_max_sync(FULL, tb[2]), r3 = __reduce_min_sync(FULL, tb[3]);
+        if (lane == 0) {
+          atomicMax(&s_acc[0], r0); atomicMax(&s_acc[1], r1);
+          atomicMax(&s_acc[2], r2); atomicMin(&s_acc[3], r3);
         }
       }
     }
@@ -1459,6 +2039,38 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   if (PERSIST) cp_wait<0>();   // no copy outstanding at exit
   __syncthreads();
   ctl = s_ctl;
+  if constexpr (HasBound<S>::value && !PERSIST && !FUSED) {
+    if (A.tmax && tid == 0 && !ctl.skip)
+      static_cast<int4*>(A.tmax)[(long long)(A.cur ^ 1) * ntiles + t] =
+          make_int4(s_acc[0], s_acc[1], s_acc[2], s_acc[3]);
+    // the hint edges on the new state, probed by the tile that holds both
+    // cells (sX is the stored new tile): the next pre-pass's exact lower bound
+    if (A.tmax && !ctl.skip && (tid == 0 || tid == 32)) {
+      const int d = tid >> 5;
+      const int o = s_hpos[d];
+      if (o >= 0) {
+        R ql[NEQ], qr[NEQ], pl[NP1], pr[NP1];
+        const int o2 = d == 0 ? o + 1 : o + LW;
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) { ql[m] = sX[m * (LW * LW) + o]; qr[m] = sX[m * (LW * LW) + o2]; }
+        R sm = (R)0;
+        if (NPR > 0) { prims_fast<S>(ql, (const R*)nullptr, P, pl); prims_fast<S>(qr, (const R*)nullptr, P, pr); }
+        if (S::cell_ok(ql, (const R*)nullptr, pl, P) && S::cell_ok(qr, (const R*)nullptr, pr, P)) {
+          bool ok = true;
+          int code;
+          if (d == 0) {
+            code = S::template probe_fast<1, FastMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
+            if (!ok) code = S::template probe_fast<1, IeeeMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
+          } else {
+            code = S::template probe_fast<2, FastMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
+            if (!ok) code = S::template probe_fast<2, IeeeMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
+          }
+          if (code) sm = (R)0;
+        }
+        ds->tnext[A.cur ^ 1][d] = Bits<R>::to(sm);
+      }
+    }
+  }
 
   // ---- last CTA commits the step.  The fence only orders this CTA's
   // error-key atomics (CHECKS) before its count; the state stores need none
@@ -1471,6 +2083,12 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     const int prev = atomicAdd(&ds->done, 1);
     if (prev == nblk - 1) {
       __threadfence();
+      if constexpr (HasBound<S>::value && !FUSED) {
+        if (A.tmax) {
+          if (!ctl.skip && !s_hany[0]) ds->tnext[A.cur ^ 1][0] = 0ull;
+          if (!ctl.skip && !s_hany[1]) ds->tnext[A.cur ^ 1][1] = 0ull;
+        }
+      }
       commit_step<R>(ds, A, ctl, L);
     }
     if (L.trace) trace_cta(L, 1, t_start);

@@ -359,6 +359,7 @@ struct EulerHLLE {
 struct ShallowRoe {
   static constexpr int NEQ = 3, NW = 3, NAUX = 0, NPR = 3;
   static constexpr bool STATIC_SPEEDS = false;
+  static constexpr bool HAS_BOUND = true;   // bound_cell: CFL candidate filter
   // W2 = a2 (0, 0, 1): only the transverse slot
   template <int NI> __host__ __device__ static constexpr bool wzero(int w, int m) { return w == 1 && m != 3 - NI; }
   template <class R> struct Params { R grav, sqg; };
@@ -444,6 +445,51 @@ struct ShallowRoe {
     // |uh| never exceeds max(|uh-c|, |uh+c|) for c >= 0 (rounding is monotone)
     smax = nmax(fabs(uh - ch), fabs(uh + ch));
     return 0;
+  }
+
+  // CFL candidate filter (k_speeds_b).  probe_fast's max |s| is |uh| + ch up
+  // to rounding, uh is a convex combination of u_l, u_r and ch = sqrt(g (h_l
+  // + h_r) / 2) <= sqrt(g max(h_l, h_r)), so for the edge
+  //     max|s| <= (max(bx_l, bx_r) + max(bc_l, bc_r)) * MARGIN
+  // with bx = |hu| / h (by = |hv| / h) and bc = sqrt(g) sqrt(h) from the
+  // approximate seeds.  Returns false (edge must be probed exactly) unless the
+  // cell is admissible and every quantity is in the seeds' safe range.
+  template <class R, class P>
+  __device__ static __forceinline__ bool bound_cell(const R* q, const R*, const P& p, R& bx,
+                                                    R& by, R& bc) {
+    const R h = q[0];
+    const R r = BoundMath::rcp(h);
+    bx = fabs(q[1]) * r;
+    by = fabs(q[2]) * r;
+    bc = p.sqg * (h * BoundMath::rsqrt(h));
+    return BoundMath::pos_ok(h) && BoundMath::abs_ok(q[1]) && BoundMath::abs_ok(q[2]) &&
+           BoundMath::small(bx) && BoundMath::small(by) && BoundMath::small(bc);
+  }
+
+  // Tile form (k_update_w epilogue -> k_speeds_t): integer maxima of the
+  // high words over the tile's new cells, a = {max |hu|, max |hv|, max h,
+  // min h} (signed, so a negative, NaN or zero depth shows up at either end),
+  // then once per tile bx = max|hu| / min h >= every cell's |u|, by likewise,
+  // bc = sqrt(g) sqrt(max h); +inf when any cell leaves the seeds' range.
+  template <class R>
+  __device__ static __forceinline__ void tile_acc(const R* q, int (&a)[4]) {
+    const int h = BoundMath::hw(q[0]);
+    a[0] = max(a[0], BoundMath::hw(q[1]) & 0x7fffffff);
+    a[1] = max(a[1], BoundMath::hw(q[2]) & 0x7fffffff);
+    a[2] = max(a[2], h);
+    a[3] = min(a[3], h);
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_bound(const int (&a)[4], const P& p, R& bx, R& by,
+                                                    R& bc) {
+    const int lo = BoundMath::hw_lo<R>(), hi = BoundMath::hw_hi<R>();
+    const R hmin = BoundMath::lb<R>(a[3]);
+    bx = BoundMath::ub<R>(a[0]) / hmin;
+    by = BoundMath::ub<R>(a[1]) / hmin;
+    bc = p.sqg * sqrt(BoundMath::ub<R>(a[2]));
+    const bool ok = a[0] < hi && a[1] < hi && a[2] < hi && a[3] >= lo &&
+                    BoundMath::small(bx) && BoundMath::small(by) && BoundMath::small(bc);
+    if (!ok) bx = by = bc = (R)INFINITY;
   }
 };
 

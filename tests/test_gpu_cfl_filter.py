@@ -1,0 +1,149 @@
+"""The candidate-filter CFL pre-pass (k_speeds_b) against the oracle.
+
+The filter probes an edge exactly only when a cheap upper bound of its max
+|s| reaches an exact lower bound of the step's maximum (the previous step's
+argmax edge re-probed on the current state, running maxima); every other
+edge provably cannot hold the maximum.  These cases aim at its corners:
+a moving maximum (hint one step stale), all edges tied (every edge a
+candidate), a single dominant edge, admissible cells outside the bound's
+safe range (forced exact probes) and both precisions.  Bar: every dt and
+max speed identical to the oracle, state bitwise.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import device_run, oracle_run, same_bits
+
+pytestmark = pytest.mark.gpu
+
+NAME = "shallow-water-roe"
+
+
+def _dam_break(nx, ny, seed=0):
+    rng = np.random.default_rng(seed)
+    dx, dy = 2.0 / nx, 2.0 / ny
+    q = np.zeros((3, nx + 4, ny + 4), order="F")
+    x = -1 + (np.arange(nx) + 0.5) * dx
+    y = -1 + (np.arange(ny) + 0.5) * dy
+    xx, yy = np.meshgrid(x, y, indexing="ij")
+    q[0, 2:-2, 2:-2] = np.where(xx * xx + yy * yy < 0.09, 2.0, 1.0) + rng.normal(0, 1e-4, (nx, ny))
+    return q, dx, dy
+
+
+def _check(q, dx, dy, steps, *, order=2, limiter="mc", bc=("extrapolate", "extrapolate"),
+           precision="f64", use_run=False):
+    nx, ny = q.shape[1] - 4, q.shape[2] - 4
+    oq, oreps = oracle_run(NAME, q, None, nx, ny, dx, dy, steps=steps, order=order,
+                           limiter=limiter, bc_x=bc[0], bc_y=bc[1])
+    dq, res, _ = device_run(NAME, q, None, nx, ny, dx, dy, steps=steps, order=order,
+                            limiter=limiter, bc_x=bc[0], bc_y=bc[1], precision=precision,
+                            use_run=use_run)
+    assert res.error.code == 0 and res.steps_done == steps
+    for k, (r, (dt, cfl, msx, msy)) in enumerate(zip(oreps, res.reports)):
+        assert (r.dt, r.max_speed_x, r.max_speed_y) == (dt, msx, msy), f"step {k}"
+    assert same_bits(oq, dq), f"max |diff| = {np.abs(oq - dq).max():.3e}"
+
+
+def test_dam_break_moving_maximum():
+    # C2's recipe at 200x170, 30 steps: the maximum sits on the expanding front
+    q, dx, dy = _dam_break(200, 170, seed=3)
+    _check(q, dx, dy, 30)
+    _check(q, dx, dy, 30, use_run=True)
+
+
+def test_all_edges_tied():
+    # lake at rest: every edge has the same max |s| (all are candidates)
+    nx, ny = 97, 61
+    q = np.zeros((3, nx + 4, ny + 4), order="F")
+    q[0] = 1.5
+    _check(q, 1.0 / nx, 1.0 / ny, 3)
+
+
+def test_single_dominant_edge_and_periodic():
+    nx, ny = 131, 77
+    q = np.zeros((3, nx + 4, ny + 4), order="F")
+    q[0] = 1.0
+    q[0, 2 + 100, 2 + 5] = 1.3
+    q[1, 2 + 7, 2 + 70] = 0.4
+    _check(q, 1.0 / nx, 1.0 / ny, 6, bc=("periodic", "periodic"))
+    _check(q, 1.0 / nx, 1.0 / ny, 6, order=1, limiter="none")
+
+
+def test_cells_outside_the_bound_range_are_probed():
+    # admissible, but the seeds' safe range is left: h just above the 1e-300
+    # floor, and momenta whose velocity bound exceeds 2^500 -> forced exact
+    # probes; the step's maximum sits on those edges
+    nx, ny = 64, 48
+    rng = np.random.default_rng(5)
+    q = np.zeros((3, nx + 4, ny + 4), order="F")
+    q[0, 2:-2, 2:-2] = rng.uniform(1.0, 1.1, (nx, ny))
+    q[0, 2 + 10, 2 + 10] = 1.2e-300
+    q[1, 2 + 30, 2 + 20] = 1e155
+    dx, dy = 1.0 / nx, 1.0 / ny
+    oq, oreps = oracle_run(NAME, q, None, nx, ny, dx, dy, steps=1, order=1)
+    dq, res, _ = device_run(NAME, q, None, nx, ny, dx, dy, steps=1, order=1)
+    assert res.error.code == 0
+    r = oreps[0]
+    assert (r.dt, r.max_speed_x, r.max_speed_y) == tuple(res.reports[0][i] for i in (0, 2, 3))
+    assert np.array_equal(oq, dq, equal_nan=True)
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_random_states_fp32(seed):
+    q, dx, dy = _dam_break(150, 90, seed=seed)
+    q[1, 2:-2, 2:-2] = np.random.default_rng(seed).uniform(-0.5, 0.5, (150, 90))
+    q32 = np.asfortranarray(q, dtype=np.float32)
+    nx, ny = 150, 90
+    oq, oreps = oracle_run(NAME, q32, None, nx, ny, dx, dy, steps=8, order=2, limiter="mc")
+    dq, res, _ = device_run(NAME, q32, None, nx, ny, dx, dy, steps=8, order=2, limiter="mc",
+                            precision="f32")
+    assert res.error.code == 0
+    for r, (dt, cfl, msx, msy) in zip(oreps, res.reports):
+        assert (r.dt, r.max_speed_x, r.max_speed_y) == (dt, msx, msy)
+    assert same_bits(oq, dq)
+
+
+def test_reupload_invalidates_tile_data():
+    # tile maxima, hint edges and the lower bound describe the state the last
+    # update wrote; a new upload on the same handle must not reuse them
+    from helpers import device_grid
+    from paper_1308_1464_b200 import _abi
+    nx, ny = 120, 90
+    q1, dx, dy = _dam_break(nx, ny, seed=1)
+    q2 = np.zeros_like(q1)
+    q2[0] = 1.0
+    q2[0, 2 + 100, 2 + 80] = 3.0   # the only fast spot, far from q1's front
+    g = device_grid(NAME, nx, ny, dx, dy, order=2, limiter="mc")
+    try:
+        ctl = _abi.make_ctl(0.9)
+        g.upload(q1)
+        for _ in range(4):
+            g.step(ctl)
+        g.poll()
+        g.upload(q2)
+        for _ in range(4):
+            g.step(ctl)
+        res = g.poll()
+        out = g.download()
+    finally:
+        g.close()
+    oq, oreps = oracle_run(NAME, q2, None, nx, ny, dx, dy, steps=4, order=2, limiter="mc")
+    assert [(r.dt, r.max_speed_x, r.max_speed_y) for r in oreps] == \
+        [(r[0], r[2], r[3]) for r in res.reports]
+    assert same_bits(oq, out)
+
+
+def test_many_tiles_two_fronts():
+    # 900x700: 32x25 tiles, several candidate tiles far apart (two dams)
+    nx, ny = 900, 700
+    rng = np.random.default_rng(9)
+    dx, dy = 1.0 / nx, 1.0 / ny
+    q = np.zeros((3, nx + 4, ny + 4), order="F")
+    x = (np.arange(nx) + 0.5) * dx
+    y = (np.arange(ny) + 0.5) * dy
+    xx, yy = np.meshgrid(x, y, indexing="ij")
+    h = 1.0 + 0.6 * np.exp(-400 * ((xx - 0.2) ** 2 + (yy - 0.3) ** 2)) \
+        + 0.59 * np.exp(-300 * ((xx - 0.8) ** 2 + (yy - 0.7) ** 2))
+    q[0, 2:-2, 2:-2] = h + rng.normal(0, 1e-5, (nx, ny))
+    _check(q, dx, dy, 12, bc=("periodic", "extrapolate"))

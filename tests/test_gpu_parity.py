@@ -412,7 +412,8 @@ def test_driver_run_t_final_and_remaining():
     assert rep.dt == 1e-5
 
 
-@pytest.mark.parametrize("env", ["WS_PDL=0", "WS_PERSIST=0", "WS_SPEEDS=smem"])
+@pytest.mark.parametrize("env", ["WS_PDL=0", "WS_PERSIST=0", "WS_SPEEDS=smem", "WS_SPEEDS=exact",
+                                 "WS_SPEEDS=edge"])
 def test_alternative_launch_paths_bitwise(monkeypatch, env):
     # the non-default execution paths (plain launches, non-persistent 4-component
     # line kernel, shared-memory pre-pass) give the same bits

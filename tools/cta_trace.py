@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
     ap.add_argument("--flush", action="store_true")
+    ap.add_argument("--steps", type=int, default=5, help="steps before the traced one")
     a = ap.parse_args()
     os.environ["WS_TRACE"] = "1"
     import torch
@@ -30,7 +31,7 @@ def main():
     g.upload(c.q, c.aux)
     ctl = _abi.make_ctl(c.cfl)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device="cuda")
-    for _ in range(5):
+    for _ in range(a.steps):
         g.step(ctl)
     g.sync()
     if a.flush:
@@ -45,7 +46,7 @@ def main():
     assert rc == 0 and n.value > 0, "tracing off?"
     rec = np.frombuffer(buf, dtype=np.uint64, count=n.value).reshape(2, -1, 4).astype(np.int64)
     t_ref = None
-    for region, name in ((0, "k_speeds_w"), (1, "k_update_w")):
+    for region, name in ((0, "pre-pass"), (1, "k_update_w")):
         r = rec[region]
         r = r[r[:, 0] > 0]
         if t_ref is None:
