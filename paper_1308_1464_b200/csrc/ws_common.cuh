@@ -111,7 +111,6 @@ struct DevState {
   unsigned long long hint_acc[2][2];
   unsigned long long hint[2];
   int tmax_ok[2];                     // tile maxima of state buffer p written by its update
-  int pq[2][2];                       // tile pre-pass: candidate tiles listed / items taken
   unsigned long long tnext[2][2];     // exact max|s| bits of one x / y edge of state buffer p
                                       // (the update that wrote it probed its hint edges)
   Report rep[REPCAP];

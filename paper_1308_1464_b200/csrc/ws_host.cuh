@@ -200,18 +200,17 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
       if constexpr (HasBound<S>::value) {
         constexpr int LW = 29, NWT = 8;
         const int nt = ((h->L.nx + LW - 1) / LW) * ((h->L.ny + LW - 1) / LW);
-        int* list = reinterpret_cast<int*>(static_cast<char*>(h->tmax) + 2 * (size_t)nt * 16);
-        launch(h, k_tiles_decide<S, R>, dim3((nt + 255) / 256), dim3(256), 0, st,
-               static_cast<const int4*>(h->tmax), h->L, prm(h), cur, list, h->ds);
-        h->launches++;
-        // persistent item loop: every warp the GPU holds at 4 CTAs per SM
-        // (fewer for small grids: 8 items per tile)
-        const long long items = (long long)nt * TILE_NG;
-        long long ctas = (items + NWT - 1) / NWT;
-        if (ctas > 148 * 4) ctas = 148 * 4;
+        // decisions interleaved over the CTAs, at most TILE_LIST tiles each
+        long long ctas = 148 * 4;
+        if ((long long)nt > ctas * TILE_LIST) ctas = ((long long)nt + TILE_LIST - 1) / TILE_LIST;
+        // split each tile's rows over up to 4 CTAs while the decisions still
+        // take one pass of the grid's threads
+        int spl = (int)((ctas * NWT * 32) / nt);
+        spl = spl < 1 ? 1 : (spl > 4 ? 4 : spl);
+        if (ctas > (long long)nt * spl) ctas = (long long)nt * spl;
         launch(h, k_speeds_t<S, R, NWT>, dim3((unsigned)ctas), dim3(NWT * 32), 0, st,
                static_cast<const R*>(q), static_cast<const R*>(h->aux),
-               static_cast<const int*>(list), h->L, prm(h), cur, h->ds);
+               static_cast<const int4*>(h->tmax), h->L, prm(h), cur, spl, h->ds);
       }
     } else if (HasBound<S>::value && !h->speeds_exact) {
       // candidate-filter pre-pass (exact result, see k_speeds_b)

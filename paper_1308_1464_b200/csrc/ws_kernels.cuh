@@ -695,78 +695,94 @@ k_speeds_b(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
 // key).  Without valid tile data (first step after an upload, another update
 // path) every tile is a candidate.
 //
-// k_tiles_decide: one thread per tile -> candidate list (warp-aggregated
-// atomics).  k_speeds_t: persistent warps pull (tile, 4-row group) items
-// from the list, so a few candidate tiles spread over the whole GPU.
-constexpr int TILE_RPW = 1, TILE_NG = 30;  // rows per item, items per tile (30 edge rows at most)
+// One kernel: CTA c decides tiles c, c + G, c + 2G, ... (G = grid size, so a
+// cluster of candidate tiles spreads over many CTAs, i.e. SMs), one thread per
+// tile, into a shared-memory list; then its warps probe the listed tiles'
+// edge rows, one row per item.
+constexpr int TILE_NG = 30;   // edge rows of a tile (29, +1 for the top boundary row)
+constexpr int TILE_LIST = 2048;
 
 template <class S, class R>
-__global__ void __launch_bounds__(256)
-k_tiles_decide(const int4* __restrict__ tmax, const Layout L, const typename S::template Params<R> P,
-               const int cur, int* __restrict__ list, DevState* __restrict__ ds) {
-  constexpr int LW = 29;
+__device__ __forceinline__ void tile_decide(const int4* __restrict__ tm, int t, int ntx, int nty,
+                                            const Layout& L, const typename S::template Params<R>& P,
+                                            R tlx, R tly, bool& cx, bool& cy) {
   const R MARGIN = (R)BoundMath::MARGIN;
-  pdl_wait();
-  pdl_trigger();
-  const int ntx = (L.nx + LW - 1) / LW, nty = (L.ny + LW - 1) / LW;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  bool cx = false, cy = false;
-  if (t < ntx * nty && !(__ldcg(&ds->err) | __ldcg(&ds->finished))) {
-    cx = cy = true;
-    if (__ldcg(&ds->tmax_ok[cur])) {
-      const R tlx = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][0])),
-                         Bits<R>::from(__ldcg(&ds->slot[cur][0])));
-      const R tly = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][1])),
-                         Bits<R>::from(__ldcg(&ds->slot[cur][1])));
-      const int tx = t % ntx, ty = t / ntx;
-      const int4* tm = tmax + (long long)cur * ntx * nty;
-      // x-edges of a tile read its own cells and the left tile's last column
-      // (periodic: tile ntx-1 left of tile 0, tile 0 right of the last tile);
-      // y-edges likewise with the tile below / above
-      auto get = [&](int x, int y) { return __ldcg(tm + (long long)y * ntx + x); };
-      auto fold = [](int (&a)[4], const int4 v) {
-        a[0] = max(a[0], v.x); a[1] = max(a[1], v.y); a[2] = max(a[2], v.z); a[3] = min(a[3], v.w);
-      };
-      const int4 self = get(tx, ty);
-      int ax[4] = {self.x, self.y, self.z, self.w};
-      int ay[4] = {self.x, self.y, self.z, self.w};
-      const bool px = L.bcx == BC_PERIODIC, py = L.bcy == BC_PERIODIC;
-      if (tx > 0) fold(ax, get(tx - 1, ty));
-      else if (px) fold(ax, get(ntx - 1, ty));
-      if (px && tx == ntx - 1) fold(ax, get(0, ty));
-      if (ty > 0) fold(ay, get(tx, ty - 1));
-      else if (py) fold(ay, get(tx, nty - 1));
-      if (py && ty == nty - 1) fold(ay, get(tx, 0));
-      R bxx, byx, bcx, bxy, byy, bcy;
-      S::tile_bound(ax, P, bxx, byx, bcx);
-      S::tile_bound(ay, P, bxy, byy, bcy);
-      cx = !((bxx + bcx) * MARGIN < tlx);
-      cy = !((byy + bcy) * MARGIN < tly);
-    }
-  }
-  const bool cand = cx || cy;
-  const unsigned m = __ballot_sync(0xffffffffu, cand);
-  int base = 0;
-  if (lane == 0 && m) base = atomicAdd(&ds->pq[cur][0], __popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (cand) list[base + __popc(m & ((1u << lane) - 1u))] = t | (cx ? 1 << 30 : 0) | (cy ? 1 << 31 : 0);
+  const int tx = t % ntx, ty = t / ntx;
+  // x-edges of a tile read its own cells and the left tile's last column
+  // (periodic: tile ntx-1 left of tile 0, tile 0 right of the last tile);
+  // y-edges likewise with the tile below / above
+  auto get = [&](int x, int y) { return __ldcg(tm + (long long)y * ntx + x); };
+  auto fold = [](int (&a)[4], const int4 v) {
+    a[0] = max(a[0], v.x); a[1] = max(a[1], v.y); a[2] = max(a[2], v.z); a[3] = min(a[3], v.w);
+  };
+  const bool px = L.bcx == BC_PERIODIC, py = L.bcy == BC_PERIODIC;
+  const int4 self = get(tx, ty);
+  const bool hl = tx > 0 || px, hr = px && tx == ntx - 1;
+  const bool hb = ty > 0 || py, ht = py && ty == nty - 1;
+  const int4 vl = hl ? get(tx > 0 ? tx - 1 : ntx - 1, ty) : self;
+  const int4 vr = hr ? get(0, ty) : self;
+  const int4 vb = hb ? get(tx, ty > 0 ? ty - 1 : nty - 1) : self;
+  const int4 vt = ht ? get(tx, 0) : self;
+  int ax[4] = {self.x, self.y, self.z, self.w};
+  int ay[4] = {self.x, self.y, self.z, self.w};
+  fold(ax, vl); fold(ax, vr);
+  fold(ay, vb); fold(ay, vt);
+  R bxx, byx, bcx, bxy, byy, bcy;
+  S::tile_bound(ax, P, bxx, byx, bcx);
+  S::tile_bound(ay, P, bxy, byy, bcy);
+  cx = !((bxx + bcx) * MARGIN < tlx);
+  cy = !((byy + bcy) * MARGIN < tly);
 }
 
 template <class S, class R, int NWT>
 __global__ void __launch_bounds__(NWT * 32, 4)
-k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int* __restrict__ list,
-           const Layout L, const typename S::template Params<R> P, const int cur,
+k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __restrict__ tmax,
+           const Layout L, const typename S::template Params<R> P, const int cur, const int SPL,
            DevState* __restrict__ ds) {
   constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
-  constexpr int LW = 29, RPW = TILE_RPW;
-  const int lane = threadIdx.x & 31;
+  constexpr int LW = 29, NT = NWT * 32;
+  __shared__ int s_list[TILE_LIST];
+  __shared__ int s_cnt, s_ok;
+  __shared__ R s_t[2];
+  const int tid = threadIdx.x, lane = tid & 31, wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const unsigned long long t_start = L.trace ? gtimer() : 0ull;
   pdl_wait();
   pdl_trigger();
-  const int ntx = (L.nx + LW - 1) / LW;
-  const int nitems = __ldcg(&ds->pq[cur][0]) * TILE_NG;
+  const int ntx = (L.nx + LW - 1) / LW, nty = (L.ny + LW - 1) / LW, nt = ntx * nty;
+  if (tid == 0) {
+    const int fl = __ldcg(&ds->err) | __ldcg(&ds->finished);
+    const int ok = __ldcg(&ds->tmax_ok[cur]);
+    const R t0 = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][0])), Bits<R>::from(__ldcg(&ds->slot[cur][0])));
+    const R t1 = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][1])), Bits<R>::from(__ldcg(&ds->slot[cur][1])));
+    s_ok = fl ? -1 : ok;
+    s_t[0] = t0; s_t[1] = t1;
+    s_cnt = 0;
+  }
+  __syncthreads();
+  if (s_ok < 0) return;
+  {
+    const int4* tm = tmax + (long long)cur * nt;
+    const R tlx = s_t[0], tly = s_t[1];
+    // virtual index v = tile * SPL + part: the SPL parts of a tile (rows
+    // part, part + SPL, ...) land on SPL consecutive CTAs, which decide it
+    // redundantly and probe its rows in parallel
+    const long long nv = (long long)nt * SPL;
+    for (long long v = blockIdx.x + (long long)tid * gridDim.x; v < nv; v += (long long)NT * gridDim.x) {
+      const int t = (int)(v / SPL), part = (int)(v - (long long)t * SPL);
+      bool cx = true, cy = true;
+      if (s_ok) tile_decide<S, R>(tm, t, ntx, nty, L, P, tlx, tly, cx, cy);
+      if (cx || cy)
+        s_list[atomicAdd(&s_cnt, 1)] = t | (part << 28) | (cx ? 1 << 30 : 0) | (cy ? 1 << 31 : 0);
+    }
+  }
+  __syncthreads();
+  const int ngs = (TILE_NG + SPL - 1) / SPL;   // rows of one part
+  const int nitems = s_cnt * ngs;
+  if (nitems == 0) {
+    if (L.trace && tid == 0) trace_cta(L, 0, t_start);
+    return;
+  }
 
   R mx = (R)0, my = (R)0;
   unsigned long long key = ~0ull, kx = 0ull, ky = 0ull;
@@ -791,104 +807,85 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int* __rest
   using NX = std::integral_constant<int, 1>;
   using NY = std::integral_constant<int, 2>;
 
-  bool worked = false;
-  // consecutive items go to different CTAs (SMs): a few candidate tiles
-  // still spread over the whole GPU
-  const int nwarps = gridDim.x * NWT;
-  const int wg = (int)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  for (int item = wg; item < nitems; item += nwarps) {
-    worked = true;
-    const int ent = __ldcg(list + item / TILE_NG), g = item % TILE_NG;
-    const int tile = ent & ((1 << 30) - 1);
+  for (int item = wid; item < nitems; item += NWT) {
+    const int ent = s_list[item / ngs];
+    const int tile = ent & ((1 << 28) - 1);
+    const int g = ((ent >> 28) & 3) + SPL * (item % ngs);
     const bool cx = (ent & (1 << 30)) != 0, cy = ent < 0;
     const int i0 = (tile % ntx) * LW, j0 = (tile / ntx) * LW;
     // edges owned: x-edges ei in [i0, iend) on rows [j0, min(j0+29, ny));
     // y-edges ci in [i0, min(i0+29, nx)) on rows [j0, rend)
     const int iend = i0 + LW >= L.nx ? L.nx + 1 : i0 + LW;
     const int rend = j0 + LW >= L.ny ? L.ny_edges_y : j0 + LW;
+    const int r = j0 + g;
+    if (g >= TILE_NG || r >= rend) continue;
     const int ci = i0 - 1 + lane;
     const int gi = map_i(ci < L.nx ? ci : L.nx, L);
-    const bool xcol = cx && lane >= 1 && ci < iend;
-    const bool ycol = cy && lane >= 1 && ci < (i0 + LW < L.nx ? i0 + LW : L.nx);
-    const int rb = j0 + g * RPW;
-    const int nr = rend - rb < RPW ? rend - rb : RPW;
-    if (nr <= 0) continue;
-    R qb[RPW + 1][NEQ], ab[RPW + 1][NA1];
+    const bool xcol = cx && lane >= 1 && ci < iend && r < L.ny;
+    const bool ycol = cy && lane >= 1 && ci < (i0 + LW < L.nx ? i0 + LW : L.nx) && r < L.ny_edges_y;
+    R qp[NEQ], qc[NEQ], ap[NA1], ac[NA1];
+    {
+      const R* sc = q + row_off(map_j(r < L.ny ? r : L.ny, L), L) + gi;
+      const R* sp = q + row_off(map_j(r - 1, L), L) + gi;
 #pragma unroll
-    for (int k = 0; k <= RPW; ++k) {
-      if (k <= nr) {
-        const int r = rb - 1 + k;
-        const int gj = map_j(r < L.ny ? r : L.ny, L);
-        const R* src = q + row_off(gj, L) + gi;
+      for (int c = 0; c < NEQ; ++c) { qc[c] = __ldcg(sc + c * L.pitch); qp[c] = __ldcg(sp + c * L.pitch); }
+      if (NAUX > 0) {
+        const R* ac_ = aux + (long long)(map_j(r < L.ny ? r : L.ny, L) + 2) * L.astride + gi;
+        const R* ap_ = aux + (long long)(map_j(r - 1, L) + 2) * L.astride + gi;
 #pragma unroll
-        for (int c = 0; c < NEQ; ++c) qb[k][c] = __ldcg(src + c * L.pitch);
-        if (NAUX > 0) {
-          const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
-#pragma unroll
-          for (int c = 0; c < NAUX; ++c) ab[k][c] = __ldcg(asrc + c * L.pitch);
-        }
+        for (int c = 0; c < NAUX; ++c) { ac[c] = __ldcg(ac_ + c * L.pitch); ap[c] = __ldcg(ap_ + c * L.pitch); }
       }
     }
-    R pp[NP1];
-    if (NPR > 0) prims_fast<S>(qb[0], ab[0], P, pp);
-    bool okp = S::cell_ok(qb[0], ab[0], pp, P);
+    R pc[NP1];
+    if (NPR > 0) prims_fast<S>(qc, ac, P, pc);
+    const bool okc = S::cell_ok(qc, ac, pc, P);
+    if (cx) {
+      R ql[NEQ], al[NA1], pl[NP1];
 #pragma unroll
-    for (int k = 1; k <= RPW; ++k) {
-      if (k > nr) break;
-      const int r = rb - 1 + k;
-      R pc[NP1];
-      if (NPR > 0) prims_fast<S>(qb[k], ab[k], P, pc);
-      const bool okc = S::cell_ok(qb[k], ab[k], pc, P);
-      if (cx) {
-        R ql[NEQ], al[NA1], pl[NP1];
+      for (int c = 0; c < NEQ; ++c) ql[c] = __shfl_up_sync(0xffffffffu, qc[c], 1);
 #pragma unroll
-        for (int c = 0; c < NEQ; ++c) ql[c] = __shfl_up_sync(0xffffffffu, qb[k][c], 1);
+      for (int c = 0; c < NAUX; ++c) al[c] = __shfl_up_sync(0xffffffffu, ac[c], 1);
 #pragma unroll
-        for (int c = 0; c < NAUX; ++c) al[c] = __shfl_up_sync(0xffffffffu, ab[k][c], 1);
-#pragma unroll
-        for (int c = 0; c < NPR; ++c) pl[c] = __shfl_up_sync(0xffffffffu, pc[c], 1);
-        const bool okl = __shfl_up_sync(0xffffffffu, okc, 1);
-        if (xcol && r < L.ny) {
-          const R sv = probe(NX{}, ql, qb[k], pl, pc, al, ab[k], okl && okc, 0, ci, r);
-          mx = nmax(mx, sv);
-          const unsigned long long hk = hint_key(sv, (long long)r * (L.nx + 1) + ci);
-          kx = hk > kx ? hk : kx;
-        }
+      for (int c = 0; c < NPR; ++c) pl[c] = __shfl_up_sync(0xffffffffu, pc[c], 1);
+      const bool okl = __shfl_up_sync(0xffffffffu, okc, 1);
+      if (xcol) {
+        const R sv = probe(NX{}, ql, qc, pl, pc, al, ac, okl && okc, 0, ci, r);
+        mx = nmax(mx, sv);
+        const unsigned long long hk = hint_key(sv, (long long)r * (L.nx + 1) + ci);
+        kx = hk > kx ? hk : kx;
       }
-      if (ycol && r < L.ny_edges_y) {
-        const R sv = probe(NY{}, qb[k - 1], qb[k], pp, pc, ab[k - 1], ab[k], okp && okc, 1, ci, r);
-        my = nmax(my, sv);
-        const unsigned long long hk = hint_key(sv, (long long)r * L.nx + ci);
-        ky = hk > ky ? hk : ky;
-      }
-#pragma unroll
-      for (int c = 0; c < NPR; ++c) pp[c] = pc[c];
-      okp = okc;
+    }
+    if (ycol) {
+      R pp[NP1];
+      if (NPR > 0) prims_fast<S>(qp, ap, P, pp);
+      const bool okp = S::cell_ok(qp, ap, pp, P);
+      const R sv = probe(NY{}, qp, qc, pp, pc, ap, ac, okp && okc, 1, ci, r);
+      my = nmax(my, sv);
+      const unsigned long long hk = hint_key(sv, (long long)r * L.nx + ci);
+      ky = hk > ky ? hk : ky;
     }
   }
-  if (worked) {
-    // per-warp results: at most one atomic per value and warp
-    if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
-    unsigned long long bxs = Bits<R>::to(mx), bys = Bits<R>::to(my);
+  // per-warp results: at most one atomic per value and warp
+  if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
+  unsigned long long bxs = Bits<R>::to(mx), bys = Bits<R>::to(my);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      unsigned long long wx = __shfl_xor_sync(0xffffffffu, bxs, o);
-      unsigned long long wy = __shfl_xor_sync(0xffffffffu, bys, o);
-      unsigned long long hx = __shfl_xor_sync(0xffffffffu, kx, o);
-      unsigned long long hy = __shfl_xor_sync(0xffffffffu, ky, o);
-      bxs = wx > bxs ? wx : bxs;
-      bys = wy > bys ? wy : bys;
-      kx = hx > kx ? hx : kx;
-      ky = hy > ky ? hy : ky;
-    }
-    if (lane == 0) {
-      if (bxs) atomicMax(&ds->slot[cur][0], bxs);
-      if (bys) atomicMax(&ds->slot[cur][1], bys);
-      if (kx) atomicMax(&ds->hint_acc[cur][0], kx);
-      if (ky) atomicMax(&ds->hint_acc[cur][1], ky);
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long wx = __shfl_xor_sync(0xffffffffu, bxs, o);
+    unsigned long long wy = __shfl_xor_sync(0xffffffffu, bys, o);
+    unsigned long long hx = __shfl_xor_sync(0xffffffffu, kx, o);
+    unsigned long long hy = __shfl_xor_sync(0xffffffffu, ky, o);
+    bxs = wx > bxs ? wx : bxs;
+    bys = wy > bys ? wy : bys;
+    kx = hx > kx ? hx : kx;
+    ky = hy > ky ? hy : ky;
   }
-  if (L.trace && threadIdx.x == 0) trace_cta(L, 0, t_start);
+  if (lane == 0) {
+    if (bxs) atomicMax(&ds->slot[cur][0], bxs);
+    if (bys) atomicMax(&ds->slot[cur][1], bys);
+    if (kx) atomicMax(&ds->hint_acc[cur][0], kx);
+    if (ky) atomicMax(&ds->hint_acc[cur][1], ky);
+  }
+  if (L.trace && tid == 0) trace_cta(L, 0, t_start);
 }
 
 // --------------------------------------------------------------------------
@@ -927,7 +924,6 @@ __device__ __forceinline__ void commit_step(DevState* ds, const StepArgs& A, con
   v->hint_acc[A.cur][0] = 0ull; v->hint_acc[A.cur][1] = 0ull;
   // this step's slot is consumed; it is the accumulator of the step after next
   v->slot[A.cur][0] = 0ull; v->slot[A.cur][1] = 0ull; v->slot[A.cur][2] = 0ull;
-  v->pq[A.cur][0] = 0; v->pq[A.cur][1] = 0;
   __threadfence();
   v->done = 0;
 }

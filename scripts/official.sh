@@ -10,7 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 echo launch_rc=$?
 CMD="python bench.py --steps 6 --warmup 3 --no-e2e --no-cpu"
 $CMD > gpurun_out/o_plain.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_update_w|k_speeds" -s 8 -c 2 -o gpurun_out/o_prof $CMD > gpurun_out/o_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_update_w|k_speeds|k_tiles" -s 12 -c 3 -o gpurun_out/o_prof $CMD > gpurun_out/o_ncu_full.log 2>&1
 echo full_rc=$?
 ncu -i gpurun_out/o_prof.ncu-rep --page raw --csv > gpurun_out/o_raw.csv 2>/dev/null
 ncu -i gpurun_out/o_prof.ncu-rep --page details --csv > gpurun_out/o_details.csv 2>/dev/null
