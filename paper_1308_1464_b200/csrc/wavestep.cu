@@ -320,7 +320,7 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   // whole-tile CFL pre-pass (k_speeds_t): the update stores per-tile bound
   // maxima of the state it writes, the next pre-pass skips tiles that cannot
   // hold the step's maximum (WS_SPEEDS=exact|edge|smem select the others)
-  h->tile_prepass = h->ops.tile_prepass && !h->multi && h->line_kernel && !h->fused &&
+  h->tile_prepass = h->ops.tile_prepass && h->line_kernel && !h->fused &&
                     !h->speeds_exact && !h->speeds_smem && !h->speeds_edge;
   if (h->tile_prepass) {
     const size_t nt = (size_t)((d->nx + 28) / 29) * ((d->ny + 28) / 29);
@@ -711,6 +711,8 @@ int ws_set_halo_peers(ws_handle* h, void* const* lo_q, void* lo_state, int32_t n
   h->L.nds_lo = static_cast<DevState*>(lo_state);
   h->L.nds_hi = static_cast<DevState*>(hi_state);
   h->L.ny_lo = lo ? ny_lo : 0;
+  // the tile pre-pass has no device-side halo wait: the exact pre-pass runs
+  if (lo || hi) h->tile_prepass = false;
   // pushes this shard receives per step: one per neighbour side it has
   h->L.hsides = (h->L.lo == ROWS_MEMORY && lo ? 1 : 0) + (h->L.hi == ROWS_MEMORY && hi ? 1 : 0);
   return WS_OK;
@@ -730,6 +732,8 @@ int ws_set_peers(ws_handle* h, int32_t npeers, void* const* peer_states) {
   }
   h->L.peers = reinterpret_cast<DevState* const*>(h->peers_dev);
   h->L.npeers = npeers;
+  // the tile pre-pass has no device-side slot push: the exact pre-pass runs
+  if (npeers > 0) h->tile_prepass = false;
   return WS_OK;
 }
 

@@ -196,7 +196,10 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
       dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + TY - 1) / TY);
       k_speeds<S, R, SPD_TX, TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(
           static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
-    } else if (HasBound<S>::value && h->tile_prepass && part == 0) {
+    } else if (HasBound<S>::value && h->tile_prepass) {
+      // a row-strip shard's split pre-pass: part 1 (overlapping the halo
+      // exchange) is empty, part 2 (after it) probes every candidate tile
+      if (part == 1) return;
       if constexpr (HasBound<S>::value) {
         constexpr int LW = 29, NWT = 8;
         const int nt = ((h->L.nx + LW - 1) / LW) * ((h->L.ny + LW - 1) / LW);

@@ -772,6 +772,10 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
       const int t = (int)(v / SPL), part = (int)(v - (long long)t * SPL);
       bool cx = true, cy = true;
       if (s_ok) tile_decide<S, R>(tm, t, ntx, nty, L, P, tlx, tly, cx, cy);
+      // a shard's y-edges next to ghost rows in memory read a neighbour's
+      // cells, which no tile maxima here describe: always probed
+      const int ty = t / ntx;
+      if ((L.lo == ROWS_MEMORY && ty == 0) || (L.hi == ROWS_MEMORY && ty == nty - 1)) cy = true;
       if (cx || cy)
         s_list[atomicAdd(&s_cnt, 1)] = t | (part << 28) | (cx ? 1 << 30 : 0) | (cy ? 1 << 31 : 0);
     }

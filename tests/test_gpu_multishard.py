@@ -216,3 +216,25 @@ def test_shard_refuses_whole_steps_without_device_collectives():
             sh.grid.run(3, _abi.make_ctl(0.9))
     finally:
         sh.grid.close()
+
+
+@pytest.mark.parametrize("bc", ["extrapolate", "periodic"])
+def test_fake_shards_tile_prepass_skips_tiles(bc):
+    # shallow water strips large enough that most tiles are skipped by the
+    # tile pre-pass (the maximum sits on one dam's front), the boundary tile
+    # rows next to ghost rows in memory always probed
+    name, nx, ny, P, steps = "shallow-water-roe", 200, 300, 3, 8
+    dx, dy = 1 / nx, 1 / ny
+    rng = np.random.default_rng(4)
+    gq = np.zeros((3, nx + 4, ny + 4), order="F")
+    xx, yy = np.meshgrid((np.arange(nx) + 0.5) * dx, (np.arange(ny) + 0.5) * dy, indexing="ij")
+    gq[0, 2:-2, 2:-2] = np.where((xx - 0.5) ** 2 + (yy - 0.33) ** 2 < 0.01, 2.0, 1.0) \
+        + rng.normal(0, 1e-4, (nx, ny))
+    ref, oreps = oracle_run(name, gq, None, nx, ny, dx, dy, steps=steps, order=2,
+                            limiter="mc", bc_x=bc, bc_y=bc)
+    out, reps, errs, strips = fake_sharded(name, gq, None, nx, ny, dx, dy, P, steps, 2, "mc", bc)
+    for r in range(P):
+        j0, j1 = strips.bounds(r)
+        assert errs[r].code == 0
+        assert reps[r] == [o.dt for o in oreps]
+        assert np.array_equal(out[r], ref[:, 2:-2, 2 + j0:2 + j1]), f"shard {r}"
