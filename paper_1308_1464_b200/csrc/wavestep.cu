@@ -281,8 +281,12 @@ int ws_create(const ws_desc* d, ws_handle** out) {
       (e = get(d->ext_aux, ab, &h->aux, &h->own_aux)) != cudaSuccess ||
       (e = get(d->ext_slots, sb, &dsp, &h->own_ds)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&h->ev_order, cudaEventDisableTiming)) != cudaSuccess ||
-      (e = cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev_in[0], cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev_in[1], cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev_copy[0], cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev_copy[1], cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming)) != cudaSuccess) {
     ws_destroy(h);
     return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
@@ -361,15 +365,19 @@ void ws_destroy(ws_handle* h) {
   for (int k = 0; k < 2; ++k) if (h->own_q[k] && h->q[k]) cudaFree(h->q[k]);
   if (h->own_aux && h->aux) cudaFree(h->aux);
   if (h->own_ds && h->ds) cudaFree(h->ds);
-  if (h->stage) cudaFree(h->stage);
+  for (int k = 0; k < 2; ++k) if (h->stage[k]) cudaFree(h->stage[k]);
   if (h->stage_out) cudaFree(h->stage_out);
   if (h->peers_dev) cudaFree(h->peers_dev);
   if (h->ev_order) cudaEventDestroy(h->ev_order);
-  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  for (int k = 0; k < 2; ++k) {
+    if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
+    if (h->ev_copy[k]) cudaEventDestroy(h->ev_copy[k]);
+  }
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->borders) cudaFree(h->borders);
   if (h->tmax) cudaFree(h->tmax);
   if (h->trace) cudaFree(h->trace);
+  if (h->cstream) { cudaStreamSynchronize(h->cstream); cudaStreamDestroy(h->cstream); }
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -386,8 +394,8 @@ static int ensure_buf(ws_handle* h, void** buf, size_t* have, size_t bytes) {
   return WS_OK;
 }
 
-static int ensure_stage(ws_handle* h, size_t bytes) {
-  return ensure_buf(h, &h->stage, &h->stage_bytes, bytes);
+static int ensure_stage(ws_handle* h, int b, size_t bytes) {
+  return ensure_buf(h, &h->stage[b], &h->stage_bytes[b], bytes);
 }
 
 static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz, void* s) {
@@ -396,22 +404,27 @@ static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz
   if (h->naux > 0 && !ah) return fail(h, WS_ERR_CONFIG, "this solver needs aux data");
   const size_t cells = (size_t)(h->d.nx + 4) * (h->d.ny + 4);
   int ncmax = h->neq > h->naux ? h->neq : h->naux;
-  int rc = ensure_stage(h, cells * ncmax * h->esz);
+  // Two staging buffers, alternating, filled on the handle's copy stream: the
+  // H2D of this upload waits only for the conversion of the upload before
+  // the previous one, so it overlaps a step and a download still in flight
+  // (PCIe is full duplex).  The conversion into the state runs on the
+  // caller's stream after everything issued before (pick) and after the H2D.
+  const int b = h->up_idx;
+  h->up_idx ^= 1;
+  int rc = ensure_stage(h, b, cells * ncmax * h->esz);
   if (rc) return rc;
-  // The H2D copy only needs the upload staging buffer free (the previous
-  // upload's conversion done), so it is issued BEFORE the handle's
-  // issue-order wait: it overlaps a download still in flight on another
-  // stream.  The conversion into the state then waits for everything before.
-  cudaStream_t st0 = s ? reinterpret_cast<cudaStream_t>(s) : h->stream;
-  WS_CUDA(h, cudaStreamWaitEvent(st0, h->ev_in, 0));
-  WS_CUDA(h, cudaMemcpyAsync(h->stage, qh, cells * h->neq * h->esz, cudaMemcpyHostToDevice, st0));
+  WS_CUDA(h, cudaStreamWaitEvent(h->cstream, h->ev_in[b], 0));
+  WS_CUDA(h, cudaMemcpyAsync(h->stage[b], qh, cells * h->neq * h->esz, cudaMemcpyHostToDevice,
+                             h->cstream));
+  WS_CUDA(h, cudaEventRecord(h->ev_copy[b], h->cstream));
   cudaStream_t st = pick(h, s);
-  h->ops.to_soa(h, h->stage, h->q[0], h->neq, st);
+  WS_CUDA(h, cudaStreamWaitEvent(st, h->ev_copy[b], 0));
+  h->ops.to_soa(h, h->stage[b], h->q[0], h->neq, st);
   if (h->naux > 0) {
-    WS_CUDA(h, cudaMemcpyAsync(h->stage, ah, cells * h->naux * h->esz, cudaMemcpyHostToDevice, st));
-    h->ops.to_soa(h, h->stage, h->aux, h->naux, st);
+    WS_CUDA(h, cudaMemcpyAsync(h->stage[b], ah, cells * h->naux * h->esz, cudaMemcpyHostToDevice, st));
+    h->ops.to_soa(h, h->stage[b], h->aux, h->naux, st);
   }
-  WS_CUDA(h, cudaEventRecord(h->ev_in, st));
+  WS_CUDA(h, cudaEventRecord(h->ev_in[b], st));
   WS_CUDA(h, cudaMemsetAsync(h->ds, 0, offsetof(DevState, rep), st));
   WS_CUDA(h, cudaMemsetAsync(h->borders, 0, h->border_bytes, st));
   h->need_prepass = true;

@@ -57,15 +57,18 @@ struct ws_handle {
   void* aux = nullptr;
   DevState* ds = nullptr;
   bool own_q[2] = {false, false}, own_aux = false, own_ds = false;
-  void* stage = nullptr;         // upload staging (host layout)
-  size_t stage_bytes = 0;
+  void* stage[2] = {nullptr, nullptr};   // upload staging (host layout), alternating
+  size_t stage_bytes[2] = {0, 0};
+  int up_idx = 0;                        // staging buffer of the next upload
   void* stage_out = nullptr;     // download staging: a download and the next upload overlap
   size_t stage_out_bytes = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t cstream = nullptr;  // upload H2D copies (staging only)
   cudaStream_t last_stream = nullptr;
   cudaEvent_t ev_order = nullptr;  // issue-order hand-off between streams (pick)
   bool order_recorded = false;     // ev_order already marks the last ordering point
-  cudaEvent_t ev_in = nullptr;     // upload staging consumed (next upload's H2D may start)
+  cudaEvent_t ev_in[2] = {nullptr, nullptr};    // staging b consumed (its next H2D may start)
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr};  // staging b filled by its H2D
   cudaEvent_t ev_out = nullptr;    // download staging copied out (next download may refill it)
   long long enq = 0;            // steps enqueued since upload (== committed after a poll)
   long long nrep_seen = 0;

@@ -1,0 +1,12 @@
+timeout 600 python -m pytest tests -m gpu -q -k "fp32 or f32" > gpurun_out/pytest_f32.log 2>&1; echo rc=$?
+timeout 600 python bench.py --config c5 --precision f32 --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/exp3_c5f32.json 2>&1
+timeout 600 python bench.py --config c5 --size 8192 --precision f32 --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/exp3_c5f32_8k.json 2>&1
+timeout 600 python bench.py --config c2 --precision f32 --steps 50 --warmup 5 --no-e2e --no-cpu > gpurun_out/exp3_c2f32.json 2>&1
+tail -n 2 gpurun_out/pytest_f32.log
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob("gpurun_out/exp3_*.json")):
+    try:
+        d=json.loads(open(f).read().strip().splitlines()[-1]); print(f, round(d["value"]/1e9,3), d["ms_per_step"], d["roofline"].get("kernel_ms"), d["roofline"].get("speeds_kernel_ms"))
+    except Exception as e: print(f, "ERR", open(f).read()[-500:])
+PY
