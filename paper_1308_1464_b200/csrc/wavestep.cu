@@ -328,8 +328,8 @@ int ws_create(const ws_desc* d, ws_handle** out) {
                     !h->speeds_exact && !h->speeds_smem && !h->speeds_edge;
   if (h->tile_prepass) {
     const size_t nt = (size_t)((d->nx + 28) / 29) * ((d->ny + 28) / 29);
-    // [2][nt] int4 tile accumulators (S::tile_acc), one set per state buffer
-    if ((e = cudaMalloc(&h->tmax, 2 * nt * 16)) != cudaSuccess) {
+    // [2][nt][nacc] int tile accumulators (S::tile_acc), one set per state buffer
+    if ((e = cudaMalloc(&h->tmax, 2 * nt * 4 * (size_t)h->ops.nacc)) != cudaSuccess) {
       ws_destroy(h);
       return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
     }

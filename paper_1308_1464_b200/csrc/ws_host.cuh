@@ -42,7 +42,8 @@ struct Ops {
   void (*prepare)();   // one-time kernel attributes (never inside a capture)
   int static_speeds;   // solver has q-independent speeds
   int can_fuse_line;   // warp-line kernel has the fused next-step CFL epilogue
-  int tile_prepass;    // solver has a bound (S::HAS_BOUND) and a non-persistent line kernel
+  int tile_prepass;    // solver has tile accumulators (S::HAS_TILE)
+  int nacc;            // ints per tile of those accumulators
 };
 
 }  // namespace wsh
@@ -199,11 +200,11 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
       dim3 grid((h->L.nx + 1 + SPD_TX - 1) / SPD_TX, (h->L.ny + 1 + TY - 1) / TY);
       k_speeds<S, R, SPD_TX, TY, SPD_NT><<<grid, SPD_NT, 0, st>>>(
           static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, h->ds);
-    } else if (HasBound<S>::value && h->tile_prepass) {
+    } else if (HasTile<S>::value && h->tile_prepass) {
       // a row-strip shard's split pre-pass: part 1 (overlapping the halo
       // exchange) is empty, part 2 (after it) probes every candidate tile
       if (part == 1) return;
-      if constexpr (HasBound<S>::value) {
+      if constexpr (HasTile<S>::value) {
         constexpr int LW = 29, NWT = 8;
         const int nt = ((h->L.nx + LW - 1) / LW) * ((h->L.ny + LW - 1) / LW);
         // decisions interleaved over the CTAs, at most TILE_LIST tiles each
@@ -357,7 +358,8 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     o.prepare = &prepare;
     o.static_speeds = S::STATIC_SPEEDS ? 1 : 0;
     o.can_fuse_line = CAN_FUSE ? 1 : 0;
-    o.tile_prepass = (HasBound<S>::value && !PERSIST_W) ? 1 : 0;
+    o.tile_prepass = HasTile<S>::value ? 1 : 0;
+    o.nacc = NAcc<S>::value;
     return o;
   }
 };

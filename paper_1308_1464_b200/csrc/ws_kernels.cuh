@@ -406,6 +406,17 @@ template <int N> __device__ __forceinline__ void cp_wait() {
 // maximum of this step, and each lane's own running maximum.
 template <class S, class = void> struct HasBound : std::false_type {};
 template <class S> struct HasBound<S, std::enable_if_t<S::HAS_BOUND>> : std::true_type {};
+// tile accumulators for the tile-filtered pre-pass (S::tile_acc / tile_bound)
+template <class S, class = void> struct HasTile : std::false_type {};
+template <class S> struct HasTile<S, std::enable_if_t<S::HAS_TILE>> : std::true_type {};
+template <class S, class = void> struct NAcc { static constexpr int value = 4; };
+template <class S> struct NAcc<S, std::enable_if_t<S::HAS_TILE>> {
+  static constexpr int value = S::NACC;
+};
+template <class S, class = void> struct AccMin { static constexpr unsigned value = 0u; };
+template <class S> struct AccMin<S, std::enable_if_t<S::HAS_TILE>> {
+  static constexpr unsigned value = S::ACC_MIN;
+};
 
 constexpr unsigned long long HINT_IDX_MASK = (1ull << 29) - 1;
 template <class R>
@@ -706,36 +717,43 @@ template <class S, class R>
 __device__ __forceinline__ void tile_decide(const int4* __restrict__ tm, int t, int ntx, int nty,
                                             const Layout& L, const typename S::template Params<R>& P,
                                             R tlx, R tly, bool& cx, bool& cy) {
+  constexpr int NA = NAcc<S>::value, NV = NA / 4;
+  constexpr unsigned MINS = AccMin<S>::value;
   const R MARGIN = (R)BoundMath::MARGIN;
   const int tx = t % ntx, ty = t / ntx;
   // x-edges of a tile read its own cells and the left tile's last column
   // (periodic: tile ntx-1 left of tile 0, tile 0 right of the last tile);
   // y-edges likewise with the tile below / above
-  auto get = [&](int x, int y) { return __ldcg(tm + (long long)y * ntx + x); };
-  auto fold = [](int (&a)[4], const int4 v) {
-    a[0] = max(a[0], v.x); a[1] = max(a[1], v.y); a[2] = max(a[2], v.z); a[3] = min(a[3], v.w);
-  };
   const bool px = L.bcx == BC_PERIODIC, py = L.bcy == BC_PERIODIC;
-  const int4 self = get(tx, ty);
-  const bool hl = tx > 0 || px, hr = px && tx == ntx - 1;
-  const bool hb = ty > 0 || py, ht = py && ty == nty - 1;
-  const int4 vl = hl ? get(tx > 0 ? tx - 1 : ntx - 1, ty) : self;
-  const int4 vr = hr ? get(0, ty) : self;
-  const int4 vb = hb ? get(tx, ty > 0 ? ty - 1 : nty - 1) : self;
-  const int4 vt = ht ? get(tx, 0) : self;
-  int ax[4] = {self.x, self.y, self.z, self.w};
-  int ay[4] = {self.x, self.y, self.z, self.w};
-  fold(ax, vl); fold(ax, vr);
-  fold(ay, vb); fold(ay, vt);
-  R bxx, byx, bcx, bxy, byy, bcy;
-  S::tile_bound(ax, P, bxx, byx, bcx);
-  S::tile_bound(ay, P, bxy, byy, bcy);
-  cx = !((bxx + bcx) * MARGIN < tlx);
-  cy = !((byy + bcy) * MARGIN < tly);
+  auto fold = [&](int (&a)[NA], int x, int y) {
+    const int4* e = tm + ((long long)y * ntx + x) * NV;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int4 w = __ldcg(e + k);
+      const int v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        a[4 * k + m] = ((MINS >> (4 * k + m)) & 1u) ? min(a[4 * k + m], v[m]) : max(a[4 * k + m], v[m]);
+    }
+  };
+  int ax[NA], ay[NA];
+  S::acc_init(ax);
+  fold(ax, tx, ty);
+#pragma unroll
+  for (int k = 0; k < NA; ++k) ay[k] = ax[k];
+  if (tx > 0 || px) fold(ax, tx > 0 ? tx - 1 : ntx - 1, ty);
+  if (px && tx == ntx - 1) fold(ax, 0, ty);
+  if (ty > 0 || py) fold(ay, tx, ty > 0 ? ty - 1 : nty - 1);
+  if (py && ty == nty - 1) fold(ay, tx, 0);
+  R bx, by, dx_, dy_;
+  S::tile_bound(ax, P, bx, dy_);
+  S::tile_bound(ay, P, dx_, by);
+  cx = !(bx * MARGIN < tlx);
+  cy = !(by * MARGIN < tly);
 }
 
 template <class S, class R, int NWT>
-__global__ void __launch_bounds__(NWT * 32, 4)
+__global__ void __launch_bounds__(NWT * 32, (S::NEQ >= 4 ? 2 : 4))
 k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __restrict__ tmax,
            const Layout L, const typename S::template Params<R> P, const int cur, const int SPL,
            DevState* __restrict__ ds) {
@@ -762,7 +780,7 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
   __syncthreads();
   if (s_ok < 0) return;
   {
-    const int4* tm = tmax + (long long)cur * nt;
+    const int4* tm = tmax + (long long)cur * nt * (NAcc<S>::value / 4);
     const R tlx = s_t[0], tly = s_t[1];
     // virtual index v = tile * SPL + part: the SPL parts of a tile (rows
     // part, part + SPL, ...) land on SPL consecutive CTAs, which decide it
@@ -1506,12 +1524,12 @@ k_border(const R* __restrict__ q, const Layout L, const typename S::template Par
 // Which tile probes the next pre-pass's lower-bound edges (k_speeds_t): the
 // hint edge of each direction (where this step's maximum was found), moved
 // by at most one cell so that both of its cells are interior and lie in one
-// 29x29 tile.  pos[d] = offset of the lower / left cell in that tile (-1: not
-// this tile), any[d] = some tile owns it.
-__device__ __forceinline__ void hint_owner(unsigned long long hk, const Layout& L, int i0, int j0,
-                                           int d, int& pos, int& any) {
+// 29x29 tile.  own = that tile's index (-1: none), off = offset of the lower
+// / left cell in it.
+__device__ __forceinline__ void hint_owner(unsigned long long hk, const Layout& L, int d,
+                                           int& own, int& off) {
   constexpr int LW = 29;
-  pos = -1; any = 0;
+  own = -1; off = 0;
   if (hk == 0ull) return;
   const unsigned idx = (unsigned)(hk & HINT_IDX_MASK);
   const unsigned w = d == 0 ? (unsigned)L.nx + 1u : (unsigned)L.nx;
@@ -1528,8 +1546,8 @@ __device__ __forceinline__ void hint_owner(unsigned long long hk, const Layout& 
     if (cj % LW == LW - 1) cj -= 1;
     ci = hi;
   }
-  any = 1;
-  if (ci / LW == i0 / LW && cj / LW == j0 / LW) pos = (cj - j0) * LW + (ci - i0);
+  own = (cj / LW) * ((L.nx + LW - 1) / LW) + ci / LW;
+  off = (cj % LW) * LW + ci % LW;
 }
 
 // one edge per lane of a grid line (see k_update_w): solve, optional
@@ -1677,11 +1695,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   // handed over at the post-staging barrier
   __shared__ Ctl s_ctl;
   __shared__ R s_dtd[2];
-  __shared__ int s_hany[2], s_hpos[2];  // TMAX: hint edge owned by some tile / offset here (-1)
-  __shared__ int s_acc[4];              // TMAX: S::tile_acc of the tile (shared-memory atomics)
-  if (HasBound<S>::value && !PERSIST && !FUSED && tid == 0) {
-    s_acc[0] = 0; s_acc[1] = 0; s_acc[2] = INT_MIN; s_acc[3] = INT_MAX;
-  }
+  __shared__ int s_hown[2], s_hoff[2];  // TMAX: tile holding the hint edge (-1: none), offset
+  __shared__ int s_acc[NAcc<S>::value][NWARP];  // TMAX: per-warp S::tile_acc of the tile
   // PERSIST (one CTA per SM, 4-component fp64): CTAs walk the tiles and
   // prefetch the next tile's raw state with cp.async while the current tile
   // computes; otherwise one tile per CTA (blockIdx)
@@ -1732,11 +1747,58 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       s_dtd[1] = (R)(c0.dt / A.dy);
     }
   }
+  // TMAX (tile pre-pass): after the tile's warps reduced into s_acc and the
+  // new tile sits in sX: store the tile accumulators, probe the hint edges
+  // if this tile holds them (the next pre-pass's exact lower bound), reset
+  // s_acc.  Runs after a barrier that follows the tile's store loop.
+  int t_prev = -1;
+  auto finish_tile = [&](int tt) {
+    if constexpr (HasTile<S>::value) {
+    constexpr int NA = NAcc<S>::value;
+    constexpr unsigned MINS = AccMin<S>::value;
+    if (tid < NA) {
+      // lane k of warp 0 folds slot k over the warps and stores it
+      const bool mn = (MINS >> tid) & 1u;
+      int v = s_acc[tid][0];
+#pragma unroll
+      for (int w = 1; w < NWARP; ++w) v = mn ? min(v, s_acc[tid][w]) : max(v, s_acc[tid][w]);
+      static_cast<int*>(A.tmax)[((long long)(A.cur ^ 1) * ntiles + tt) * NA + tid] = v;
+    }
+    if (tid == 0 || tid == 32) {
+      const int d = tid >> 5;
+      const int o = s_hown[d] == tt ? s_hoff[d] : -1;
+      if (o >= 0) {
+        R ql[NEQ], qr[NEQ], pl[NP1], pr[NP1];
+        const int o2 = d == 0 ? o + 1 : o + LW;
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) { ql[m] = sX[m * (LW * LW) + o]; qr[m] = sX[m * (LW * LW) + o2]; }
+        R sm = (R)0;
+        if (NPR > 0) { prims_fast<S>(ql, (const R*)nullptr, P, pl); prims_fast<S>(qr, (const R*)nullptr, P, pr); }
+        if (S::cell_ok(ql, (const R*)nullptr, pl, P) && S::cell_ok(qr, (const R*)nullptr, pr, P)) {
+          bool ok = true;
+          int code;
+          if (d == 0) {
+            code = S::template probe_fast<1, FastMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
+            if (!ok) code = S::template probe_fast<1, IeeeMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
+          } else {
+            code = S::template probe_fast<2, FastMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
+            if (!ok) code = S::template probe_fast<2, IeeeMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
+          }
+          if (code) sm = (R)0;
+        }
+        ds->tnext[A.cur ^ 1][d] = Bits<R>::to(sm);
+      }
+    }
+    }
+  };
   for (;;) {
   if (PERSIST) {
     if (t >= ntiles) break;
     cp_wait<0>();
     __syncthreads();   // raw tile landed for every thread; previous tile fully stored
+    if constexpr (HasTile<S>::value && !FUSED) {
+      if (A.tmax && t_prev >= 0) finish_tile(t_prev);
+    }
 #pragma unroll 4
     for (int idx = tid; idx < HC; idx += NT) {
       R qc[NEQ], ac[NA1], pc[NP1];
@@ -1819,11 +1881,12 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 
     const bool cell_lane = lane >= 1 && lane <= LW;
 
-    // TMAX: the last warp walks one row fewer in the x pass; it fetches and
-    // decodes this step's hint edges (the pre-pass has completed: the
-    // step-control thread waited for it before the barrier above)
-    unsigned long long hk0 = 0ull, hk1 = 0ull;
-    const bool hwarp = HasBound<S>::value && !PERSIST && !FUSED && A.tmax != nullptr &&
+    // TMAX: the last warp walks one row fewer in the x pass; during a CTA's
+    // first tile it fetches and decodes this step's hint edges (the pre-pass
+    // has completed: the step-control thread waited for it before the
+    // barrier above)
+    unsigned long long hk0 = 0ull;
+    const bool hwarp = HasTile<S>::value && !FUSED && A.tmax != nullptr && t_prev < 0 &&
                        warp == NWARP - 1 && lane < 2;
     if (hwarp) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
     // ---- x pass: warps walk rows; lane l = x-edge i0-1+l
@@ -1847,9 +1910,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       }
     }
     if (hwarp) {
-      int o, anyd;
-      hint_owner(hk0, L, i0, j0, lane, o, anyd);
-      s_hpos[lane] = o; s_hany[lane] = anyd;
+      int own, off;
+      hint_owner(hk0, L, lane, own, off);
+      s_hown[lane] = own; s_hoff[lane] = off;
     }
     __syncthreads();
 
@@ -1966,7 +2029,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       }
     }
 
-    int tb[4] = {0, 0, INT_MIN, INT_MAX};   // TMAX: this thread's S::tile_acc accumulator
+    int tb[NAcc<S>::value];   // TMAX: this thread's S::tile_acc accumulator
+    if constexpr (HasTile<S>::value) S::acc_init(tb);
     // ---- row-coalesced store of the tile; the strip's two first / last rows
     // also go straight into the low / high neighbour's ghost rows (P2P
     // stores into its buffer of the same parity) when halos are pushed
@@ -1978,14 +2042,14 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         R* dst = qn + row_off(gj, L) + gi;
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = sX[m * (LW * LW) + idx];
-        if constexpr (HasBound<S>::value && !PERSIST && !FUSED) {
+        if constexpr (HasTile<S>::value && !FUSED) {
           // tile-bound ingredients of the new cell for the next pre-pass
-          // (k_speeds_t): integer maxima, no FP64 work
+          // (k_speeds_t)
           if (A.tmax) {
             R qv[NEQ];
 #pragma unroll
             for (int m = 0; m < NEQ; ++m) qv[m] = sX[m * (LW * LW) + idx];
-            S::tile_acc(qv, tb);
+            S::tile_acc(qv, P, tb);
           }
         }
         if (L.nds_lo && gj < 2) {
@@ -2000,13 +2064,14 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         }
       }
     }
-    if constexpr (HasBound<S>::value && !PERSIST && !FUSED) {
+    if constexpr (HasTile<S>::value && !FUSED) {
       if (A.tmax) {
-        const int r0 = __reduce_max_sync(FULL, tb[0]), r1 = __reduce_max_sync(FULL, tb[1]);
-        const int r2 = __reduce_max_sync(FULL, tb[2]), r3 = __reduce_min_sync(FULL, tb[3]);
-        if (lane == 0) {
-          atomicMax(&s_acc[0], r0); atomicMax(&s_acc[1], r1);
-          atomicMax(&s_acc[2], r2); atomicMin(&s_acc[3], r3);
+        constexpr unsigned MINS = AccMin<S>::value;
+#pragma unroll
+        for (int k = 0; k < NAcc<S>::value; ++k) {
+          const bool mn = (MINS >> k) & 1u;
+          const int r = mn ? __reduce_min_sync(FULL, tb[k]) : __reduce_max_sync(FULL, tb[k]);
+          if (lane == 0) s_acc[k][warp] = r;
         }
       }
     }
@@ -2032,6 +2097,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
     if (CHECKS && key != ~0ull) atomicMax(&ds->slot[A.cur][2], NKEY_MAX - key);
   }
+  t_prev = t;
   if (!PERSIST) break;
   t += gridDim.x;
   tile_origin(t, i0, j0);
@@ -2039,38 +2105,10 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   if (PERSIST) cp_wait<0>();   // no copy outstanding at exit
   __syncthreads();
   ctl = s_ctl;
-  if constexpr (HasBound<S>::value && !PERSIST && !FUSED) {
-    if (A.tmax && tid == 0 && !ctl.skip)
-      static_cast<int4*>(A.tmax)[(long long)(A.cur ^ 1) * ntiles + t] =
-          make_int4(s_acc[0], s_acc[1], s_acc[2], s_acc[3]);
-    // the hint edges on the new state, probed by the tile that holds both
-    // cells (sX is the stored new tile): the next pre-pass's exact lower bound
-    if (A.tmax && !ctl.skip && (tid == 0 || tid == 32)) {
-      const int d = tid >> 5;
-      const int o = s_hpos[d];
-      if (o >= 0) {
-        R ql[NEQ], qr[NEQ], pl[NP1], pr[NP1];
-        const int o2 = d == 0 ? o + 1 : o + LW;
-#pragma unroll
-        for (int m = 0; m < NEQ; ++m) { ql[m] = sX[m * (LW * LW) + o]; qr[m] = sX[m * (LW * LW) + o2]; }
-        R sm = (R)0;
-        if (NPR > 0) { prims_fast<S>(ql, (const R*)nullptr, P, pl); prims_fast<S>(qr, (const R*)nullptr, P, pr); }
-        if (S::cell_ok(ql, (const R*)nullptr, pl, P) && S::cell_ok(qr, (const R*)nullptr, pr, P)) {
-          bool ok = true;
-          int code;
-          if (d == 0) {
-            code = S::template probe_fast<1, FastMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
-            if (!ok) code = S::template probe_fast<1, IeeeMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
-          } else {
-            code = S::template probe_fast<2, FastMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
-            if (!ok) code = S::template probe_fast<2, IeeeMath>(ql, qr, pl, pr, (const R*)nullptr, (const R*)nullptr, P, sm, ok);
-          }
-          if (code) sm = (R)0;
-        }
-        ds->tnext[A.cur ^ 1][d] = Bits<R>::to(sm);
-      }
-    }
+  if constexpr (HasTile<S>::value && !FUSED) {
+    if (A.tmax && !ctl.skip && t_prev >= 0) finish_tile(t_prev);
   }
+
 
   // ---- last CTA commits the step.  The fence only orders this CTA's
   // error-key atomics (CHECKS) before its count; the state stores need none
@@ -2085,8 +2123,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       __threadfence();
       if constexpr (HasBound<S>::value && !FUSED) {
         if (A.tmax) {
-          if (!ctl.skip && !s_hany[0]) ds->tnext[A.cur ^ 1][0] = 0ull;
-          if (!ctl.skip && !s_hany[1]) ds->tnext[A.cur ^ 1][1] = 0ull;
+          if (!ctl.skip && s_hown[0] < 0) ds->tnext[A.cur ^ 1][0] = 0ull;
+          if (!ctl.skip && s_hown[1] < 0) ds->tnext[A.cur ^ 1][1] = 0ull;
         }
       }
       commit_step<R>(ds, A, ctl, L);

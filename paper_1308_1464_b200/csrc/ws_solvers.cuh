@@ -19,6 +19,7 @@
 // the translation unit is compiled with --fmad=false, IEEE div/sqrt, so
 // fp64 results are bitwise identical to numpy.
 #pragma once
+#include <climits>
 #include "ws_common.cuh"
 #include "ws_math.cuh"
 
@@ -178,10 +179,98 @@ __device__ __forceinline__ void gas_prims(const R* q, const P& p, R* pr, bool& o
   pr[0] = u; pr[1] = v; pr[2] = pp; pr[3] = sq; pr[4] = M::div(sq * (q[3] + pp), rho, ok);
 }
 
+// ---------------------------------------------------------------------------
+// Tile accumulators of the ideal-gas solvers (k_update_w epilogue ->
+// k_speeds_t).  Per new cell, from the approximate reciprocal seed of rho:
+// u, v and c^2 = gamma (gamma-1) (E - |m|^2 / (2 rho)) / rho, plus a "safe"
+// flag: finite, rho and E inside the seeds' range, internal energy at least
+// KAPPA E (Mach ~< 40 in fp64, ~< 6 in fp32), so the approximations are
+// accurate to 2^-8 and the exact path can neither find p <= floor nor lose
+// Roe's c^2 > 0 to rounding.  Accumulators (sortable integer keys of the high
+// words): max u, min u, max v, min v, max c^2, min c^2, min safe.
+// Bound: with w the Roe weight, c_hat^2 = w c_l^2 + (1-w) c_r^2 + (gamma-1)/2
+// w (1-w) |u_l - u_r|^2 <= max c^2 + (gamma-1)/8 |du|^2, and |u_hat| <= max
+// |u|, so every HLLE / Roe edge speed of the folded tiles is at most
+// max|u_n| + sqrt(max c^2 + (gamma-1)/8 (du^2 + dv^2)).
+struct GasTile {
+  static constexpr int NACC = 8;
+  static constexpr unsigned ACC_MIN = 0x6Au;   // slots 1, 3, 5, 6
+  __device__ static __forceinline__ int skey(int w) { return w ^ ((w >> 31) & 0x7fffffff); }
+  template <class R> __device__ static __forceinline__ R ub_s(int k) {
+    const int w = skey(k);
+    return k >= 0 ? BoundMath::ub<R>(w) : BoundMath::lb<R>(w);
+  }
+  template <class R> __device__ static __forceinline__ R lb_s(int k) {
+    const int w = skey(k);
+    return k >= 0 ? BoundMath::lb<R>(w) : BoundMath::ub<R>(w);
+  }
+  __device__ static __forceinline__ void acc_init(int (&a)[NACC]) {
+    a[0] = INT_MIN; a[1] = INT_MAX; a[2] = INT_MIN; a[3] = INT_MAX;
+    a[4] = INT_MIN; a[5] = INT_MAX; a[6] = INT_MAX; a[7] = 0;
+  }
+  // gg2 = gamma (gamma-1) / 2: c^2 ~ gg2 (2E - m.u) / rho.  Bound-only
+  // arithmetic (explicit FMAs; the parity-relevant code has none).
+  template <class R>
+  __device__ static __forceinline__ void acc(const R* q, R gg2, int (&a)[NACC]) {
+    // internal energy >= KAPPA E as an exponent test: 2E - m.u >= 2^-KB (2E)
+    constexpr int KB = sizeof(R) == 8 ? 9 : 3;
+    constexpr int ESH = sizeof(R) == 8 ? 20 : 23;
+    const int elo = sizeof(R) == 8 ? 0x07B00000 : 0x21800000;
+    const R rho = q[0], mx = q[1], my = q[2], E = q[3];
+    const R r = BoundMath::rcp(rho);
+    const R u = mx * r, v = my * r;
+    const R ei2 = fma((R)2, E, -fma(mx, u, my * v));   // 2 x internal energy density
+    const R c2 = gg2 * ei2 * r;
+    const int he = BoundMath::hw(E), hi2 = BoundMath::hw(ei2);
+    const bool safe = BoundMath::pos_ok(rho) && BoundMath::abs_ok(mx) && BoundMath::abs_ok(my) &&
+                      he >= elo && he < BoundMath::hw_hi<R>() &&
+                      hi2 >= he - (KB << ESH) && hi2 > 0 &&
+                      BoundMath::small(fabs(u)) && BoundMath::small(fabs(v)) && BoundMath::small(c2);
+    const int ku = skey(BoundMath::hw(u)), kv = skey(BoundMath::hw(v));
+    const int kc = BoundMath::hw(c2);
+    a[0] = max(a[0], ku); a[1] = min(a[1], ku);
+    a[2] = max(a[2], kv); a[3] = min(a[3], kv);
+    a[4] = max(a[4], kc); a[5] = min(a[5], kc);
+    a[6] = min(a[6], safe ? 1 : 0);
+  }
+  template <class R>
+  __device__ static __forceinline__ void bound(const int (&a)[NACC], R gm1, R& bndx, R& bndy) {
+    bndx = bndy = (R)INFINITY;
+    if (a[6] < 1 || !(gm1 >= (R)(1.0 / 1048576.0))) return;
+    const R umax = ub_s<R>(a[0]), umin = lb_s<R>(a[1]);
+    const R vmax = ub_s<R>(a[2]), vmin = lb_s<R>(a[3]);
+    const R c2u = BoundMath::ub<R>(a[4]) * (R)(1.0 + 1.0 / 64.0);
+    const R c2l = BoundMath::lb<R>(a[5]) * (R)(1.0 - 1.0 / 64.0);
+    const R au = nmax(fabs(umax), fabs(umin)), av = nmax(fabs(vmax), fabs(vmin));
+    const R du = (umax - umin) + (fabs(umax) + fabs(umin)) * (R)(1.0 / 65536.0);
+    const R dv = (vmax - vmin) + (fabs(vmax) + fabs(vmin)) * (R)(1.0 / 65536.0);
+    const R ch2 = c2u + gm1 * (R)0.125 * (du * du + dv * dv);
+    const R tol = sizeof(R) == 8 ? (R)(1.0 / 1099511627776.0) : (R)(1.0 / 16384.0);
+    if (!(c2l > tol * (c2u + au * au + av * av))) return;
+    const R ch = sqrt(ch2);
+    const R bx = au + ch, by = av + ch;
+    if (!(BoundMath::small(bx) && BoundMath::small(by))) return;
+    bndx = bx; bndy = by;
+  }
+};
+
 // Euler, Roe linearisation, no entropy fix — reference kernels.py:457-533
 struct EulerRoe {
   static constexpr int NEQ = 4, NW = 3, NAUX = 0, NPR = 5;
   static constexpr bool STATIC_SPEEDS = false;
+  // tile-filtered CFL pre-pass (GasTile)
+  static constexpr bool HAS_TILE = true;
+  static constexpr int NACC = GasTile::NACC;
+  static constexpr unsigned ACC_MIN = GasTile::ACC_MIN;
+  __device__ static __forceinline__ void acc_init(int (&a)[NACC]) { GasTile::acc_init(a); }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_acc(const R* q, const P& p, int (&a)[NACC]) {
+    GasTile::acc(q, (R)0.5 * (p.gm1 + (R)1) * p.gm1, a);
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_bound(const int (&a)[NACC], const P& p, R& bx, R& by) {
+    GasTile::bound(a, p.gm1, bx, by);
+  }
   template <int NI> __host__ __device__ static constexpr bool wzero(int, int) { return false; }
   template <class R> struct Params { R gm1; };
 
@@ -267,6 +356,19 @@ struct EulerRoe {
 struct EulerHLLE {
   static constexpr int NEQ = 4, NW = 2, NAUX = 0, NPR = 6;  // gas prims + c
   static constexpr bool STATIC_SPEEDS = false;
+  // tile-filtered CFL pre-pass (GasTile)
+  static constexpr bool HAS_TILE = true;
+  static constexpr int NACC = GasTile::NACC;
+  static constexpr unsigned ACC_MIN = GasTile::ACC_MIN;
+  __device__ static __forceinline__ void acc_init(int (&a)[NACC]) { GasTile::acc_init(a); }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_acc(const R* q, const P& p, int (&a)[NACC]) {
+    GasTile::acc(q, (R)0.5 * p.gam * p.gm1, a);
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_bound(const int (&a)[NACC], const P& p, R& bx, R& by) {
+    GasTile::bound(a, p.gm1, bx, by);
+  }
   template <int NI> __host__ __device__ static constexpr bool wzero(int, int) { return false; }
   template <class R> struct Params { R gm1, gam; };
 
@@ -469,10 +571,18 @@ struct ShallowRoe {
   // Tile form (k_update_w epilogue -> k_speeds_t): integer maxima of the
   // high words over the tile's new cells, a = {max |hu|, max |hv|, max h,
   // min h} (signed, so a negative, NaN or zero depth shows up at either end),
-  // then once per tile bx = max|hu| / min h >= every cell's |u|, by likewise,
-  // bc = sqrt(g) sqrt(max h); +inf when any cell leaves the seeds' range.
-  template <class R>
-  __device__ static __forceinline__ void tile_acc(const R* q, int (&a)[4]) {
+  // then, from the accumulators folded over the cells an edge set reads,
+  // bx = max|hu| / min h >= every cell's |u|, by likewise, bc = sqrt(g)
+  // sqrt(max h), and the edge-speed bounds bx + bc (x), by + bc (y); +inf
+  // when any cell leaves the seeds' range.
+  static constexpr bool HAS_TILE = true;
+  static constexpr int NACC = 4;
+  static constexpr unsigned ACC_MIN = 0x8u;   // slots reduced with min
+  __device__ static __forceinline__ void acc_init(int (&a)[NACC]) {
+    a[0] = 0; a[1] = 0; a[2] = INT_MIN; a[3] = INT_MAX;
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_acc(const R* q, const P&, int (&a)[NACC]) {
     const int h = BoundMath::hw(q[0]);
     a[0] = max(a[0], BoundMath::hw(q[1]) & 0x7fffffff);
     a[1] = max(a[1], BoundMath::hw(q[2]) & 0x7fffffff);
@@ -480,16 +590,17 @@ struct ShallowRoe {
     a[3] = min(a[3], h);
   }
   template <class R, class P>
-  __device__ static __forceinline__ void tile_bound(const int (&a)[4], const P& p, R& bx, R& by,
-                                                    R& bc) {
+  __device__ static __forceinline__ void tile_bound(const int (&a)[NACC], const P& p, R& bndx,
+                                                    R& bndy) {
     const int lo = BoundMath::hw_lo<R>(), hi = BoundMath::hw_hi<R>();
     const R hmin = BoundMath::lb<R>(a[3]);
-    bx = BoundMath::ub<R>(a[0]) / hmin;
-    by = BoundMath::ub<R>(a[1]) / hmin;
-    bc = p.sqg * sqrt(BoundMath::ub<R>(a[2]));
+    const R bx = BoundMath::ub<R>(a[0]) / hmin;
+    const R by = BoundMath::ub<R>(a[1]) / hmin;
+    const R bc = p.sqg * sqrt(BoundMath::ub<R>(a[2]));
     const bool ok = a[0] < hi && a[1] < hi && a[2] < hi && a[3] >= lo &&
                     BoundMath::small(bx) && BoundMath::small(by) && BoundMath::small(bc);
-    if (!ok) bx = by = bc = (R)INFINITY;
+    bndx = ok ? bx + bc : (R)INFINITY;
+    bndy = ok ? by + bc : (R)INFINITY;
   }
 };
 

@@ -147,3 +147,67 @@ def test_many_tiles_two_fronts():
         + 0.59 * np.exp(-300 * ((xx - 0.8) ** 2 + (yy - 0.7) ** 2))
     q[0, 2:-2, 2:-2] = h + rng.normal(0, 1e-5, (nx, ny))
     _check(q, dx, dy, 12, bc=("periodic", "extrapolate"))
+
+
+# ---- ideal gas (Euler Roe / HLLE): tile accumulators of u, v, c^2 and a
+# "safe" flag (internal energy >= 2^-10 E, ranges); unsafe tiles probe all
+
+def _gas(rho, u, v, p, gamma=1.4):
+    return np.stack([rho, rho * u, rho * v, p / (gamma - 1) + 0.5 * rho * (u * u + v * v)])
+
+
+def _check_gas(name, q, dx, dy, steps, *, order=2, limiter="minmod",
+               bc=("extrapolate", "extrapolate"), precision="f64"):
+    nx, ny = q.shape[1] - 4, q.shape[2] - 4
+    if precision == "f32":
+        q = np.asfortranarray(q, dtype=np.float32)
+    oq, oreps = oracle_run(name, q, None, nx, ny, dx, dy, steps=steps, order=order,
+                           limiter=limiter, bc_x=bc[0], bc_y=bc[1], cfl=0.8)
+    dq, res, _ = device_run(name, q, None, nx, ny, dx, dy, steps=steps, order=order,
+                            limiter=limiter, bc_x=bc[0], bc_y=bc[1], precision=precision, cfl=0.8)
+    assert res.error.code == 0 and res.steps_done == steps
+    for k, (r, (dt, cfl, msx, msy)) in enumerate(zip(oreps, res.reports)):
+        assert (r.dt, r.max_speed_x, r.max_speed_y) == (dt, msx, msy), f"step {k}"
+    assert same_bits(oq, dq), f"max |diff| = {np.abs(oq - dq).max():.3e}"
+
+
+@pytest.mark.parametrize("name", ["euler", "euler-hlle"])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_gas_quadrants(name, precision):
+    # the C3 recipe at 180x150: piecewise-constant quadrants, one fastest
+    nx, ny = 180, 150
+    rng = np.random.default_rng(33)
+    q = np.zeros((4, nx + 4, ny + 4), order="F")
+    x = (np.arange(nx) + 0.5) / nx
+    y = (np.arange(ny) + 0.5) / ny
+    xx, yy = np.meshgrid(x, y, indexing="ij")
+    rho = np.empty((nx, ny)); u = np.empty_like(rho); v = np.empty_like(rho); p = np.empty_like(rho)
+    for m in ((xx >= .5) & (yy >= .5), (xx < .5) & (yy >= .5), (xx < .5) & (yy < .5),
+              (xx >= .5) & (yy < .5)):
+        rho[m], u[m], v[m], p[m] = (rng.uniform(.1, 1.5), rng.uniform(-.8, .8),
+                                    rng.uniform(-.8, .8), rng.uniform(.1, 1.5))
+    q[:, 2:-2, 2:-2] = _gas(rho, u, v, p)
+    _check_gas(name, q, 1 / nx, 1 / ny, 10, precision=precision)
+
+
+@pytest.mark.parametrize("name", ["euler", "euler-hlle"])
+def test_gas_high_mach_and_hot_spot(name):
+    # a Mach ~100 jet (internal energy below 2^-10 E: unsafe tiles, probed in
+    # full), a hot spot far from it that holds the maximum, periodic x
+    nx, ny = 160, 120
+    rho = np.ones((nx, ny)); u = np.zeros((nx, ny)); v = np.zeros((nx, ny)); p = np.ones((nx, ny))
+    u[20:40, 10:30] = 120.0
+    p[120:126, 90:96] = 2.0e5
+    q = np.zeros((4, nx + 4, ny + 4), order="F")
+    q[:, 2:-2, 2:-2] = _gas(rho, u, v, p)
+    _check_gas(name, q, 1 / nx, 1 / ny, 6, bc=("periodic", "extrapolate"))
+
+
+def test_gas_contact_with_large_temperature_ratio():
+    # density ratio 1e9 across a contact at rest: c^2 differs by 1e9 between
+    # neighbours (the c^2 > 0 safety margin of the Roe average)
+    nx, ny = 90, 64
+    rho = np.where(np.arange(nx)[:, None] < 45, 1.0, 1e-9) * np.ones((nx, ny))
+    q = np.zeros((4, nx + 4, ny + 4), order="F")
+    q[:, 2:-2, 2:-2] = _gas(rho, np.zeros((nx, ny)), np.full((nx, ny), 0.1), np.ones((nx, ny)))
+    _check_gas("euler-hlle", q, 1 / nx, 1 / ny, 5)
