@@ -799,7 +799,11 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
     }
   }
   __syncthreads();
-  const int ngs = (TILE_NG + SPL - 1) / SPL;   // rows of one part
+  // an item is a run of TR consecutive edge rows of a listed tile; part s of
+  // a tile takes the runs s, s + SPL, ...
+  constexpr int TR = S::NEQ >= 4 ? 4 : 1;       // gas prims are dear: march runs
+  constexpr int NRUN = (TILE_NG + TR - 1) / TR;
+  const int ngs = (NRUN + SPL - 1) / SPL;       // runs of one part
   const int nitems = s_cnt * ngs;
   if (nitems == 0) {
     if (L.trace && tid == 0) trace_cta(L, 0, t_start);
@@ -832,59 +836,78 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
   for (int item = wid; item < nitems; item += NWT) {
     const int ent = s_list[item / ngs];
     const int tile = ent & ((1 << 28) - 1);
-    const int g = ((ent >> 28) & 3) + SPL * (item % ngs);
+    const int run = ((ent >> 28) & 3) + SPL * (item % ngs);
     const bool cx = (ent & (1 << 30)) != 0, cy = ent < 0;
     const int i0 = (tile % ntx) * LW, j0 = (tile / ntx) * LW;
     // edges owned: x-edges ei in [i0, iend) on rows [j0, min(j0+29, ny));
     // y-edges ci in [i0, min(i0+29, nx)) on rows [j0, rend)
     const int iend = i0 + LW >= L.nx ? L.nx + 1 : i0 + LW;
     const int rend = j0 + LW >= L.ny ? L.ny_edges_y : j0 + LW;
-    const int r = j0 + g;
-    if (g >= TILE_NG || r >= rend) continue;
+    const int g0 = run * TR;
+    const int rb = j0 + g0;
+    int nr = rend - rb;
+    nr = nr < TR ? nr : TR;
+    if (g0 + nr > TILE_NG) nr = TILE_NG - g0;
+    if (run >= NRUN || nr <= 0) continue;
     const int ci = i0 - 1 + lane;
     const int gi = map_i(ci < L.nx ? ci : L.nx, L);
-    const bool xcol = cx && lane >= 1 && ci < iend && r < L.ny;
-    const bool ycol = cy && lane >= 1 && ci < (i0 + LW < L.nx ? i0 + LW : L.nx) && r < L.ny_edges_y;
-    R qp[NEQ], qc[NEQ], ap[NA1], ac[NA1];
-    {
-      const R* sc = q + row_off(map_j(r < L.ny ? r : L.ny, L), L) + gi;
-      const R* sp = q + row_off(map_j(r - 1, L), L) + gi;
+    const bool xc = cx && lane >= 1 && ci < iend;
+    const bool yc = cy && lane >= 1 && ci < (i0 + LW < L.nx ? i0 + LW : L.nx);
+    // all TR + 1 rows of the run in flight at once
+    R qb[TR + 1][NEQ], ab[TR + 1][NA1];
 #pragma unroll
-      for (int c = 0; c < NEQ; ++c) { qc[c] = __ldcg(sc + c * L.pitch); qp[c] = __ldcg(sp + c * L.pitch); }
-      if (NAUX > 0) {
-        const R* ac_ = aux + (long long)(map_j(r < L.ny ? r : L.ny, L) + 2) * L.astride + gi;
-        const R* ap_ = aux + (long long)(map_j(r - 1, L) + 2) * L.astride + gi;
+    for (int k = 0; k <= TR; ++k) {
+      if (k <= nr) {
+        const int rr = rb - 1 + k;
+        const int gj = map_j(rr < L.ny ? rr : L.ny, L);
+        const R* src = q + row_off(gj, L) + gi;
 #pragma unroll
-        for (int c = 0; c < NAUX; ++c) { ac[c] = __ldcg(ac_ + c * L.pitch); ap[c] = __ldcg(ap_ + c * L.pitch); }
+        for (int c = 0; c < NEQ; ++c) qb[k][c] = __ldcg(src + c * L.pitch);
+        if (NAUX > 0) {
+          const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+#pragma unroll
+          for (int c = 0; c < NAUX; ++c) ab[k][c] = __ldcg(asrc + c * L.pitch);
+        }
       }
     }
-    R pc[NP1];
-    if (NPR > 0) prims_fast<S>(qc, ac, P, pc);
-    const bool okc = S::cell_ok(qc, ac, pc, P);
-    if (cx) {
-      R ql[NEQ], al[NA1], pl[NP1];
-#pragma unroll
-      for (int c = 0; c < NEQ; ++c) ql[c] = __shfl_up_sync(0xffffffffu, qc[c], 1);
-#pragma unroll
-      for (int c = 0; c < NAUX; ++c) al[c] = __shfl_up_sync(0xffffffffu, ac[c], 1);
-#pragma unroll
-      for (int c = 0; c < NPR; ++c) pl[c] = __shfl_up_sync(0xffffffffu, pc[c], 1);
-      const bool okl = __shfl_up_sync(0xffffffffu, okc, 1);
-      if (xcol) {
-        const R sv = probe(NX{}, ql, qc, pl, pc, al, ac, okl && okc, 0, ci, r);
-        mx = nmax(mx, sv);
-        const unsigned long long hk = hint_key(sv, (long long)r * (L.nx + 1) + ci);
-        kx = hk > kx ? hk : kx;
-      }
+    R pp[NP1];
+    bool okp = true;
+    if (cy) {   // the row below the run: its prims only feed y-edges
+      if (NPR > 0) prims_fast<S>(qb[0], ab[0], P, pp);
+      okp = S::cell_ok(qb[0], ab[0], pp, P);
     }
-    if (ycol) {
-      R pp[NP1];
-      if (NPR > 0) prims_fast<S>(qp, ap, P, pp);
-      const bool okp = S::cell_ok(qp, ap, pp, P);
-      const R sv = probe(NY{}, qp, qc, pp, pc, ap, ac, okp && okc, 1, ci, r);
-      my = nmax(my, sv);
-      const unsigned long long hk = hint_key(sv, (long long)r * L.nx + ci);
-      ky = hk > ky ? hk : ky;
+#pragma unroll
+    for (int k = 1; k <= TR; ++k) {
+      if (k > nr) break;
+      const int r = rb - 1 + k;
+      R pc[NP1];
+      if (NPR > 0) prims_fast<S>(qb[k], ab[k], P, pc);
+      const bool okc = S::cell_ok(qb[k], ab[k], pc, P);
+      if (cx) {
+        R ql[NEQ], al[NA1], pl[NP1];
+#pragma unroll
+        for (int c = 0; c < NEQ; ++c) ql[c] = __shfl_up_sync(0xffffffffu, qb[k][c], 1);
+#pragma unroll
+        for (int c = 0; c < NAUX; ++c) al[c] = __shfl_up_sync(0xffffffffu, ab[k][c], 1);
+#pragma unroll
+        for (int c = 0; c < NPR; ++c) pl[c] = __shfl_up_sync(0xffffffffu, pc[c], 1);
+        const bool okl = __shfl_up_sync(0xffffffffu, okc, 1);
+        if (xc && r < L.ny) {
+          const R sv = probe(NX{}, ql, qb[k], pl, pc, al, ab[k], okl && okc, 0, ci, r);
+          mx = nmax(mx, sv);
+          const unsigned long long hk = hint_key(sv, (long long)r * (L.nx + 1) + ci);
+          kx = hk > kx ? hk : kx;
+        }
+      }
+      if (yc && r < L.ny_edges_y) {
+        const R sv = probe(NY{}, qb[k - 1], qb[k], pp, pc, ab[k - 1], ab[k], okp && okc, 1, ci, r);
+        my = nmax(my, sv);
+        const unsigned long long hk = hint_key(sv, (long long)r * L.nx + ci);
+        ky = hk > ky ? hk : ky;
+      }
+#pragma unroll
+      for (int c = 0; c < NPR; ++c) pp[c] = pc[c];
+      okp = okc;
     }
   }
   // per-warp results: at most one atomic per value and warp
