@@ -1692,7 +1692,8 @@ __device__ __forceinline__ void wait_arrivals(DevState* ds, unsigned long long n
 // the tile is stored row-coalesced.
 template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUSED,
           bool PERSIST = false>
-__global__ void __launch_bounds__(NWARP * 32, (20 / NWARP > 0 ? 20 / NWARP : 1))
+__global__ void __launch_bounds__(NWARP * 32, (sizeof(R) == 4 && NWARP == 10 ? 3
+                                                   : (20 / NWARP > 0 ? 20 / NWARP : 1)))
 k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
            const Layout L, const typename S::template Params<R> P, const StepArgs A,
            DevState* __restrict__ ds) {
