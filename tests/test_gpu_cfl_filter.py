@@ -211,3 +211,33 @@ def test_gas_contact_with_large_temperature_ratio():
     q = np.zeros((4, nx + 4, ny + 4), order="F")
     q[:, 2:-2, 2:-2] = _gas(rho, np.zeros((nx, ny)), np.full((nx, ny), 0.1), np.ones((nx, ny)))
     _check_gas("euler-hlle", q, 1 / nx, 1 / ny, 5)
+
+
+@pytest.mark.parametrize("name,steps", [("shallow-water-roe", 120), ("euler-hlle", 60),
+                                        ("euler", 40)])
+def test_long_runs_equal_the_exact_prepass(monkeypatch, name, steps):
+    # many steps of an evolving flow at a size with hundreds of tiles: the
+    # filtered pre-pass (default) against the probe-every-edge pre-pass,
+    # device against device -- every report and the final state identical
+    from helpers import device_run
+    nx, ny = 640, 470
+    if name == "shallow-water-roe":
+        q, dx, dy = _dam_break(nx, ny, seed=8)
+    else:
+        rng = np.random.default_rng(8)
+        dx, dy = 1 / nx, 1 / ny
+        xx, yy = np.meshgrid((np.arange(nx) + .5) * dx, (np.arange(ny) + .5) * dy, indexing="ij")
+        r2 = (xx - .4) ** 2 + (yy - .6) ** 2
+        rho = np.where(r2 < .02, 2.0, 1.0) + rng.normal(0, 1e-4, (nx, ny))
+        p = np.where(r2 < .02, 5.0, 1.0)
+        q = np.zeros((4, nx + 4, ny + 4), order="F")
+        q[:, 2:-2, 2:-2] = _gas(rho, 0.1 * np.ones_like(rho), np.zeros_like(rho), p)
+    kw = dict(steps=steps, order=2, limiter="mc", bc_x="periodic", bc_y="extrapolate",
+              use_run=True)
+    monkeypatch.setenv("WS_SPEEDS", "exact")
+    ref, rres, _ = device_run(name, q, None, nx, ny, dx, dy, **kw)
+    monkeypatch.delenv("WS_SPEEDS")
+    out, res, _ = device_run(name, q, None, nx, ny, dx, dy, **kw)
+    assert res.error.code == 0 and res.steps_done == steps
+    assert res.reports == rres.reports
+    assert same_bits(ref, out)
