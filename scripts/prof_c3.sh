@@ -1,0 +1,7 @@
+CMD="python bench.py --config c3 --size 2048 --steps 3 --warmup 3 --no-e2e --no-cpu"
+$CMD > gpurun_out/c3p_plain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_update_w|k_speeds_t" -s 6 -c 2 -o gpurun_out/c3p $CMD > gpurun_out/c3p_ncu.log 2>&1
+echo ncu_rc=$?
+ncu -i gpurun_out/c3p.ncu-rep --page raw --csv > gpurun_out/c3p_raw.csv 2>/dev/null
+ncu -i gpurun_out/c3p.ncu-rep --page details --csv > gpurun_out/c3p_details.csv 2>/dev/null
+ncu -i gpurun_out/c3p.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/c3p_src.csv 2>/dev/null
+rm -f gpurun_out/*.ncu-rep

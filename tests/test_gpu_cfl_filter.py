@@ -241,3 +241,47 @@ def test_long_runs_equal_the_exact_prepass(monkeypatch, name, steps):
     assert res.error.code == 0 and res.steps_done == steps
     assert res.reports == rres.reports
     assert same_bits(ref, out)
+
+
+def test_gas_error_in_a_far_tile_after_filtered_steps():
+    # Roe without entropy fix in a strong 2D rarefaction (two streams moving
+    # apart) turns inadmissible after a few steps, in tiles far from the hot
+    # spot that holds the CFL maximum: the emptying tiles fall below the
+    # "safe" internal-energy fraction, get probed, and the device stops at
+    # the oracle's last good step with the same error text
+    from helpers import device_grid
+    from paper_1308_1464_b200 import SweepError, _abi
+    from oracle import wavestep_oracle as O
+    name, nx, ny = "euler", 200, 150
+    rho = np.ones((nx, ny)); u = np.zeros((nx, ny)); v = np.zeros((nx, ny)); p = np.ones((nx, ny))
+    u[20:60, 20:60] = np.where(np.arange(20, 60)[:, None] < 40, -2.0, 2.0)
+    p[20:60, 20:60] = 0.2
+    p[170:176, 120:126] = 300.0
+    q = np.zeros((4, nx + 4, ny + 4), order="F")
+    q[:, 2:-2, 2:-2] = _gas(rho, u, v, p)
+    dx, dy = 1 / nx, 1 / ny
+    oq = np.asfortranarray(q.copy())
+    solver = O.make_solver(name, gamma=1.4)
+    good, err = 0, None
+    for _ in range(40):
+        try:
+            O.step(oq, None, O.Spec(nx, ny, dx, dy), solver, O.Controller(0.9),
+                   bc_x="extrapolate", bc_y="extrapolate", order=2, limiter="mc")
+            good += 1
+        except O.OracleError as e:
+            err = e
+            break
+    assert err is not None and good >= 2, "the rarefaction should fail after a few steps"
+    g = device_grid(name, nx, ny, dx, dy, order=2, limiter="mc")
+    try:
+        g.upload(q, None)
+        g.run(40, _abi.make_ctl(0.9))
+        res = g.poll()
+        assert res.steps_done == good and res.error.step == good
+        with pytest.raises(SweepError) as de:
+            g.raise_for(res.error)
+        assert str(de.value) == str(err)
+        out = g.download()
+    finally:
+        g.close()
+    assert same_bits(out[:, 2:-2, 2:-2], oq[:, 2:-2, 2:-2])
