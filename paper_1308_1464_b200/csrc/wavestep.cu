@@ -724,8 +724,6 @@ int ws_set_halo_peers(ws_handle* h, void* const* lo_q, void* lo_state, int32_t n
   h->L.nds_lo = static_cast<DevState*>(lo_state);
   h->L.nds_hi = static_cast<DevState*>(hi_state);
   h->L.ny_lo = lo ? ny_lo : 0;
-  // the tile pre-pass has no device-side halo wait: the exact pre-pass runs
-  if (lo || hi) h->tile_prepass = false;
   // pushes this shard receives per step: one per neighbour side it has
   h->L.hsides = (h->L.lo == ROWS_MEMORY && lo ? 1 : 0) + (h->L.hi == ROWS_MEMORY && hi ? 1 : 0);
   return WS_OK;
@@ -745,8 +743,6 @@ int ws_set_peers(ws_handle* h, int32_t npeers, void* const* peer_states) {
   }
   h->L.peers = reinterpret_cast<DevState* const*>(h->peers_dev);
   h->L.npeers = npeers;
-  // the tile pre-pass has no device-side slot push: the exact pre-pass runs
-  if (npeers > 0) h->tile_prepass = false;
   return WS_OK;
 }
 

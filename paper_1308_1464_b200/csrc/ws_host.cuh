@@ -217,7 +217,8 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
         if (ctas > (long long)nt * spl) ctas = (long long)nt * spl;
         launch(h, k_speeds_t<S, R, NWT>, dim3((unsigned)ctas), dim3(NWT * 32), 0, st,
                static_cast<const R*>(q), static_cast<const R*>(h->aux),
-               static_cast<const int4*>(h->tmax), h->L, prm(h), cur, spl, h->ds);
+               static_cast<const int4*>(h->tmax), h->L, prm(h), cur, spl, (long long)h->enq,
+               h->ds);
       }
     } else if (HasBound<S>::value && !h->speeds_exact) {
       // candidate-filter pre-pass (exact result, see k_speeds_b)

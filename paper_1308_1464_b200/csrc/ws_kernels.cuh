@@ -756,7 +756,7 @@ template <class S, class R, int NWT>
 __global__ void __launch_bounds__(NWT * 32, (S::NEQ >= 4 ? 2 : 4))
 k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __restrict__ tmax,
            const Layout L, const typename S::template Params<R> P, const int cur, const int SPL,
-           DevState* __restrict__ ds) {
+           const long long seq, DevState* __restrict__ ds) {
   constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   constexpr int LW = 29, NT = NWT * 32;
@@ -766,6 +766,13 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
   const int tid = threadIdx.x, lane = tid & 31, wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const unsigned long long t_start = L.trace ? gtimer() : 0ull;
   pdl_wait();
+  if (L.hsides > 0) {
+    // device-side halos: the neighbours' updates pushed this step's ghost
+    // rows; wait for them (the update launched after us stages ghost rows
+    // too, so the trigger comes after this wait)
+    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * seq, ds);
+    __syncthreads();
+  }
   pdl_trigger();
   const int ntx = (L.nx + LW - 1) / LW, nty = (L.ny + LW - 1) / LW, nt = ntx * nty;
   if (tid == 0) {
@@ -778,8 +785,8 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
     s_cnt = 0;
   }
   __syncthreads();
-  if (s_ok < 0) return;
-  {
+  const bool skip = s_ok < 0;
+  if (!skip) {
     const int4* tm = tmax + (long long)cur * nt * (NAcc<S>::value / 4);
     const R tlx = s_t[0], tly = s_t[1];
     // virtual index v = tile * SPL + part: the SPL parts of a tile (rows
@@ -804,11 +811,7 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
   constexpr int TR = S::NEQ >= 4 ? 4 : 1;       // gas prims are dear: march runs
   constexpr int NRUN = (TILE_NG + TR - 1) / TR;
   const int ngs = (NRUN + SPL - 1) / SPL;       // runs of one part
-  const int nitems = s_cnt * ngs;
-  if (nitems == 0) {
-    if (L.trace && tid == 0) trace_cta(L, 0, t_start);
-    return;
-  }
+  const int nitems = skip ? 0 : s_cnt * ngs;
 
   R mx = (R)0, my = (R)0;
   unsigned long long key = ~0ull, kx = 0ull, ky = 0ull;
@@ -911,6 +914,7 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
     }
   }
   // per-warp results: at most one atomic per value and warp
+  if (nitems > 0) {
   if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
   unsigned long long bxs = Bits<R>::to(mx), bys = Bits<R>::to(my);
 #pragma unroll
@@ -929,6 +933,29 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
     if (bys) atomicMax(&ds->slot[cur][1], bys);
     if (kx) atomicMax(&ds->hint_acc[cur][0], kx);
     if (ky) atomicMax(&ds->hint_acc[cur][1], ky);
+  }
+  }
+  if (L.npeers > 0) {
+    // device-side reduction across shards: the last CTA pushes this shard's
+    // slot into every shard's slot (64-bit MAX, over NVLink for peers) and
+    // announces the push with a release increment (as k_speeds_w)
+    __threadfence();
+    __syncthreads();
+    if (tid == 0 && atomicAdd(&ds->pdone, 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      ds->pdone = 0;
+      const unsigned long long v0 = atomicOr(&ds->slot[cur][0], 0ull);
+      const unsigned long long v1 = atomicOr(&ds->slot[cur][1], 0ull);
+      const unsigned long long v2 = atomicOr(&ds->slot[cur][2], 0ull);
+      for (int r = 0; r < L.npeers; ++r) {
+        DevState* pr = L.peers[r];
+        atomicMax_system(&pr->slot[cur][0], v0);
+        atomicMax_system(&pr->slot[cur][1], v1);
+        if (v2) atomicMax_system(&pr->slot[cur][2], v2);
+      }
+      __threadfence_system();
+      for (int r = 0; r < L.npeers; ++r) atomicAdd_system(&L.peers[r]->arrive, 1ull);
+    }
   }
   if (L.trace && tid == 0) trace_cta(L, 0, t_start);
 }
