@@ -327,9 +327,17 @@ def gpu_arm(args):
             roofline["traffic"] = pr.get("bytes_per_launch")
             if pr.get("fp64_pipe_active_pct") is not None:
                 # the binding resource: FP64 pipe, from the ncu capture
+                ipc = pr.get("fp64_instr_per_cell_approx")
+                pk = pr.get("fp64_peak_instr_per_s")
+                ach = ipc * cells / (upd_ms / 1e3) if ipc else None
                 roofline["fp64"] = {"pipe_active_frac_ncu": pr["fp64_pipe_active_pct"] / 100.0,
-                                    "instr_per_cell": pr.get("fp64_instr_per_cell_approx"),
-                                    "peak_instr_per_s": pr.get("fp64_peak_instr_per_s"),
+                                    "instr_per_cell": ipc,
+                                    "achieved_instr_per_s": ach,
+                                    "peak_instr_per_s": pk,
+                                    "frac": (ach / pk) if (ach and pk) else None,
+                                    "note": "FP64 warp-lane instructions per cell from the ncu "
+                                            "capture x cells / event-timed update kernel, "
+                                            "against the measured DFMA peak",
                                     "peak_source": pr.get("fp64_peak_source")}
         except Exception:
             pass
