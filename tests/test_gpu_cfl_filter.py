@@ -285,3 +285,30 @@ def test_gas_error_in_a_far_tile_after_filtered_steps():
     finally:
         g.close()
     assert same_bits(out[:, 2:-2, 2:-2], oq[:, 2:-2, 2:-2])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_configs_filtered_equals_exact(monkeypatch, seed):
+    # randomised sizes (partial tiles, 1-tile-wide strips), boundary
+    # conditions, limiters and precisions: the tile pre-pass against the
+    # probe-every-edge pre-pass, device against device
+    from helpers import device_run, random_state
+    rng = np.random.default_rng(1000 + seed)
+    name = ["shallow-water-roe", "euler-hlle", "euler"][seed % 3]
+    nx, ny = int(rng.integers(20, 400)), int(rng.integers(20, 300))
+    bc = [("extrapolate", "extrapolate"), ("periodic", "periodic"),
+          ("periodic", "extrapolate")][int(rng.integers(0, 3))]
+    limiter = ["minmod", "superbee", "mc"][int(rng.integers(0, 3))]
+    precision = "f32" if rng.random() < 0.3 else "f64"
+    q, _ = random_state(name, nx, ny, seed=seed)
+    if precision == "f32":
+        q = np.asfortranarray(q, dtype=np.float32)
+    dx, dy = 1 / nx, 1 / ny
+    kw = dict(steps=15, order=2, limiter=limiter, bc_x=bc[0], bc_y=bc[1], precision=precision)
+    monkeypatch.setenv("WS_SPEEDS", "exact")
+    ref, rres, _ = device_run(name, q, None, nx, ny, dx, dy, **kw)
+    monkeypatch.delenv("WS_SPEEDS")
+    out, res, _ = device_run(name, q, None, nx, ny, dx, dy, **kw)
+    assert res.error.code == rres.error.code
+    assert res.reports == rres.reports
+    assert same_bits(ref, out)
