@@ -12,7 +12,9 @@ Metric: cell-updates/s = nx*ny*steps / time (reference bench.py:194-203).
   python bench.py --impl reference ...      # reference-path CPU arm
 
 N > 1 (torchrun): weak scaling, row strips of nx x ny per rank stacked along
-y, halo rows + the CFL max exchanged with NCCL every step (parallel.py).
+y, halo rows + the CFL max exchanged with NCCL every step (parallel.py);
+--strong cuts the 1-GPU grid into N row strips instead (BASELINE C3 / C5
+strong-scaling runs: `--config c5 --strong`).
 """
 
 from __future__ import annotations
@@ -52,6 +54,9 @@ def parse():
     ap.add_argument("--device-halo", action="store_true",
                     help="row-strip path: halo rows pushed by the update kernel into the "
                          "neighbours' ghost rows over peer memory (implies --device-reduce)")
+    ap.add_argument("--strong", action="store_true",
+                    help="row-strip path: strong scaling (the 1-GPU grid cut into N strips) "
+                         "instead of weak (an N-times taller grid, one 1-GPU strip per rank)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the row-strip (NCCL) path even with one rank (tests it on 1 GPU)")
     ap.add_argument("--size", type=int, default=None,

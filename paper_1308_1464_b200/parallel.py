@@ -325,22 +325,28 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    base = build_case(args.config, precision=args.precision)
+    base = build_case(args.config, precision=args.precision,
+                      device=torch.device("cuda", local), size=getattr(args, "size", None))
     prec = base.dtype
-    # weak scaling: the per-GPU strip is the 1-GPU workload; strips stack along y
-    ny_g = base.ny * world
+    strong = bool(getattr(args, "strong", False))
+    # weak scaling: the per-GPU strip is the 1-GPU workload, strips stacked
+    # along y; strong scaling: the 1-GPU grid itself, cut into row strips
+    ny_g = base.ny if strong else base.ny * world
     strips = RowStrips(ny_g, world)
     j0, j1 = strips.bounds(rank)
 
     def stack(f):
-        if f is None:
-            return None
+        if f is None or strong:
+            return f
         g = np.zeros((f.shape[0], base.nx + 4, ny_g + 4), order="F")
         for r in range(world):
             g[:, :, 2 + r * base.ny:2 + (r + 1) * base.ny] = f[:, :, 2:-2]
         return g
 
     glob, gaux = stack(base.q), stack(base.aux)
+    if strong:
+        glob = np.asfortranarray(glob.copy())
+        gaux = np.asfortranarray(gaux.copy()) if gaux is not None else None
     if periodic_rows(base.bc):
         # periodic y: the outermost strips' memory ghost rows wrap around
         # (static aux rows are never exchanged, so they must be right here)
@@ -412,8 +418,10 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k,
             "warmup": args.warmup, "ms_per_step": ms_max / k, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
-            "config": {"workload": f"{case.name} x{world} strips (weak)", "kernel": case.kernel,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": prec,
+            "data": "synthetic",
+            "config": {"workload": (f"{case.name} in {world} strips (strong)" if strong else
+                                    f"{case.name} x{world} strips (weak)"), "kernel": case.kernel,
                        "nx": case.nx, "ny": ny_g, "limiter": case.limiter, "order": case.order,
                        "cfl": case.cfl, "parallelism": f"row-strips{world}",
                        "l2": "flushed between timed steps (512 MiB write)",

@@ -83,6 +83,20 @@ def test_bench_force_sharded_line():
     assert line["gpu_launches"] > 0
 
 
+def test_bench_force_sharded_strong_line():
+    # strong scaling: the 1-GPU grid cut into row strips (one strip at world 1)
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+               WORLD_SIZE="1", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-sharded",
+                        "--strong", "--config", "c3", "--steps", "3", "--warmup", "3",
+                        "--no-e2e", "--no-cpu"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["scaling"] == "strong" and line["value"] > 0
+    assert line["config"]["ny"] == 4096 and "(strong)" in line["config"]["workload"]
+
+
 @pytest.mark.parametrize("flag,text", [("--device-reduce", "device-side slot reduction"),
                                        ("--device-halo", "done by the kernels over peer memory")])
 def test_bench_force_sharded_device_collective_line(flag, text):
