@@ -526,7 +526,8 @@ def correction_flux(w, s, dtdn, limiter, axis):
     the upwind edge (k-1 if s_p > 0 else k+1):
         theta = (W_up . W) / (W . W)   (dot products summed m = 0..neq-1)
         W~ = phi(theta) W   (W~ = 0 when W . W == 0)
-        F~ = 0.5 * sum_p (|s_p| * (1 - dtdn |s_p|)) * W~_p
+        F~ = 0.5 * sum_p ((|s_p| * (1 - dtdn |s_p|)) * phi_p) * W_p
+    (the wave's scalar factors multiplied first: one product per component)
     Returns F~ for edges 1..nE-2 of the input (i.e. edges [0, n]).
     """
     mw, neq = w.shape[0], w.shape[1]
@@ -545,12 +546,12 @@ def correction_flux(w, s, dtdn, limiter, axis):
     theta = np.zeros_like(dow)
     np.divide(dup, dow, out=theta, where=nz)
     ph = phi(theta, limiter)
-    wl = ph[:, None] * own
     a = np.abs(so)
     coef = a * (1.0 - dtdn * a)
-    f = coef[0][None] * wl[0]
+    cph = coef * ph
+    f = cph[0][None] * own[0]
     for p in range(1, mw):
-        f = f + coef[p][None] * wl[p]
+        f = f + cph[p][None] * own[p]
     return 0.5 * f
 
 

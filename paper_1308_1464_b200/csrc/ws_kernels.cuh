@@ -1351,10 +1351,11 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
                 R ph = limiter_phi<LIM>(th);
                 R a = fabs(so);
                 R coef = a * ((R)1 - dtdn * a);
+                R cph = coef * ph;
 #pragma unroll
                 for (int m = 0; m < NEQ; ++m) {
-                  R wl = ph * own[m];
-                  f[m] = (w == 0) ? coef * wl : f[m] + coef * wl;
+                  R wl = cph * own[m];
+                  f[m] = (w == 0) ? wl : f[m] + wl;
                 }
               }
 #pragma unroll
@@ -1676,11 +1677,12 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
       R ph = limiter_phi<LIM>(th);
       R a = fabs(s[w]);
       R coef = a * ((R)1 - dtdn * a);
+      R cph = coef * ph;
 #pragma unroll
       for (int m = 0; m < NEQ; ++m) {
         if (S::template wzero<NI>(w, m)) continue;
-        R wl = ph * W[w][m];
-        f[m] = fz[m] ? coef * wl : f[m] + coef * wl;
+        R wl = cph * W[w][m];
+        f[m] = fz[m] ? wl : f[m] + wl;
         fz[m] = false;
       }
     }
