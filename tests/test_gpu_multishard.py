@@ -218,8 +218,12 @@ def test_shard_refuses_whole_steps_without_device_collectives():
         sh.grid.close()
 
 
-@pytest.mark.parametrize("bc", ["extrapolate", "periodic"])
-def test_fake_shards_tile_prepass_skips_tiles(bc):
+@pytest.mark.parametrize("bc,dred,dhalo", [("extrapolate", False, False),
+                                           ("periodic", False, False),
+                                           ("periodic", True, False),
+                                           ("extrapolate", True, True),
+                                           ("periodic", True, True)])
+def test_fake_shards_tile_prepass_skips_tiles(bc, dred, dhalo):
     # shallow water strips large enough that most tiles are skipped by the
     # tile pre-pass (the maximum sits on one dam's front), the boundary tile
     # rows next to ghost rows in memory always probed
@@ -232,7 +236,8 @@ def test_fake_shards_tile_prepass_skips_tiles(bc):
         + rng.normal(0, 1e-4, (nx, ny))
     ref, oreps = oracle_run(name, gq, None, nx, ny, dx, dy, steps=steps, order=2,
                             limiter="mc", bc_x=bc, bc_y=bc)
-    out, reps, errs, strips = fake_sharded(name, gq, None, nx, ny, dx, dy, P, steps, 2, "mc", bc)
+    out, reps, errs, strips = fake_sharded(name, gq, None, nx, ny, dx, dy, P, steps, 2, "mc", bc,
+                                           device_reduce=dred, device_halo=dhalo)
     for r in range(P):
         j0, j1 = strips.bounds(r)
         assert errs[r].code == 0
