@@ -130,7 +130,10 @@ int ws_download_f32(ws_handle* h, float* q_host, void* stream);
  * handle execute in issue order whatever streams they are issued on (a call
  * on a different stream than the previous one waits for it), with two
  * relaxations that let transfers overlap: ws_upload's host-to-device copy
- * may start before earlier work finishes, and work issued after a download
+ * may start before earlier work finishes (it runs on the handle's copy stream
+ * into one of two alternating staging buffers; the conversion into the
+ * state, on the caller's stream, waits for it, so the host array may be
+ * reused once the caller's stream has passed the upload), and work issued after a download
  * on another stream does not wait for that download's device-to-host copy
  * (wait for the stream, or use the synchronous ws_download, before reading
  * the host array). */
