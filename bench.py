@@ -265,7 +265,7 @@ def gpu_arm(args):
     dyn = not (case.kernel.startswith("acoustics"))
     k = args.steps
 
-    def timed_loop(split):
+    def timed_loop(split, g=g):
         # events bracket each step (split: also between the two kernels, which
         # costs the programmatic overlap of the pre-pass tail with the update's
         # launch, so the headline uses the unsplit loop)
@@ -364,6 +364,50 @@ def gpu_arm(args):
     g.raise_for(res_run.error)
     sim_ms = e0.elapsed_time(e1)
 
+    # The default CFL pre-pass of shallow water and Euler probes only the tiles
+    # that can hold the step's maximum.  Twin handle with
+    # WS_SPEEDS=exact (every edge probed): its timing next to ours, and a
+    # bitwise guard -- same upload, same steps, states and every report equal.
+    exact = None
+    if dyn and case.kernel in ("shallow-water-roe", "euler", "euler-hlle"):
+        old_env = os.environ.get("WS_SPEEDS")
+        os.environ["WS_SPEEDS"] = "exact"
+        try:
+            g2 = DeviceGrid(case.nx, case.ny, case.dx, case.dy, kernel, order=case.order,
+                            limiter=case.limiter, bc_x=case.bc, bc_y=case.bc, precision=prec,
+                            device=local)
+        finally:
+            if old_env is None:
+                os.environ.pop("WS_SPEEDS", None)
+            else:
+                os.environ["WS_SPEEDS"] = old_env
+        ns = min(case.steps, 20)
+        outs = []
+        for h in (g, g2):
+            h.upload(host_q, host_aux, stream=sp)
+            h.run(ns, ctl, stream=sp)
+            torch.cuda.synchronize()
+            r = h.poll()
+            h.raise_for(r.error)
+            outs.append((h.download(), r.reports))
+        same = bool(np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1])
+        g2.upload(host_q, host_aux, stream=sp)
+        for _ in range(args.warmup):
+            g2.step(ctl, stream=sp)
+        torch.cuda.synchronize()
+        ev2 = timed_loop(split=False, g=g2)
+        r2 = g2.poll()
+        g2.raise_for(r2.error)
+        ms2 = sum(ev2[i][0].elapsed_time(ev2[i][2]) for i in range(k)) / k
+        exact = {"value": cells / (ms2 / 1e3), "unit": UNIT, "ms_per_step": ms2,
+                 "bitwise_equal_to_default": same, "guard_steps": ns,
+                 "note": "same step with the CFL pre-pass probing every edge "
+                         "(WS_SPEEDS=exact); the default's tile filter is exact, the guard "
+                         "compares the state and every report after guard_steps steps"}
+        g2.close()
+        if not same:
+            raise SystemExit("tile-filtered pre-pass differs from the exact pre-pass")
+
     e2e = None
     if not args.no_e2e:
         e2e = e2e_leg(g, case, host_q, host_aux, ctl, stream, k)
@@ -386,6 +430,7 @@ def gpu_arm(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
+        "exact_prepass": exact,
         "clocks": clk.summary(),
         "simulation": {"steps": case.steps, "ms": sim_ms,
                        "cell_updates_per_s": cells * res_run.steps_done / (sim_ms / 1e3),
