@@ -688,16 +688,17 @@ k_speeds_b(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
 }
 
 // --------------------------------------------------------------------------
-// CFL / admissibility pre-pass over whole tiles (single-domain solvers with
-// S::HAS_BOUND; the default for them), two kernels.
+// CFL / admissibility pre-pass over whole tiles (solvers with S::HAS_TILE:
+// shallow water, Euler Roe / HLLE; the default for them).
 //
 // The update kernel that wrote the state also stored, per 29x29 tile, integer
-// maxima of its new cells (S::tile_acc) and probed one x- and one y-edge of
-// the new state exactly (DevState::tnext: the edges where this step's maxima
-// were found).  Every edge a tile owns reads cells of the tile or of its 8
-// neighbours (boundary mapping included), so S::tile_bound over the 3x3
-// neighbourhood gives B_x(tile) >= max|s| of each x-edge it owns (B_y
-// likewise).  With T an exact max|s| of some edge of this state (tnext, the
+// maxima / minima of its new cells (S::tile_acc) and probed one x- and one
+// y-edge of the new state exactly (DevState::tnext: the edges where this
+// step's maxima were found).  The x-edges a tile owns read cells of the tile
+// and of its left neighbour (periodic: also the wrapped right one for the
+// domain's last edge column), its y-edges the tile and the one below, so
+// S::tile_bound over those accumulators gives B_x(tile) >= max|s| of each
+// x-edge it owns (B_y likewise).  With T an exact max|s| of some edge of this state (tnext, the
 // running slot maximum), a tile with B_x * MARGIN < T cannot hold the x
 // maximum: its x-edges are not even loaded.  The others are probed exactly,
 // so the step's maxima are bit-identical to probing every edge.  A cell that
@@ -1801,9 +1802,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
   }
   // TMAX (tile pre-pass): after the tile's warps reduced into s_acc and the
-  // new tile sits in sX: store the tile accumulators, probe the hint edges
-  // if this tile holds them (the next pre-pass's exact lower bound), reset
-  // s_acc.  Runs after a barrier that follows the tile's store loop.
+  // new tile sits in sX: warp 0 folds and stores the tile accumulators, the
+  // tile that holds a hint edge probes it (the next pre-pass's exact lower
+  // bound).  Runs after a barrier that follows the tile's store loop.
   int t_prev = -1;
   auto finish_tile = [&](int tt) {
     if constexpr (HasTile<S>::value) {
