@@ -16,10 +16,13 @@ The ``cuda`` row is the twin: a ``cuda-run`` whose final state is not
 bitwise identical to it aborts the bench (BenchGuardError, as the
 reference's threaded-vs-serial guard :176-183).  ``speedup`` is relative to
 the ``cuda`` row; ``threads`` is the GPU count (1: one process drives one
-GPU; multi-GPU rows come from ``bench.py --gpus N`` under torchrun).  Three
-roofline columns follow the reference's eleven: algorithmic bytes per
-cell-update (q read + aux read + q written), achieved GB/s and the fraction
-of the measured HBM peak (MEASURED_PEAKS.json when present).
+GPU; multi-GPU rows come from ``bench.py --gpus N`` under torchrun).
+
+The CSV is byte-for-byte the reference's eleven-column format, so the
+reference's own ``parse_csv`` (bench.py:236-270) reads it back.  The roofline
+columns (algorithmic bytes per cell-update = q read + aux read + q written,
+achieved GB/s, fraction of the measured HBM peak from MEASURED_PEAKS.json)
+go to a sidecar file (``--roofline-out``, :func:`emit_roofline_csv`).
 
     python -m paper_1308_1464_b200.benchmatrix --kernels shallow-water-roe \
         --sizes 1024x1024 --order 2 --limiter mc --out matrix.csv
@@ -45,6 +48,7 @@ from .sweep import CellWise, RowWise, Strategy, Tiled
 
 CSV_HEADER = ("kernel,nx,ny,strategy,backend,threads,steps,"
               "ms_per_step,mcells_per_s,speedup,efficiency")
+ROOFLINE_KEY = "kernel,nx,ny,strategy,backend"
 ROOFLINE_HEADER = "bytes_per_cell,achieved_gbs,hbm_frac"
 BACKEND_NAMES = ("cuda", "cuda-run")
 EFFICIENCY_FLAG = 1.5
@@ -246,28 +250,64 @@ def _fmt(x: float) -> str:
     return f"{x:.6g}"
 
 
-def emit_csv(records: list[BenchRecord], out=None) -> None:
-    """Reference emit_csv (bench.py:211-234): exact header, 6 significant
-    digits for reals; the roofline columns are appended after the eleven."""
-    own = False
+def _open(out):
     if out is None:
-        fh = sys.stdout
-    elif hasattr(out, "write"):
-        fh = out
-    else:
-        fh = open(out, "w", encoding="utf-8")
-        own = True
+        return sys.stdout, False
+    if hasattr(out, "write"):
+        return out, False
+    return open(out, "w", encoding="utf-8"), True
+
+
+def emit_csv(records: list[BenchRecord], out=None) -> None:
+    """Reference emit_csv (bench.py:209-234): the exact eleven-column header
+    and rows, 6 significant digits for reals."""
+    fh, own = _open(out)
     try:
-        fh.write(CSV_HEADER + "," + ROOFLINE_HEADER + "\n")
+        fh.write(CSV_HEADER + "\n")
         for r in records:
             fh.write(",".join([
                 r.kernel, str(r.nx), str(r.ny), r.strategy, r.backend, str(r.threads),
                 str(r.steps), _fmt(r.ms_per_step), _fmt(r.mcells_per_s), _fmt(r.speedup),
-                _fmt(r.efficiency), str(r.bytes_per_cell), _fmt(r.achieved_gbs),
-                _fmt(r.hbm_frac)]) + "\n")
+                _fmt(r.efficiency)]) + "\n")
     finally:
         if own:
             fh.close()
+
+
+def emit_roofline_csv(records: list[BenchRecord], out=None) -> None:
+    """Sidecar of emit_csv: the row key plus the three roofline columns."""
+    fh, own = _open(out)
+    try:
+        fh.write(ROOFLINE_KEY + "," + ROOFLINE_HEADER + "\n")
+        for r in records:
+            fh.write(",".join([r.kernel, str(r.nx), str(r.ny), r.strategy, r.backend,
+                               str(r.bytes_per_cell), _fmt(r.achieved_gbs),
+                               _fmt(r.hbm_frac)]) + "\n")
+    finally:
+        if own:
+            fh.close()
+
+
+def parse_csv(source) -> list[BenchRecord]:
+    """Reference parse_csv (bench.py:236-270): header and eleven fields checked."""
+    fh, own = (source, False) if hasattr(source, "read") else (
+        open(source, "r", encoding="utf-8"), True)
+    try:
+        lines = [ln.strip() for ln in fh if ln.strip()]
+    finally:
+        if own:
+            fh.close()
+    if not lines or lines[0] != CSV_HEADER:
+        raise ValueError("not a bench CSV: bad or missing header")
+    out = []
+    for ln in lines[1:]:
+        p = ln.split(",")
+        if len(p) != 11:
+            raise ValueError(f"malformed row: {ln!r}")
+        out.append(BenchRecord(p[0], int(p[1]), int(p[2]), p[3], p[4], int(p[5]), int(p[6]),
+                               float(p[7]), float(p[8]), float(p[9]), float(p[10]),
+                               0, 0.0, 0.0))
+    return out
 
 
 def _size(s: str) -> tuple[int, int]:
@@ -290,6 +330,8 @@ def main(argv=None) -> int:
     ap.add_argument("--limiter", default="none")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--out", default=None)
+    ap.add_argument("--roofline-out", default=None,
+                    help="sidecar CSV with bytes/cell, achieved GB/s and the HBM fraction")
     a = ap.parse_args(argv)
     strat = {"rowwise": RowWise(), "cellwise": CellWise(), "tiled": Tiled()}
     cfg = BenchConfig(kernels=tuple(a.kernels), sizes=tuple(_size(s) for s in a.sizes),
@@ -299,6 +341,8 @@ def main(argv=None) -> int:
                       limiter=a.limiter, precision=a.precision, out=a.out)
     recs = run_bench(cfg, progress=lambda m: print(m, file=sys.stderr))
     emit_csv(recs, cfg.out)
+    if a.roofline_out:
+        emit_roofline_csv(recs, a.roofline_out)
     return 0
 
 

@@ -445,6 +445,7 @@ static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz
   WS_CUDA(h, launch_status(h));
   h->enq = 0;
   h->nrep_seen = 0;
+  h->tf_pending = false;
   h->uploaded = true;
   return WS_OK;
 }
@@ -524,6 +525,27 @@ int ws_download_async(ws_handle* h, void* q, void* s) {
   return download_impl(h, q, h ? h->esz : 8, s, false);
 }
 
+// Steps pick their buffers from the host's count of enqueued steps.  A step
+// whose control carries t_final can stop on the device (t reached), so after
+// one the host count may run ahead of the committed steps.  Continuing with
+// the same t_final is harmless (every further step is a no-op), anything else
+// first re-aligns the count with the device and clears the finished flag.
+static int tfinal_guard(ws_handle* h, const ws_ctl* c, cudaStream_t st) {
+  const bool tf = !std::isnan(c->t_final);
+  if (h->tf_pending && tf && c->t_final == h->tf_value) return WS_OK;
+  if (h->tf_pending) {
+    HostState hs;
+    int rc = read_state(h, &hs, st);
+    if (rc) return rc;
+    if ((rc = resync(h, hs, st))) return rc;
+    // only a t_final step sets the flag, and upload clears it
+    WS_CUDA(h, cudaMemsetAsync(&h->ds->finished, 0, sizeof(int), st));
+  }
+  h->tf_pending = tf;
+  h->tf_value = tf ? c->t_final : 0.0;
+  return WS_OK;
+}
+
 // a row-strip shard can run whole steps only when the kernels do its
 // collectives (slot reduction and every memory ghost-row side pushed)
 static bool device_collectives(const ws_handle* h) {
@@ -542,7 +564,7 @@ int ws_step(ws_handle* h, const ws_ctl* c, void* s) {
   int rc = check_ctl(h, c);
   if (rc) return rc;
   cudaStream_t st = pick(h, s);
-  if (!std::isnan(c->t_final)) WS_CUDA(h, cudaMemsetAsync(&h->ds->finished, 0, sizeof(int), st));
+  if ((rc = tfinal_guard(h, c, st))) return rc;
   enqueue_step(h, c, (int)(h->enq & 1), st);
   h->enq++;
   WS_CUDA(h, launch_status(h));
@@ -610,7 +632,7 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
   int rc = check_ctl(h, c);
   if (rc) return rc;
   cudaStream_t st = pick(h, s);
-  WS_CUDA(h, cudaMemsetAsync(&h->ds->finished, 0, sizeof(int), st));
+  if ((rc = tfinal_guard(h, c, st))) return rc;
   long long left = nsteps;
   if (left > 0 && (h->enq & 1)) { enqueue_step(h, c, 1, st); h->enq++; left--; }
   if (left >= 4 && h->need_prepass && !h->ops.static_speeds) {

@@ -73,6 +73,11 @@ struct ws_handle {
   cudaEvent_t ev_out = nullptr;    // download staging copied out (next download may refill it)
   long long enq = 0;            // steps enqueued since upload (== committed after a poll)
   long long nrep_seen = 0;
+  // a t_final control was enqueued since the last resync: the device may have
+  // stopped early, so enq can run ahead of the committed steps (and of the
+  // buffer parity).  The next call with another control resyncs first.
+  bool tf_pending = false;
+  double tf_value = 0.0;
   bool multi = false;           // row-strip shard with memory ghost rows
   bool uploaded = false;
   double host_static[2] = {0, 0};

@@ -10,15 +10,45 @@ from paper_1308_1464_b200 import benchmatrix as BM
 from paper_1308_1464_b200.sweep import RowWise, Tiled
 
 
-def test_header_is_the_reference_header_plus_roofline():
+def _rec():
+    return BM.BenchRecord("euler", 64, 32, "tiled", "cuda-run", 1, 5, 0.123456789,
+                          16.6666666, 3.14159265, 3.14159265, 64, 1062.666, 0.16)
+
+
+def test_csv_is_exactly_the_reference_format():
     assert BM.CSV_HEADER == ("kernel,nx,ny,strategy,backend,threads,steps,"
                              "ms_per_step,mcells_per_s,speedup,efficiency")
     buf = io.StringIO()
-    BM.emit_csv([BM.BenchRecord("euler", 64, 32, "tiled", "cuda-run", 1, 5, 0.123456789,
-                                16.6666666, 3.14159265, 3.14159265, 64, 1062.666, 0.16)], buf)
+    BM.emit_csv([_rec()], buf)
     lines = buf.getvalue().splitlines()
-    assert lines[0] == BM.CSV_HEADER + ",bytes_per_cell,achieved_gbs,hbm_frac"
-    assert lines[1] == "euler,64,32,tiled,cuda-run,1,5,0.123457,16.6667,3.14159,3.14159,64,1062.67,0.16"
+    assert lines[0] == BM.CSV_HEADER
+    assert lines[1] == "euler,64,32,tiled,cuda-run,1,5,0.123457,16.6667,3.14159,3.14159"
+    back = BM.parse_csv(io.StringIO(buf.getvalue()))
+    assert (back[0].kernel, back[0].nx, back[0].backend, back[0].mcells_per_s) == (
+        "euler", 64, "cuda-run", 16.6667)
+    side = io.StringIO()
+    BM.emit_roofline_csv([_rec()], side)
+    assert side.getvalue().splitlines() == [
+        "kernel,nx,ny,strategy,backend,bytes_per_cell,achieved_gbs,hbm_frac",
+        "euler,64,32,tiled,cuda-run,64,1062.67,0.16"]
+
+
+def test_csv_round_trips_through_the_reference_parser():
+    # the reference's own reader (bench.py:236-270) accepts our file
+    import sys
+    src = "/root/reference/pkg/src"
+    import os
+    if not os.path.isdir(src):
+        pytest.skip("reference not present (GPU box)")
+    sys.path.insert(0, src)
+    try:
+        from wavesweep import bench as RB
+    finally:
+        sys.path.remove(src)
+    buf = io.StringIO()
+    BM.emit_csv([_rec(), _rec()], buf)
+    recs = RB.parse_csv(io.StringIO(buf.getvalue()))
+    assert len(recs) == 2 and recs[0].kernel == "euler" and recs[1].steps == 5
 
 
 @pytest.mark.parametrize("kw,msg", [

@@ -385,6 +385,51 @@ def test_run_to_t_final_matches_oracle(name, order, limiter):
         g.close()
 
 
+@pytest.mark.parametrize("first_steps,second", [(50, "t_final"), (50, "steps"), (3, "t_final")])
+def test_t_final_runs_back_to_back_without_polling(first_steps, second):
+    # a t_final run that stops early leaves the host's step count
+    # ahead of the device's; the next run (larger t_final, or plain steps)
+    # must continue from the newest state, not the stale ping-pong buffer
+    from paper_1308_1464_b200 import _abi
+    from helpers import device_grid
+    name, nx, ny = "shallow-water-roe", 48, 37
+    dx, dy = 1.0 / nx, 1.0 / ny
+    q, aux = random_state(name, nx, ny, 31)
+    solver = O.make_solver(name, **PARAMS[name])
+    spec = O.Spec(nx, ny, dx, dy)
+    kw = dict(bc_x="periodic", bc_y="periodic", order=2, limiter="mc")
+    probe = O.step(np.asfortranarray(q.copy()), None, spec, solver, O.Controller(0.9), **kw)
+    t1, t2 = 6.37 * probe.dt, 11.71 * probe.dt      # 7 steps (odd) then more
+    oq = np.asfortranarray(q.copy())
+    oreps = O.run(oq, None, spec, solver, O.Controller(0.9), t_final=t1, **kw)
+    if second == "t_final":
+        # the reference loop restarted with remaining = t2 - t
+        t = sum(r.dt for r in oreps)
+        while t2 - t > 1e-14 * max(1.0, t2):
+            r = O.step(oq, None, spec, solver, O.Controller(0.9), remaining=t2 - t, **kw)
+            oreps.append(r)
+            t += r.dt
+    else:
+        oreps += [O.step(oq, None, spec, solver, O.Controller(0.9), **kw) for _ in range(4)]
+    g = device_grid(name, nx, ny, dx, dy, **kw)
+    try:
+        g.upload(q, aux)
+        g.run(first_steps, _abi.make_ctl(0.9, t_final=t1))   # stops itself after 7
+        if first_steps < 7:
+            g.run(50, _abi.make_ctl(0.9, t_final=t1))        # same t_final continues
+        if second == "t_final":
+            g.run(50, _abi.make_ctl(0.9, t_final=t2))
+        else:
+            g.run(4, _abi.make_ctl(0.9))
+        res = g.poll()
+        assert res.error.code == 0
+        assert res.steps_done == len(oreps)
+        assert [r[0] for r in res.reports] == [r.dt for r in oreps]
+        assert same_bits(oq, g.download())
+    finally:
+        g.close()
+
+
 def test_driver_run_t_final_and_remaining():
     # the public driver API: run(config with t_final) and step(remaining=...)
     from paper_1308_1464_b200 import (BoundaryCondition, GridSpec, SimulationConfig,
