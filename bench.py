@@ -1,10 +1,11 @@
 #!/usr/bin/env python
 """Benchmark of the B200 wave-propagation step (contract: see DESIGN.md §7).
 
-Default workload = BASELINE.json configs[1] (C2): 2D shallow water, Roe +
-Harten entropy fix, 1024x1024 cells on [-1,1]^2, MC limiter, second order,
-CFL 0.9, extrapolation BCs, seeded dam-break input.  One bench "step" is one
-time step of that simulation.
+Default workload = BASELINE.json configs[4] (C5), the largest single-GPU
+configuration: 2D shallow water, Roe + Harten entropy fix, 16384x16384 cells
+on the unit square, fp64, MC limiter, second order, CFL 0.9, extrapolation
+BCs, h = 1 + 64 seeded Gaussian bumps.  One bench "step" is one time step of
+that simulation.  `--config c1..c4` time the other BASELINE configurations.
 
 Metric: cell-updates/s = nx*ny*steps / time (reference bench.py:194-203).
 
@@ -40,14 +41,16 @@ UNIT = "cell-updates/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--precision", default=None, choices=[None, "f64", "f32"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-ref-code", action="store_true",
+                    help="skip timing the reference package's own step (baseline/_ref)")
     ap.add_argument("--device-reduce", action="store_true",
                     help="row-strip path: CFL reduction by the kernels over peer memory "
                          "(symmetric memory) instead of an NCCL all-reduce")
@@ -74,7 +77,7 @@ def build_case(name: str, n_ranks: int = 1, precision: str | None = None, device
     from paper_1308_1464_b200 import configs
     if name == "c5":
         # 16384^2: the 64-bump sum runs in torch on the GPU when one is given
-        # (numpy would take minutes); the host block is then filled from it
+        # (from the numpy 1D factors: the same bits as the host generator)
         c = configs.c5_bumps(size or 16384, dtype=precision or "f64", device=device)
         if c.q is None:
             h = c.meta.pop("h_dev").t().contiguous().cpu().numpy()    # [i][j]
@@ -88,6 +91,66 @@ def build_case(name: str, n_ranks: int = 1, precision: str | None = None, device
     if precision:
         c.dtype = precision
     return c
+
+
+# the CPU legs time whole steps of a bounded row band of the workload (its
+# own grid: the band's cells plus the two rows either side as its ghost
+# frame, extrapolation BCs): at most this many cells per sample step
+CPU_SAMPLE_CELLS = 1 << 23
+
+
+def cpu_sample_case(name: str, precision: str | None = None, size: int | None = None):
+    """The workload's bounded CPU sample: the whole grid when it has at most
+    CPU_SAMPLE_CELLS cells, else the centred row band of that many cells."""
+    from paper_1308_1464_b200 import configs
+    if name == "c5":
+        n = size or 16384
+        rows = max(2, min(n, CPU_SAMPLE_CELLS // n))
+        j0 = (n - rows) // 2
+        c = configs.c5_bumps(n, rows=(j0, j0 + rows))
+    else:
+        c = build_case(name, size=size)
+        if c.cells > CPU_SAMPLE_CELLS:
+            rows = max(2, CPU_SAMPLE_CELLS // c.nx)
+            j0 = (c.ny - rows) // 2
+            sl = slice(j0, j0 + rows + 4)       # band rows + 2 ghost rows each side
+            c.q = np.asfortranarray(c.q[:, :, sl])
+            if c.aux is not None:
+                c.aux = np.asfortranarray(c.aux[:, :, sl])
+            c.meta = dict(c.meta, rows=(j0, j0 + rows), ny_full=c.ny)
+            c.ny = rows
+    if precision:
+        c.dtype = precision
+    return c
+
+
+def sample_text(c) -> str:
+    j0, j1 = c.meta.get("rows", (0, c.ny))
+    if "ny_full" in c.meta and (j0, j1) != (0, c.meta["ny_full"]):
+        return (f"rows [{j0}, {j1}) of the {c.nx}x{c.meta['ny_full']} grid as their own "
+                f"{c.nx}x{c.ny} grid (same recipe, extrapolation BCs)")
+    return f"the whole {c.nx}x{c.ny} grid"
+
+
+def l2_note(case, ny: int) -> str:
+    from paper_1308_1464_b200 import configs
+    nb = case.nx * ny * configs.bytes_per_cell(case.kernel, case.dtype) // 2
+    if nb > 4 * 126 * 2**20:
+        return (f"state {nb / 2**30:.1f} GiB per buffer, larger than the 126 MB L2; "
+                "L2 also flushed between timed steps (512 MiB write)")
+    return "flushed between timed steps (512 MiB write)"
+
+
+def workload_config(case, world: int = 1, strong: bool = False, ny_total: int | None = None):
+    """The `config` object of the JSON line: identical in both arms."""
+    ny = ny_total if ny_total is not None else case.meta.get("ny_full", case.ny)
+    wl = case.name
+    if world > 1:
+        wl = f"{case.name} in {world} strips (strong)" if strong else \
+             f"{case.name} x{world} strips (weak)"
+    return {"workload": wl, "kernel": case.kernel, "nx": case.nx, "ny": ny,
+            "limiter": case.limiter, "order": case.order, "cfl": case.cfl, "bc": case.bc,
+            "precision": case.dtype, "l2": l2_note(case, ny)}
 
 
 # ---------------------------------------------------------------------------
@@ -161,17 +224,22 @@ def measured_peak_hbm():
 # ---------------------------------------------------------------------------
 # CPU legs (oracle port, numpy + threads; the reference itself is numpy)
 
-def cpu_rate(case, seconds: float, threads: int, max_steps: int = 10**9):
-    """Time the oracle port on a bounded sample: whole steps of the same
-    workload until `seconds` of CPU work; returns (cell-updates/s, steps)."""
+def _oracle_setup(case, threads):
     from oracle import wavestep_oracle as O
     solver = O.make_solver(case.kernel, **case.kernel_params)
     spec = O.Spec(case.nx, case.ny, case.dx, case.dy)
-    q = np.asfortranarray(case.q.copy())
-    aux = np.asfortranarray(case.aux.copy()) if case.aux is not None else None
+    npdt = np.float64 if case.dtype == "f64" else np.float32
+    q = np.asfortranarray(case.q, dtype=npdt).copy(order="F")
+    aux = np.asfortranarray(case.aux, dtype=npdt).copy(order="F") if case.aux is not None else None
     kw = dict(bc_x=case.bc, bc_y=case.bc, order=case.order, limiter=case.limiter,
               threads=threads)
-    ctl = O.Controller(case.cfl)
+    return O, solver, spec, q, aux, kw, O.Controller(case.cfl)
+
+
+def cpu_rate(case, seconds: float, threads: int, max_steps: int = 10**9):
+    """Time the oracle port on a bounded sample: whole steps of the sample
+    case until `seconds` of CPU work; returns (cell-updates/s, steps, s)."""
+    O, solver, spec, q, aux, kw, ctl = _oracle_setup(case, threads)
     O.step(q, aux, spec, solver, ctl, **kw)      # warm-up step (pool start, caches)
     n, t0 = 0, time.perf_counter()
     while n < max_steps:
@@ -183,49 +251,154 @@ def cpu_rate(case, seconds: float, threads: int, max_steps: int = 10**9):
     return case.nx * case.ny * n / el, n, el
 
 
+# the reference package itself, installed by bench setup into baseline/_ref
+# (pip install --target baseline/_ref /root/reference; it travels with the
+# repo to the GPU box).  It has no shallow-water solver, no limiter and no
+# second order, so its own code path is timed on its closest kernel.
+REF_CLOSEST = {"shallow-water-roe": "euler", "euler-hlle": "euler", "euler": "euler",
+               "acoustics-const": "acoustics-const", "acoustics-var": "acoustics-var",
+               "advection": "advection"}
+
+
+def reference_code_path(sample, budget_s: float = 20.0):
+    """Time the reference's own ``wavesweep.driver.step`` (first order) on the
+    sample band with its three backends through ``for_each_unit`` (reference
+    bench.py:126-147 method: warm-up step, repetitions, median ms/step)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "wavesweep")):
+        return {"unavailable": "reference package not installed in baseline/_ref"}
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import wavesweep
+    from wavesweep import driver as RD
+    from wavesweep.grid import BoundaryCondition, GridSpec, StateField, AuxField
+    from wavesweep.parallel import Serial, StaticThreads, WorkStealing
+    from wavesweep.sweep import CellWise
+    kern = REF_CLOSEST[sample.kernel]
+    ncores = os.cpu_count() or 1
+    g = 2
+    neq = {"euler": 4, "acoustics-const": 3, "acoustics-var": 3, "advection": 1}[kern]
+    naux = 2 if kern == "acoustics-var" else 0
+    # the reference grid needs dx, dy only for dt; the sample's own widths
+    spec = GridSpec(nx=sample.nx, ny=sample.ny, dx=sample.dx, dy=sample.dy, num_eqn=neq,
+                    num_aux=naux)
+    st = StateField(spec)
+    q = sample.q
+    if kern == "euler" and sample.kernel == "shallow-water-roe":
+        # gas at rest with rho = p = h: an admissible Euler state from the band
+        h = q[0]
+        st.data[0] = h
+        st.data[3] = h / 0.4
+        params = {"gamma": 1.4}
+    else:
+        st.data[...] = q[:neq]
+        params = dict(sample.kernel_params)
+        if sample.kernel == "euler-hlle":
+            params = {"gamma": params.get("gamma", 1.4)}
+    aux = None
+    if naux:
+        aux = AuxField(spec)
+        aux.data[...] = sample.aux
+    ext = BoundaryCondition.EXTRAPOLATE
+    ctl = RD.TimestepController(cfl_target=min(sample.cfl, 0.9))
+    out = {"package": f"wavesweep {getattr(wavesweep, '__version__', '')}".strip(),
+           "kernel": kern, "order": 1, "strategy": "cellwise", "cores": ncores,
+           "sample": f"{sample_text(sample)}; "
+                     + ("Euler gas at rest with rho = p = h (closest reference kernel: "
+                        "it has no shallow-water solver)" if kern != sample.kernel
+                        else "the sample's own state"),
+           "backends": {}}
+    per = budget_s / 3.0
+    for name, be in (("serial", Serial()), ("static", StaticThreads(ncores)),
+                     ("workstealing", WorkStealing(ncores))):
+        cfg = RD.SimulationConfig(spec=spec, kernel=kern, ic=RD.DEFAULT_IC[kern],
+                                  strategy=CellWise(), backend=be, bc_x=ext, bc_y=ext,
+                                  num_steps=1, kernel_params=params)
+        s_ = st.copy()
+        a_ = aux.copy() if aux is not None else None
+        t0 = time.perf_counter()
+        RD.step(s_, a_, cfg, ctl)          # warm-up (thread pool start)
+        first = time.perf_counter() - t0
+        ms = []
+        while len(ms) < 3 and (sum(ms) / 1e3 + first) < per:
+            t0 = time.perf_counter()
+            RD.step(s_, a_, cfg, ctl)
+            ms.append((time.perf_counter() - t0) * 1e3)
+        if not ms:
+            ms = [first * 1e3]
+        med = statistics.median(ms)
+        out["backends"][name] = {"ms_per_step": med, "reps": len(ms),
+                                 "value": sample.nx * sample.ny / (med / 1e3)}
+    best = max(out["backends"], key=lambda k: out["backends"][k]["value"])
+    out["best"] = best
+    out["value"] = out["backends"][best]["value"]
+    out["unit"] = UNIT
+    return out
+
+
 def reference_arm(args):
+    """`--impl reference`: the reference path's CPU implementation on the
+    host cores -- the oracle port of the full second-order step (the
+    reference package has neither the solvers nor the limiters of the
+    workload) on the bounded sample, exactly --warmup + --steps time steps;
+    the reference package's own first-order step is timed beside it."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    case = build_case(args.config, precision=args.precision)
+    sample = cpu_sample_case(args.config, precision=args.precision, size=args.size)
     threads = os.cpu_count() or 1
-    from oracle import wavestep_oracle as O
-    solver = O.make_solver(case.kernel, **case.kernel_params)
-    spec = O.Spec(case.nx, case.ny, case.dx, case.dy)
-    q = np.asfortranarray(case.q.copy())
-    aux = np.asfortranarray(case.aux.copy()) if case.aux is not None else None
-    kw = dict(bc_x=case.bc, bc_y=case.bc, order=case.order, limiter=case.limiter,
-              threads=threads)
-    ctl = O.Controller(case.cfl)
+    O, solver, spec, q, aux, kw, ctl = _oracle_setup(sample, threads)
     for _ in range(args.warmup):
         O.step(q, aux, spec, solver, ctl, **kw)
-    # each timed step is one full time step of the workload; K is capped so the
-    # run stays within a few minutes
     k = args.steps
     t0 = time.perf_counter()
-    done = 0
     for _ in range(k):
         O.step(q, aux, spec, solver, ctl, **kw)
-        done += 1
-        if time.perf_counter() - t0 > 120.0:
-            break
     el = time.perf_counter() - t0
-    v = case.nx * case.ny * done / el
+    v = sample.nx * sample.ny * k / el
+    ref_code = None
+    if not args.no_ref_code:
+        try:
+            ref_code = reference_code_path(sample)
+        except Exception as e:  # reported, never fatal for the arm
+            ref_code = {"unavailable": f"{type(e).__name__}: {e}"}
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": done, "warmup": args.warmup, "ms_per_step": el * 1e3 / done,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": case.name, "nx": case.nx, "ny": case.ny,
-                   "limiter": case.limiter, "order": case.order, "cfl": case.cfl,
-                   "parallelism": "cpu-threads"},
+        "steps": k, "warmup": args.warmup, "ms_per_step": el * 1e3 / k,
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None, "dtype": sample.dtype, "data": "synthetic",
+        "config": workload_config(sample, world, args.strong,
+                                  ny_total=sample_ny_total(sample, world, args.strong)),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{done} full time steps of {case.name} "
-                                   f"({case.nx}x{case.ny}) after {args.warmup} warm-up"},
+                         "sample": f"{k} time steps (after {args.warmup} warm-up) of "
+                                   f"{sample_text(sample)}, numpy oracle port of the "
+                                   f"second-order step with {threads} threads",
+                         "reference_code_path": ref_code},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def sample_ny_total(sample, world, strong):
+    ny = sample.meta.get("ny_full", sample.ny)
+    return ny if (strong or world == 1) else ny * world
+
+
+def cpu_baseline_block(case_name, args, precision=None, size=None):
+    """cpu_baseline of the GPU arm's line (rank 0, N = 1)."""
+    sample = cpu_sample_case(case_name, precision=precision, size=size)
+    threads = os.cpu_count() or 1
+    v, n, el = cpu_rate(sample, args.cpu_seconds, threads)
+    out = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"{n} time steps of {sample_text(sample)} in {el:.1f} s, numpy oracle "
+                     f"port of the second-order step with {threads} threads"}
+    if not args.no_ref_code:
+        try:
+            out["reference_code_path"] = reference_code_path(sample)
+        except Exception as e:
+            out["reference_code_path"] = {"unavailable": f"{type(e).__name__}: {e}"}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -413,19 +586,19 @@ def gpu_arm(args):
         e2e = e2e_leg(g, case, host_q, host_aux, ctl, stream, k)
     cpu = None
     if not args.no_cpu:
-        v, n, el = cpu_rate(case, args.cpu_seconds, os.cpu_count() or 1)
-        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-               "sample": f"{n} full time steps of {case.name} ({case.nx}x{case.ny}) "
-                         f"in {el:.1f} s, numpy oracle with {os.cpu_count()} threads"}
+        # free the host copies of the 6 GB state before the CPU sample runs
+        del host_q, host_aux
+        case.q = case.aux = None
+        cpu = cpu_baseline_block(args.config, args, precision=args.precision, size=args.size)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": k,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
-        "config": {"workload": case.name, "kernel": case.kernel, "nx": case.nx,
-                   "ny": case.ny, "limiter": case.limiter, "order": case.order,
-                   "cfl": case.cfl, "bc": case.bc, "parallelism": "single-gpu",
-                   "l2": "flushed between timed steps (512 MiB write)",
-                   "timed_step": "one time step = CFL pre-pass + fused update"},
+        "config": workload_config(case),
+        "measurement": {"parallelism": "single-gpu",
+                        "timed_step": "one time step = CFL pre-pass + fused update",
+                        "scaling_note": "N = 1 is the first point of the weak-scaling curve "
+                                        "(bench.py --gpus N keeps the per-GPU grid)"},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -8,7 +8,8 @@ zero ghosts (reference grid.py:76-95), interior cell (i, j) at
 
 Generation is plain numpy on the host (input preparation, not the hot
 path); the 16384^2 scaling case can instead be generated on the device with
-torch (``device=...``) because a 268 M-cell numpy Gaussian sum takes minutes.
+torch (``device=...``) because a 268 M-cell numpy Gaussian sum takes minutes
+-- from the same numpy 1D factors, so the device field has the host's bits.
 """
 
 from __future__ import annotations
@@ -129,15 +130,13 @@ def c4_var_acoustics(n: int = 8192, seed: int = 0, steps: int = 50) -> Case:
                 steps, "extrapolate", q, aux, meta={"pulse": (x0, y0)})
 
 
-def c5_bumps(nx: int = 16384, ny: int | None = None, seed: int = 0, steps: int = 20,
-             dtype: str = "f64", device=None) -> Case:
-    """configs[4]: h = 1 + sum of 64 Gaussian bumps per unit square, hu = hv = 0.
+def c5_factors(nx: int, ny: int | None = None, seed: int = 0):
+    """The 64-bump recipe's draws and its separable 1D factors (numpy).
 
-    Weak scaling stacks unit squares along y (ny = nx*P, 64*P bumps, bump
-    centres y offset by the square index).  Each bump is separable,
-    exp(-(x-xk)^2/2w^2) * exp(-(y-yk)^2/2w^2), summed bump by bump in draw
-    order.  With ``device`` set the sum runs in torch on that device and
-    the returned Case carries the device tensor in meta["h_dev"] ([j][i], fp64).
+    Returns (amp, ex, ey): ``amp`` (nb,), ``ex`` (nb, nx) = exp(-(x-x_k)^2/2w_k^2),
+    ``ey`` (nb, ny) likewise in y.  Every generator of the C5 field (full grid
+    on the host, a row band on the host, the full grid on the GPU) multiplies
+    these same float64 factors in the same order, so all give the same bits.
     """
     ny = nx if ny is None else ny
     squares = max(1, ny // nx)
@@ -149,27 +148,57 @@ def c5_bumps(nx: int = 16384, ny: int | None = None, seed: int = 0, steps: int =
     dx = 1.0 / nx
     x = (np.arange(nx) + 0.5) * dx
     y = (np.arange(ny) + 0.5) * dx
-    case = Case("C5-shallow-water-scaling", "shallow-water-roe", {"grav": 9.81},
-                nx, ny, dx, dx, "mc", 2, 0.9, steps, "extrapolate", None,
-                dtype=dtype, meta={"squares": squares})
+    two_w2 = 2.0 * wid ** 2
+    ex = np.exp(-((x[None, :] - cen[:, 0:1]) ** 2) / two_w2[:, None])
+    ey = np.exp(-((y[None, :] - cen[:, 1:2]) ** 2) / two_w2[:, None])
+    return amp, ex, ey
+
+
+def c5_h_rows(nx: int, ny: int, j0: int, j1: int, seed: int = 0) -> np.ndarray:
+    """Rows [j0, j1) of the C5 depth, h[i, j - j0] (numpy, bitwise equal to the
+    same rows of the full field: h = 1 + sum_k amp_k (ex_k[i] ey_k[j]), k in
+    draw order)."""
+    amp, ex, ey = c5_factors(nx, ny, seed)
+    h = np.ones((nx, j1 - j0))
+    for k in range(amp.shape[0]):
+        h += amp[k] * np.outer(ex[k], ey[k, j0:j1])
+    return h
+
+
+def c5_bumps(nx: int = 16384, ny: int | None = None, seed: int = 0, steps: int = 20,
+             dtype: str = "f64", device=None, rows: tuple[int, int] | None = None) -> Case:
+    """configs[4]: h = 1 + sum of 64 Gaussian bumps per unit square, hu = hv = 0.
+
+    Weak scaling stacks unit squares along y (ny = nx*P, 64*P bumps, bump
+    centres y offset by the square index).  Each bump is separable,
+    exp(-(x-xk)^2/2w^2) * exp(-(y-yk)^2/2w^2) (stated choice: the product of
+    the two 1D factors), summed bump by bump in draw order.  With ``device``
+    set the sum runs in torch on that device from the same numpy factors (the
+    same IEEE products and sums, so the same bits as the host) and the Case
+    carries the device tensor in meta["h_dev"] ([j][i], fp64).  ``rows=(j0,
+    j1)`` builds only that row band of the field as its own grid (the bounded
+    CPU-baseline sample).
+    """
+    ny = nx if ny is None else ny
+    squares = max(1, ny // nx)
+    dx = 1.0 / nx
+    j0, j1 = rows if rows is not None else (0, ny)
+    name = "C5-shallow-water-scaling"
+    case = Case(name, "shallow-water-roe", {"grav": 9.81},
+                nx, j1 - j0, dx, dx, "mc", 2, 0.9, steps, "extrapolate", None,
+                dtype=dtype, meta={"squares": squares, "rows": (j0, j1), "ny_full": ny})
     if device is None:
-        h = np.ones((nx, ny))
-        for k in range(cen.shape[0]):
-            ex = np.exp(-((x - cen[k, 0]) ** 2) / (2.0 * wid[k] ** 2))
-            ey = np.exp(-((y - cen[k, 1]) ** 2) / (2.0 * wid[k] ** 2))
-            h += amp[k] * np.outer(ex, ey)
-        q = _field(3, nx, ny)
-        q[0, G:G + nx, G:G + ny] = h
+        q = _field(3, nx, j1 - j0)
+        q[0, G:G + nx, G:G + (j1 - j0)] = c5_h_rows(nx, ny, j0, j1, seed)
         case.q = q
     else:
         import torch
-        xt = torch.as_tensor(x, device=device)
-        yt = torch.as_tensor(y, device=device)
-        h = torch.ones((ny, nx), dtype=torch.float64, device=device)  # [j][i]
-        for k in range(cen.shape[0]):
-            ex = torch.exp(-((xt - float(cen[k, 0])) ** 2) / (2.0 * float(wid[k]) ** 2))
-            ey = torch.exp(-((yt - float(cen[k, 1])) ** 2) / (2.0 * float(wid[k]) ** 2))
-            h += float(amp[k]) * torch.outer(ey, ex)
+        amp, ex, ey = c5_factors(nx, ny, seed)
+        ext = torch.as_tensor(ex, device=device)
+        eyt = torch.as_tensor(ey[:, j0:j1], device=device)
+        h = torch.ones((j1 - j0, nx), dtype=torch.float64, device=device)  # [j][i]
+        for k in range(amp.shape[0]):
+            h += float(amp[k]) * torch.outer(eyt[k], ext[k])
         case.meta["h_dev"] = h
     return case
 

@@ -97,3 +97,54 @@ def device_run(name, q, aux, nx, ny, dx, dy, *, steps, order=1, limiter="none",
 def same_bits(a, b):
     """Value equality (the reference's own guard, bench.py:181: np.array_equal)."""
     return np.array_equal(a, b)
+
+
+def case_oracle_run(case, steps, threads=None, dtype=np.float64):
+    """Oracle run of a BASELINE recipe (paper_1308_1464_b200.configs.Case)."""
+    import os
+    q = np.asfortranarray(case.q, dtype=dtype).copy(order="F")
+    aux = (np.asfortranarray(case.aux, dtype=dtype).copy(order="F")
+           if case.aux is not None else None)
+    solver = O.make_solver(case.kernel, **case.kernel_params)
+    spec = O.Spec(case.nx, case.ny, case.dx, case.dy)
+    c = O.Controller(case.cfl)
+    reps = [O.step(q, aux, spec, solver, c, bc_x=case.bc, bc_y=case.bc, order=case.order,
+                   limiter=case.limiter, threads=threads or os.cpu_count() or 1)
+            for _ in range(steps)]
+    return q, reps
+
+
+def case_device_run(case, steps, precision="f64", use_run=True, download=True):
+    """Device run of a BASELINE recipe through the C ABI (DeviceGrid)."""
+    from paper_1308_1464_b200 import DeviceGrid, _abi, make_kernel
+    g = DeviceGrid(case.nx, case.ny, case.dx, case.dy,
+                   make_kernel(case.kernel, **case.kernel_params), order=case.order,
+                   limiter=case.limiter, bc_x=case.bc, bc_y=case.bc, precision=precision)
+    npdt = np.float64 if precision == "f64" else np.float32
+    try:
+        g.upload(np.asfortranarray(case.q, dtype=npdt),
+                 np.asfortranarray(case.aux, dtype=npdt) if case.aux is not None else None)
+        c = _abi.make_ctl(case.cfl)
+        if use_run:
+            g.run(steps, c)
+        else:
+            for _ in range(steps):
+                g.step(c)
+        res = g.poll()
+        out = g.download() if download else None
+        return out, res
+    finally:
+        g.close()
+
+
+def assert_same_run(oq, oreps, dq, res, steps):
+    """Bitwise state and identical dt / cfl / max speeds for every step."""
+    assert res.error.code == 0, res.error
+    assert res.steps_done == steps
+    assert len(res.reports) == steps
+    for k, (r, (dt, cfl, msx, msy)) in enumerate(zip(oreps, res.reports)):
+        assert (r.dt, r.max_speed_x, r.max_speed_y, r.cfl) == (dt, msx, msy, cfl), f"step {k}"
+    if not np.array_equal(oq, dq):
+        d = np.abs(oq - dq)
+        raise AssertionError(f"state differs: max |diff| {d.max():.3e} at "
+                             f"{np.unravel_index(np.argmax(d), d.shape)}")
