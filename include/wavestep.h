@@ -20,7 +20,7 @@
  *   WS_OK (0), WS_ERR_KERNEL (1: inadmissible state, see ws_error_info),
  *   WS_ERR_CONFIG (2: bad descriptor / argument, message in ws_last_error),
  *   WS_ERR_CUDA (3), WS_ERR_STATIONARY (4: all wave speeds zero and no
- *   fixed_dt — reference driver.py:330-331 raises ValueError).
+ *   fixed_dt — reference driver.py:50-51 raises ValueError).
  */
 #ifndef WAVESTEP_H
 #define WAVESTEP_H
@@ -36,14 +36,14 @@ extern "C" {
 enum ws_status { WS_OK = 0, WS_ERR_KERNEL = 1, WS_ERR_CONFIG = 2, WS_ERR_CUDA = 3,
                  WS_ERR_STATIONARY = 4 };
 
-/* Riemann solvers: reference kernels.py:282-287 (DESCRIPTORS) plus the two
+/* Riemann solvers: reference kernels.py:89-94 (DESCRIPTORS) plus the two
  * north-star solvers the reference lacks. */
-enum ws_solver { WS_ACOUSTICS_CONST = 0,   /* kernels.py:374-406, params rho, bulk      */
-                 WS_ACOUSTICS_VAR = 1,     /* kernels.py:409-454, aux (rho, c)          */
-                 WS_EULER_ROE = 2,         /* kernels.py:457-533, params gamma          */
+enum ws_solver { WS_ACOUSTICS_CONST = 0,   /* kernels.py:181-213, params rho, bulk      */
+                 WS_ACOUSTICS_VAR = 1,     /* kernels.py:216-261, aux (rho, c) rp_acoustics_var */
+                 WS_EULER_ROE = 2,         /* kernels.py:264-340, params gamma          */
                  WS_EULER_HLLE = 3,        /* extension, params gamma                   */
                  WS_SHALLOW_ROE = 4,       /* extension (Roe + Harten fix), params grav */
-                 WS_ADVECTION = 5 };       /* kernels.py:356-371, params u, v           */
+                 WS_ADVECTION = 5 };       /* kernels.py:163-178, rp_advection u, v   */
 
 enum ws_limiter { WS_LIM_NONE = 0, WS_LIM_MINMOD = 1, WS_LIM_SUPERBEE = 2, WS_LIM_MC = 3 };
 enum ws_bc { WS_BC_PERIODIC = 0, WS_BC_EXTRAPOLATE = 1 };  /* grid.py:12-16 */
@@ -52,8 +52,8 @@ enum ws_precision { WS_FP64 = 0, WS_FP32 = 1 };
 enum ws_rowmode { WS_ROWS_MEMORY = 0,   /* ghost rows in memory (halo exchange) */
                   WS_ROWS_BC = 1 };     /* physical boundary: apply bc_y         */
 
-/* Replaces GridSpec (grid.py:19-50) + SimulationConfig (driver.py:340-363)
- * + make_kernel (kernels.py:589-633) for one shard. */
+/* Replaces GridSpec (grid.py:19-50) + SimulationConfig (driver.py:60-83)
+ * + make_kernel (kernels.py:396-440) for one shard. */
 typedef struct ws_desc {
   int32_t nx, ny;            /* interior cells of this shard (ny = local rows)      */
   double dx, dy;             /* cell widths                                         */
@@ -75,8 +75,8 @@ typedef struct ws_desc {
   void *ext_q0, *ext_q1, *ext_aux, *ext_slots;
 } ws_desc;
 
-/* Replaces TimestepController (driver.py:297-311) + the `remaining`
- * argument of step() (driver.py:479-481).  NaN = "None". */
+/* Replaces TimestepController (driver.py:17-31) + the `remaining`
+ * argument of step() (driver.py:199-201).  NaN = "None". */
 typedef struct ws_ctl {
   double cfl;        /* cfl_target in (0,1)                   */
   double dt_max;     /* NaN = None                            */
@@ -85,12 +85,12 @@ typedef struct ws_ctl {
   double t_final;    /* NaN = None; device-side run() target  */
 } ws_ctl;
 
-/* Replaces StepReport (driver.py:366-375), minus the wall-clock fields. */
+/* Replaces StepReport (driver.py:86-95), minus the wall-clock fields. */
 typedef struct ws_report {
   double dt, cfl, max_speed_x, max_speed_y;
 } ws_report;
 
-/* Replaces SweepError (sweep.py:68-75) / KernelError (kernels.py:237-248). */
+/* Replaces SweepError (sweep.py:68-75) / KernelError (kernels.py:44-55). */
 typedef struct ws_error_info {
   int32_t code;        /* 0 none, else enum ws_status                          */
   int32_t direction;   /* 0 = x-interface, 1 = y-interface                     */
@@ -141,10 +141,10 @@ int ws_download_async(ws_handle* h, void* q_host, void* stream);
 
 /* One step, enqueued only (no host sync): fill ghosts (implicit, by index
  * mapping) -> sweep -> choose_dt on device -> update.
- * Replaces driver.step (driver.py:479-505). */
+ * Replaces driver.step (driver.py:199-225). */
 int ws_step(ws_handle* h, const ws_ctl* c, void* stream);
 /* nsteps steps through a captured CUDA graph; stops early on error or when
- * t_final is reached.  Replaces driver.run's loop (driver.py:508-530). */
+ * t_final is reached.  Replaces driver.run's loop (driver.py:228-250). */
 int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* stream);
 
 /* Split step for multi-shard runs: the caller all-reduces the 3 x uint64
@@ -176,7 +176,7 @@ int ws_poll(ws_handle* h, int64_t* steps_done, ws_report* reports, int32_t max_r
 int ws_sync(ws_handle* h);
 
 /* Pointwise plugin call, batched: replaces Kernel.solve(direction, ql, qr,
- * auxl, auxr) -> RiemannResult (kernels.py:567-586) for one solver on n
+ * auxl, auxr) -> RiemannResult (kernels.py:374-393) for one solver on n
  * interfaces.  Host arrays, C order: ql/qr (num_eqn, n), aux (num_aux, n)
  * or NULL, waves (num_waves, num_eqn, n), speeds (num_waves, n),
  * amdq/apdq (num_eqn, n), codes (n): 0 admissible, else

@@ -4,7 +4,7 @@ Classical pressure-function root solve (Toro, "Riemann Solvers and Numerical
 Methods for Fluid Dynamics", ch. 4) — the same independent oracle role as
 reference oracles.py:114-250 (exact_riemann_euler_1d), restated here so the
 builder-owned HLLE / limiter extension can be anchored by the Sod L1 check
-(reference oracles.py:495-512 pattern).
+(reference sod_density_l1, oracles.py:495-512 pattern).
 """
 
 from __future__ import annotations

@@ -11,18 +11,18 @@ A numpy restatement of the reference's hot path
 (``/root/reference/pkg/src/wavesweep``, "the reference" below):
 
 * ghost fill ........ grid.py:156-193 (x pass over the full y extent, then y)
-* Riemann kernels ... kernels.py:374-454 (acoustics const/var),
-                      kernels.py:457-533 (Euler Roe, no entropy fix)
-* admissibility ..... kernels.py:331-349 (finite first, then positivity,
-                      left before right), floor 1e-300 (kernels.py:227)
+* Riemann kernels ... kernels.py:181-261 (acoustics const/var),
+                      kernels.py:264-340 (Euler Roe, no entropy fix)
+* admissibility ..... kernels.py:138-156 (finite first, then positivity,
+                      left before right), ADMISSIBILITY_FLOOR 1e-300 (kernels.py:34)
 * sweep ............. sweep.py:111-163 (x-edge i between cells i-1,i for
                       j in [0,ny); y-edge j between rows j-1,j for i in
                       [0,nx)); max |s| over exactly that edge set
-* error location .... sweep.py:166-168, 203-243 (CellWise/Serial order:
+* error location .... _locate, sweep.py:166-168, 203-243 (CellWise/Serial order:
                       all x chunks of MAX_BLOCK//width rows, then y)
-* choose_dt ......... driver.py:314-337
+* choose_dt ......... driver.py:34-57
 * donor-cell update . sweep.py:254-280 (x term then y term, fixed order)
-* step / run ........ driver.py:479-530
+* step / run ........ driver.py:199-250
 
 Every arithmetic expression keeps numpy's left-to-right association of the
 reference so that ``order=1`` is BITWISE identical to ``wavesweep.driver.step``
@@ -52,8 +52,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-FLOOR = 1e-300          # reference kernels.py:227 (ADMISSIBILITY_FLOOR)
-MAX_BLOCK = 1 << 15     # reference sweep.py:30 — only used to order errors
+FLOOR = 1e-300          # reference kernels.py:34 (ADMISSIBILITY_FLOOR)
+MAX_BLOCK = 1 << 15     # reference _MAX_BLOCK, sweep.py:30 — only used to order errors
 PERIODIC = "periodic"
 EXTRAPOLATE = "extrapolate"
 LIMITERS = ("none", "minmod", "superbee", "mc")
@@ -119,14 +119,14 @@ def fill_ghost(a: np.ndarray, bc_x: str, bc_y: str, g: int = 2):
 
 
 def _finite_checks(ql, qr):
-    # kernels.py:338-341: left then right; element = first bad in C order
+    # kernels.py:145-148: left then right; element = first bad in C order
     # over (component, batch...) — i.e. the lowest component wins
     return [("non-finite left state", "left", ~np.isfinite(ql), True),
             ("non-finite right state", "right", ~np.isfinite(qr), True)]
 
 
 def _pos(arr, what, side):
-    # kernels.py:345-349
+    # kernels.py:152-156
     return (f"nonpositive {what} on {side} side", side, ~(arr > FLOOR), False)
 
 
@@ -148,7 +148,7 @@ class Solver:
 
 
 def rp_advection(ni, ql, qr, auxl, auxr, p):
-    """kernels.py:356-371 — one wave qr-ql at u (x) or v (y)."""
+    """kernels.py:163-178 — one wave qr-ql at u (x) or v (y)."""
     sp = p["u"] if ni == 1 else p["v"]
     jump = qr - ql
     w = jump[np.newaxis]
@@ -161,13 +161,13 @@ def _chk_advection(ni, ql, qr, auxl, auxr, p):
 
 
 def acoustics_const_params(rho: float, bulk: float) -> dict:
-    # kernels.py:305-311: c = sqrt(K/rho), Z = rho*c (Python floats)
+    # kernels.py:112-118: c = sqrt(K/rho), Z = rho*c (Python floats)
     c = math.sqrt(bulk / rho)
     return {"c": c, "z": rho * c}
 
 
 def rp_acoustics_const(ni, ql, qr, auxl, auxr, p):
-    """kernels.py:374-406."""
+    """kernels.py:181-213."""
     z, c = p["z"], p["c"]
     dp = qr[0] - ql[0]
     dn = qr[ni] - ql[ni]
@@ -189,7 +189,7 @@ def _chk_acoustics_const(ni, ql, qr, auxl, auxr, p):
 
 
 def rp_acoustics_var(ni, ql, qr, auxl, auxr, p):
-    """kernels.py:409-454 — aux = (rho, c) per cell."""
+    """kernels.py:216-261 — aux = (rho, c) per cell."""
     zl = auxl[0] * auxl[1]
     zr = auxr[0] * auxr[1]
     cl, cr = auxl[1], auxr[1]
@@ -210,7 +210,7 @@ def rp_acoustics_var(ni, ql, qr, auxl, auxr, p):
 
 
 def _chk_acoustics_var(ni, ql, qr, auxl, auxr, p):
-    # kernels.py:428-430: for each side: density then sound speed
+    # kernels.py:235-237: for each side: density then sound speed
     return _finite_checks(ql, qr) + [
         _pos(auxl[0], "density", "left"), _pos(auxl[1], "sound speed", "left"),
         _pos(auxr[0], "density", "right"), _pos(auxr[1], "sound speed", "right")]
@@ -225,7 +225,7 @@ def _gas_primitives(q, ni, ti, gm1):
 
 
 def rp_euler_roe(ni, ql, qr, auxl, auxr, p):
-    """kernels.py:457-533 — Roe, three waves, no entropy fix."""
+    """kernels.py:264-340 — Roe, three waves, no entropy fix."""
     gm1 = p["gamma"] - 1.0
     ti = 3 - ni
     rl, ul, vl, pl = _gas_primitives(ql, ni, ti, gm1)
@@ -286,7 +286,7 @@ def _roe_c2(ni, ql, qr, gm1):
 
 
 def _chk_gas(ni, ql, qr, auxl, auxr, p):
-    # kernels.py:467-494: finite, density L/R, pressure L/R, Roe c^2 > 0
+    # kernels.py:274-301: finite, density L/R, pressure L/R, Roe c^2 > 0
     gm1 = p["gamma"] - 1.0
     c2, (pl, pr) = _roe_c2(ni, ql, qr, gm1)
     return _finite_checks(ql, qr) + [
@@ -299,8 +299,8 @@ def rp_euler_hlle(ni, ql, qr, auxl, auxr, p):
     """Euler HLLE (Einfeldt 1988): two waves bounding the Riemann fan.
 
     Builder-owned formula (no reference counterpart):
-      per side: u_n, u_t, p as reference kernels.py:475-478, c = sqrt(g p/rho)
-      Roe averages u^, c^ as reference kernels.py:482-495
+      per side: u_n, u_t, p (u_l, v_l, p_l) as reference kernels.py:282-285, c = sqrt(g p/rho)
+      Roe averages u^, c^ as reference kernels.py:289-302
       s1 = min(u_l - c_l, u^ - c^),  s2 = max(u_r + c_r, u^ + c^)
       with df = f(q_r) - f(q_l), dq = q_r - q_l and the middle state
       q_m = (df - s2 q_r + s1 q_l) / (s1 - s2):
@@ -326,7 +326,7 @@ def rp_euler_hlle(ni, ql, qr, auxl, auxr, p):
     ch = np.sqrt(c2)
     s1 = np.minimum(ul - cl, uh - ch)
     s2 = np.maximum(ur + cr, uh + ch)
-    # physical fluxes (normal/transverse slots as reference kernels.py:559-563)
+    # physical fluxes (normal/transverse slots as reference kernels.py:366-370)
     fl = np.empty_like(ql)
     fr = np.empty_like(qr)
     for f, q, u, pp in ((fl, ql, ul, pl), (fr, qr, ur, pr)):
@@ -579,7 +579,7 @@ def _collect(checks, dir_idx, width, i_of, j_of):
 
     Chunks of MAX_BLOCK//width rows (sweep.py:117-120); inside a chunk the
     kernel's check order (stage), then first bad in C order over
-    (component, i, j) (kernels.py:325-328).
+    (component, i, j) (_first_bad, kernels.py:132-135).
     """
     rows_per = max(1, MAX_BLOCK // width)
     out = []
@@ -667,7 +667,7 @@ def _update_band(q, spec: Spec, r: _BandResult, dt: float, order: int, limiter: 
 
 @dataclass
 class Controller:
-    """reference driver.py:297-311 (TimestepController)."""
+    """reference driver.py:17-31 (TimestepController)."""
 
     cfl: float = 0.9
     dt_max: float | None = None
@@ -675,7 +675,7 @@ class Controller:
 
 
 def choose_dt(msx, msy, dx, dy, ctl: Controller, remaining=None) -> float:
-    """reference driver.py:314-337, same operation order."""
+    """reference driver.py:34-57, same operation order."""
     if ctl.fixed_dt is not None:
         dt = ctl.fixed_dt
     else:
@@ -718,7 +718,7 @@ def _bands(ny, nb):
 def step(q, aux, spec: Spec, solver: Solver, ctl: Controller, *,
          bc_x=EXTRAPOLATE, bc_y=EXTRAPOLATE, order=1, limiter="none",
          remaining=None, threads=1) -> Report:
-    """One ghost-fill / sweep / choose-dt / update cycle (driver.py:479-505).
+    """One ghost-fill / sweep / choose-dt / update cycle (driver.py:199-225).
 
     Mutates q.  order=1 reproduces the reference step bitwise; order=2 adds
     the limited correction flux.  threads>1 splits rows into bands executed
@@ -754,7 +754,7 @@ def step(q, aux, spec: Spec, solver: Solver, ctl: Controller, *,
 
 
 def run(q, aux, spec, solver, ctl, *, num_steps=None, t_final=None, **kw):
-    """reference driver.py:508-530 loop (num_steps, or t_final with the
+    """reference driver.py:228-250 loop (num_steps, or t_final with the
     1e-14*max(1, t_final) tolerance)."""
     reps = []
     if num_steps is not None:

@@ -19,7 +19,7 @@ the ``cuda`` row; ``threads`` is the GPU count (1: one process drives one
 GPU; multi-GPU rows come from ``bench.py --gpus N`` under torchrun).
 
 The CSV is byte-for-byte the reference's eleven-column format, so the
-reference's own ``parse_csv`` (bench.py:236-270) reads it back.  The roofline
+reference's own ``parse_csv`` (bench.py:236-264) reads it back.  The roofline
 columns (algorithmic bytes per cell-update = q read + aux read + q written,
 achieved GB/s, fraction of the measured HBM peak from MEASURED_PEAKS.json)
 go to a sidecar file (``--roofline-out``, :func:`emit_roofline_csv`).
@@ -289,7 +289,7 @@ def emit_roofline_csv(records: list[BenchRecord], out=None) -> None:
 
 
 def parse_csv(source) -> list[BenchRecord]:
-    """Reference parse_csv (bench.py:236-270): header and eleven fields checked."""
+    """Reference parse_csv (bench.py:236-264): header and eleven fields checked."""
     fh, own = (source, False) if hasattr(source, "read") else (
         open(source, "r", encoding="utf-8"), True)
     try:

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-G = 2  # ghost layers (reference grid.py:36)
+G = 2  # ghost layers (reference num_ghost, grid.py:36)
 
 
 @dataclass

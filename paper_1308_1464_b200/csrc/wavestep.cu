@@ -33,7 +33,7 @@ template <class R> bool bind(ws_handle* h, std::string& msg) {
   const double* p = d.params;
   switch (d.solver) {
     case WS_ACOUSTICS_CONST: {
-      // reference kernels.py:299-311: both positive; c = sqrt(K/rho), Z = rho*c
+      // reference kernels.py:106-118: both positive; c = sqrt(K/rho), Z = rho*c
       if (!(p[0] > 0 && p[1] > 0)) {
         char b[160];
         snprintf(b, sizeof b, "density and bulk modulus must be positive, got %.17g, %.17g",
@@ -78,7 +78,7 @@ template <class R> bool bind(ws_handle* h, std::string& msg) {
       return true;
     }
     case WS_ADVECTION: {
-      // reference kernels.py:362-363: non-finite velocity is a KernelError
+      // reference kernels.py:169-170: non-finite velocity is a KernelError
       if (!(std::isfinite(p[0]) && std::isfinite(p[1]))) {
         char b[128];
         snprintf(b, sizeof b, "non-finite advection velocity (%.17g, %.17g)", p[0], p[1]);
@@ -142,7 +142,7 @@ int validate(const ws_desc* d, std::string& m) {
   if (d->precision != WS_FP64 && d->precision != WS_FP32) {
     m = "unknown precision"; return WS_ERR_CONFIG;
   }
-  // reference grid.py:165-169
+  // reference grid.py:165-169 (PERIODIC needs n >= num_ghost)
   if (d->bc_x == WS_BC_PERIODIC && d->nx < 2) {
     snprintf(b, sizeof b, "periodic boundary needs at least num_ghost=2 interior cells, got %d",
              d->nx);
@@ -197,7 +197,7 @@ StepArgs make_args(ws_handle* h, const ws_ctl* c, int cur) {
   a.has_fixed = !std::isnan(c->fixed_dt); a.fixed_dt = c->fixed_dt;
   a.has_remaining = !std::isnan(c->remaining); a.remaining = c->remaining;
   a.has_t_final = !std::isnan(c->t_final); a.t_final = c->t_final;
-  a.tol = a.has_t_final ? 1e-14 * std::fmax(1.0, c->t_final) : 0.0;   // driver.py:525
+  a.tol = a.has_t_final ? 1e-14 * std::fmax(1.0, c->t_final) : 0.0;   // driver.py:245
   a.cur = cur;
   a.seq = h->enq;
   a.static_speeds = (h->ops.static_speeds && !h->multi) ? 1 : 0;
@@ -207,7 +207,7 @@ StepArgs make_args(ws_handle* h, const ws_ctl* c, int cur) {
 }
 
 int check_ctl(ws_handle* h, const ws_ctl* c) {
-  // reference driver.py:305-311
+  // reference TimestepController.__post_init__, driver.py:25-31
   char b[128];
   if (!(c->cfl > 0.0 && c->cfl < 1.0)) {
     snprintf(b, sizeof b, "cfl_target must lie in (0, 1), got %.17g", c->cfl);

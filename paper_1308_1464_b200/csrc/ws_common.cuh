@@ -152,7 +152,7 @@ __device__ __forceinline__ long long row_off(int j, const Layout& L) {
 // Error key: ordering of reference CellWise/Serial sweeps (sweep.py:203-218):
 // all x chunks, then y; chunk = MAX_BLOCK // width rows (sweep.py:117-119);
 // inside a chunk the kernel's admissibility stage, then the first bad element
-// in C order over (component, i, j) (kernels.py:325-328).  63 bits, so the
+// in C order over (component, i, j) (_first_bad, kernels.py:132-135).  63 bits, so the
 // reduction slot stores NKEY_MAX - key >= 0 and one int64/u64 MAX all-reduce
 // across shards picks the smallest key.
 constexpr unsigned long long NKEY_MAX = 0x7fffffffffffffffull;
@@ -190,7 +190,7 @@ template <class R> __device__ __forceinline__ R nmin(R a, R b) { return (a <= b)
 template <class R> __device__ __forceinline__ R nmax(R a, R b) { return (a >= b) ? a : b; }
 
 // Step control computed identically by every CTA: dt from this step's max
-// speeds exactly as reference choose_dt (driver.py:314-337), all in fp64.
+// speeds exactly as reference choose_dt (driver.py:34-57), all in fp64.
 struct Ctl {
   double dt, msx, msy;
   int skip;        // 1: do nothing (sticky error, pending error, or t_final reached)

@@ -1,7 +1,7 @@
 // ws_kernels.cuh — the step kernels.
 //
 //   k_speeds  : CFL pre-pass.  Every reference edge (x: i in [0,nx], j in
-//               [0,ny); y: i in [0,nx), j in [0,ny], sweep.py:111-163, 250)
+//               [0,ny); y: i in [0,nx), j in [0,ny], solve_x / solve_y, sweep.py:111-163, 250)
 //               is probed: admissibility in the reference order and max |s|,
 //               reduced warp-shuffle -> block -> one atomicMax per CTA.
 //   k_update  : fused edge + update kernel.  One CTA owns a TX x TY tile; the
@@ -9,7 +9,7 @@
 //               per-cell primitives are computed once per cell, every edge
 //               is solved once per tile, waves are limited against their
 //               upwind neighbour, and the donor-cell update (reference order,
-//               sweep.py:275-277) plus the correction flux are applied in
+//               apply_update cells -= ..., sweep.py:275-277) plus the correction flux are applied in
 //               registers.  No fluctuation arrays ever reach HBM.  The last
 //               CTA to finish commits the step (report, t, counters).
 //   k_to_soa / k_to_aos / k_static_speed : layout conversion, acoustics setup.
@@ -979,7 +979,7 @@ __device__ __forceinline__ void commit_step(DevState* ds, const StepArgs& A, con
       long long n = v->nrep;
       Report r;
       r.dt = c.dt;
-      r.cfl = c.dt * (c.msx / A.dx + c.msy / A.dy);   // driver.py:501
+      r.cfl = c.dt * (c.msx / A.dx + c.msy / A.dy);   // cfl, driver.py:221
       r.msx = c.msx; r.msy = c.msy;
       ds->rep[n % REPCAP] = r;
       v->nrep = n + 1;

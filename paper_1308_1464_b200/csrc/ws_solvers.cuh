@@ -1,11 +1,11 @@
 // ws_solvers.cuh — pointwise Riemann solvers as parallelism-unaware device
 // plugins (the paper's decoupling goal; reference plugin
-// contract kernels.py:567-586).
+// contract: class Kernel, kernels.py:374-393).
 //
 // A solver is a struct with
 //   NEQ, NW, NAUX, NPR           components, waves, aux fields, per-cell primitives
 //   STATIC_SPEEDS                speeds independent of q (acoustics)
-//   Params<R>                    bound parameters (reference make_kernel, kernels.py:589-633)
+//   Params<R>                    bound parameters (reference make_kernel, kernels.py:396-440)
 //   prims<M>(q, aux, P, pr, ok)  per-cell quantities shared by the 4 edges of a cell
 //   solve<NI,M>(ql,qr,pl,pr,al,ar,P,W,s,amdq,apdq,ok)  one edge, NI = normal slot (1=x, 2=y)
 //   probe<NI,M>(...,smax,ok) -> code  admissibility tests in the reference order and
@@ -25,7 +25,7 @@
 
 namespace ws {
 
-constexpr double FLOOR = 1e-300;  // reference kernels.py:227
+constexpr double FLOOR = 1e-300;  // reference ADMISSIBILITY_FLOOR, kernels.py:34
 
 // code = (stage + 1) | (component << 8); 0 = admissible
 template <class R, int N>
@@ -54,7 +54,7 @@ template <> __device__ __forceinline__ double floor_v<double>() { return FLOOR; 
 template <class R> __device__ __forceinline__ bool bad_pos(R v) { return !(v > floor_v<R>()); }
 
 // ---------------------------------------------------------------------------
-// constant-coefficient acoustics — reference kernels.py:374-406
+// constant-coefficient acoustics — reference kernels.py:181-213
 struct AcousticsConst {
   static constexpr int NEQ = 3, NW = 2, NAUX = 0, NPR = 0;
   static constexpr bool STATIC_SPEEDS = true;
@@ -105,7 +105,7 @@ struct AcousticsConst {
 };
 
 // ---------------------------------------------------------------------------
-// variable-coefficient acoustics, aux = (rho, c) — reference kernels.py:409-454
+// variable-coefficient acoustics, aux = (rho, c) — reference kernels.py:216-261
 struct AcousticsVar {
   static constexpr int NEQ = 3, NW = 2, NAUX = 2, NPR = 1;  // pr[0] = Z = rho*c
   static constexpr bool STATIC_SPEEDS = true;
@@ -144,7 +144,7 @@ struct AcousticsVar {
     smax = nmax(al[1], ar[1]);
     int c = finite_code<R, NEQ>(ql, qr);
     if (c) return c;
-    // kernels.py:428-430: per side density then sound speed, left first
+    // kernels.py:235-237: per side density then sound speed, left first
     if (bad_pos(al[0])) return 3;
     if (bad_pos(al[1])) return 4;
     if (bad_pos(ar[0])) return 5;
@@ -166,7 +166,7 @@ struct AcousticsVar {
 };
 
 // ---------------------------------------------------------------------------
-// ideal gas, shared per-cell primitives (reference kernels.py:475-478, 482, 487)
+// ideal gas, shared per-cell primitives (reference rp_euler u_l, p_l, sq_l: kernels.py:282-285, 289, 294)
 //   pr = {u = q1/rho, v = q2/rho, p, sqrt(rho), sqrt(rho)*(E+p)/rho [, c]}
 // p uses (u*u + v*v); the y sweep's (v*v + u*u) is the same IEEE sum.
 template <class M, class R, class P>
@@ -254,7 +254,7 @@ struct GasTile {
   }
 };
 
-// Euler, Roe linearisation, no entropy fix — reference kernels.py:457-533
+// Euler, Roe linearisation, no entropy fix — reference kernels.py:264-340
 struct EulerRoe {
   static constexpr int NEQ = 4, NW = 3, NAUX = 0, NPR = 5;
   static constexpr bool STATIC_SPEEDS = false;
@@ -605,7 +605,7 @@ struct ShallowRoe {
 };
 
 // ---------------------------------------------------------------------------
-// scalar advection with constant velocity (u, v) — reference kernels.py:356-371
+// scalar advection with constant velocity (u, v) — reference kernels.py:163-178
 //   one wave W = qr - ql at s = u (x) or v (y); amdq = min(s,0) W, apdq = max(s,0) W
 //   with Python's min/max on floats: min(s, 0.0) = 0.0 if 0.0 < s else s
 struct Advection {

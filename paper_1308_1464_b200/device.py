@@ -4,7 +4,7 @@
 (driver.step/run, the row-strip orchestrator in parallel.py, bench.py).
 It owns the handle, converts host arrays to the C ABI's expectations and
 maps device error records to the reference's exception types
-(SweepError / ValueError, reference sweep.py:68-75, driver.py:330-331).
+(SweepError / ValueError, reference sweep.py:68-75, driver.py:50-51).
 """
 
 from __future__ import annotations

@@ -4,7 +4,7 @@ The physics lives in CUDA device-function templates (csrc/ws_solvers.cuh)
 that know nothing of tiles or threads.  This module is their host-side
 registry: descriptors, parameter binding (``make_kernel``) and
 ``Kernel.solve`` — the reference's batched pointwise plugin call
-(kernels.py:567-586) — executed on the GPU through ``ws_riemann``.
+(kernels.py:374-393) — executed on the GPU through ``ws_riemann``.
 """
 
 from __future__ import annotations
@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _abi
 
-ADMISSIBILITY_FLOOR = 1e-300  # reference kernels.py:227
+ADMISSIBILITY_FLOOR = 1e-300  # reference kernels.py:34
 
 
 class Direction(enum.Enum):
@@ -28,7 +28,7 @@ class Direction(enum.Enum):
 
 
 class KernelError(ValueError):
-    """Inadmissible kernel input (reference kernels.py:237-248)."""
+    """Inadmissible kernel input (reference kernels.py:44-55)."""
 
     def __init__(self, message: str, side: str | None = None, element: tuple | None = None):
         super().__init__(message)
@@ -53,7 +53,7 @@ class KernelDescriptor:
     arithmetic_intensity: Fraction
 
 
-# reference kernels.py:282-287 plus the two north-star solvers the reference lacks
+# reference kernels.py:89-94 plus the two north-star solvers the reference lacks
 DESCRIPTORS: dict[str, KernelDescriptor] = {
     "advection": KernelDescriptor("advection", 1, 1, 0, Fraction(1, 3)),
     "acoustics-const": KernelDescriptor("acoustics-const", 3, 2, 0, Fraction(4, 5)),
@@ -65,7 +65,7 @@ DESCRIPTORS: dict[str, KernelDescriptor] = {
 KERNEL_NAMES = tuple(DESCRIPTORS)
 
 # reason text per admissibility stage, in the order the device tests them
-# (reference kernels.py:338-349, 428-430, 473-494)
+# (reference _check_states / _check_positive, kernels.py:145-156, 235-237, 280-301)
 _FINITE = [("non-finite left state", "left"), ("non-finite right state", "right")]
 STAGES = {
     "advection": _FINITE,
@@ -209,7 +209,7 @@ class Kernel:
 
 
 def make_kernel(name: str, **params) -> Kernel:
-    """Bind a solver to parameters (reference kernels.py:589-633).
+    """Bind a solver to parameters (reference kernels.py:396-440).
 
     advection(u, v), acoustics-const(rho, bulk), acoustics-var() reading per-cell (rho, c)
     from aux, euler(gamma=1.4), euler-hlle(gamma=1.4),

@@ -1,4 +1,4 @@
-"""Bench matrix in the reference CSV format (reference bench.py:28-29,
+"""Bench matrix in the reference CSV format (reference CSV_HEADER bench.py:28-29,
 :43-80, :191-234): config validation and the CSV writer on CPU; one tiny
 matrix with the bitwise twin guard on the GPU."""
 
@@ -34,7 +34,7 @@ def test_csv_is_exactly_the_reference_format():
 
 
 def test_csv_round_trips_through_the_reference_parser():
-    # the reference's own reader (bench.py:236-270) accepts our file
+    # the reference's own reader (bench.py:236-264) accepts our file
     import sys
     src = "/root/reference/pkg/src"
     import os

@@ -354,7 +354,7 @@ def test_persistent_line_kernel_walks_tiles_bitwise(name, bc):
 def test_run_to_t_final_matches_oracle(name, order, limiter):
     # device-resident run with the t_final truncation decided on the GPU
     # (remaining = t_final - t, tolerance 1e-14 max(1, t_final), reference
-    # driver.py:508-530): same number of steps, same dts (the last one
+    # driver.py:228-250): same number of steps, same dts (the last one
     # truncated), same state; the graph path is used (> 4 steps)
     from paper_1308_1464_b200 import _abi
     from helpers import device_grid
