@@ -139,6 +139,21 @@ int ws_download_f32(ws_handle* h, float* q_host, void* stream);
  * the host array). */
 int ws_download_async(ws_handle* h, void* q_host, void* stream);
 
+/* The BC ghost frame of the aux the last ws_upload carried, filled like the
+ * reference's fill_ghost (grid.py:179-193) from its interior, written into
+ * the ghost frame of the host aux array (reference layout); the interior is
+ * left untouched.  The reference's step refills the caller's aux ghosts
+ * every step (driver.py:211-212); this is that mutation.  Synchronous.
+ * No-op for solvers without aux. */
+int ws_download_aux_ghosts(ws_handle* h, void* aux_host, void* stream);
+
+/* Page-lock (cudaHostRegister, portable) / release a caller's host array so
+ * ws_upload / ws_download copy it by DMA at full PCIe rate.  The drop-in
+ * driver.step pins the caller's StateField / AuxField arrays once per array
+ * (the reference's step mutates them in place, driver.py:199-225). */
+int ws_pin_host(void* ptr, uint64_t bytes);
+int ws_unpin_host(void* ptr);
+
 /* One step, enqueued only (no host sync): fill ghosts (implicit, by index
  * mapping) -> sweep -> choose_dt on device -> update.
  * Replaces driver.step (driver.py:199-225). */

@@ -80,6 +80,9 @@ SIGNATURES = [
     ("ws_step", C.c_int, [_P, C.POINTER(WsCtl), _P]),
     ("ws_run", C.c_int, [_P, C.c_int32, C.POINTER(WsCtl), _P]),
     ("ws_download_async", C.c_int, [_P, _P, _P]),
+    ("ws_download_aux_ghosts", C.c_int, [_P, _P, _P]),
+    ("ws_pin_host", C.c_int, [_P, C.c_uint64]),
+    ("ws_unpin_host", C.c_int, [_P]),
     ("ws_phase_speeds", C.c_int, [_P, _P]),
     ("ws_phase_speeds_part", C.c_int, [_P, C.c_int32, _P]),
     ("ws_phase_update", C.c_int, [_P, C.POINTER(WsCtl), _P]),

@@ -367,6 +367,7 @@ void ws_destroy(ws_handle* h) {
   if (h->own_ds && h->ds) cudaFree(h->ds);
   for (int k = 0; k < 2; ++k) if (h->stage[k]) cudaFree(h->stage[k]);
   if (h->stage_out) cudaFree(h->stage_out);
+  if (h->stage_aux) cudaFree(h->stage_aux);
   if (h->peers_dev) cudaFree(h->peers_dev);
   if (h->ev_order) cudaEventDestroy(h->ev_order);
   for (int k = 0; k < 2; ++k) {
@@ -543,6 +544,47 @@ static int tfinal_guard(ws_handle* h, const ws_ctl* c, cudaStream_t st) {
   }
   h->tf_pending = tf;
   h->tf_value = tf ? c->t_final : 0.0;
+  return WS_OK;
+}
+
+int ws_download_aux_ghosts(ws_handle* h, void* ah, void* s) {
+  if (!h || !ah) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (h->naux == 0) return WS_OK;
+  if (!h->uploaded) return fail(h, WS_ERR_CONFIG, "no state uploaded");
+  cudaStream_t st = pick(h, s);
+  const long long nxt = h->d.nx + 4, nyt = h->d.ny + 4;
+  const size_t es = h->esz, na = (size_t)h->naux;
+  int rc = ensure_buf(h, &h->stage_aux, &h->stage_aux_bytes, (size_t)(nxt * nyt) * na * es);
+  if (rc) return rc;
+  h->ops.to_aos_aux(h, h->stage_aux, st);
+  char* hd = static_cast<char*>(ah);
+  const char* sd = static_cast<const char*>(h->stage_aux);
+  const size_t row = (size_t)nxt * na * es;           // one j of the host layout
+  // rows j = 0, 1 and j = ny+2, ny+3: contiguous
+  WS_CUDA(h, cudaMemcpyAsync(hd, sd, 2 * row, cudaMemcpyDeviceToHost, st));
+  const size_t top = (size_t)(nyt - 2) * row;
+  WS_CUDA(h, cudaMemcpyAsync(hd + top, sd + top, 2 * row, cudaMemcpyDeviceToHost, st));
+  // columns i = 0, 1 and i = nx+2, nx+3 of the interior rows: strided
+  const size_t lo = 2 * row, hi = 2 * row + (size_t)(nxt - 2) * na * es;
+  WS_CUDA(h, cudaMemcpy2DAsync(hd + lo, row, sd + lo, row, 2 * na * es, (size_t)h->d.ny,
+                               cudaMemcpyDeviceToHost, st));
+  WS_CUDA(h, cudaMemcpy2DAsync(hd + hi, row, sd + hi, row, 2 * na * es, (size_t)h->d.ny,
+                               cudaMemcpyDeviceToHost, st));
+  WS_CUDA(h, cudaStreamSynchronize(st));
+  return WS_OK;
+}
+
+int ws_pin_host(void* p, uint64_t bytes) {
+  if (!p || bytes == 0) return fail(nullptr, WS_ERR_CONFIG, "null or empty host range");
+  cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e)); }
+  return WS_OK;
+}
+
+int ws_unpin_host(void* p) {
+  if (!p) return fail(nullptr, WS_ERR_CONFIG, "null host pointer");
+  cudaError_t e = cudaHostUnregister(p);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e)); }
   return WS_OK;
 }
 

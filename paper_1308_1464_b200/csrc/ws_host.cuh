@@ -38,6 +38,7 @@ struct Ops {
   void (*update)(ws_handle*, const void* q, void* qn, const StepArgs&, cudaStream_t);
   void (*to_soa)(ws_handle*, const void* stage, void* dst, int ncomp, cudaStream_t);
   void (*to_aos)(ws_handle*, const void* cur, const void* gsrc, void* stage, cudaStream_t);
+  void (*to_aos_aux)(ws_handle*, void* stage, cudaStream_t);   // aux + BC ghost frame
   void (*static_speed)(ws_handle*, cudaStream_t);
   void (*prepare)();   // one-time kernel attributes (never inside a capture)
   int static_speeds;   // solver has q-independent speeds
@@ -63,6 +64,8 @@ struct ws_handle {
   int up_idx = 0;                        // staging buffer of the next upload
   void* stage_out = nullptr;     // download staging: a download and the next upload overlap
   size_t stage_out_bytes = 0;
+  void* stage_aux = nullptr;     // aux in the host layout with its BC ghost frame
+  size_t stage_aux_bytes = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t cstream = nullptr;  // upload H2D copies (staging only)
   cudaStream_t last_stream = nullptr;
@@ -347,6 +350,14 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     h->launches++;
   }
 
+  static void to_aos_aux(ws_handle* h, void* stage, cudaStream_t st) {
+    Layout La = h->L;
+    La.rstride = h->L.astride;     // aux rows: naux component rows per j
+    const R* a = static_cast<const R*>(h->aux);
+    k_to_aos<R, R><<<148 * 8, 256, 0, st>>>(a, a, static_cast<R*>(stage), La, h->naux);
+    h->launches++;
+  }
+
   static void static_speed(ws_handle* h, cudaStream_t st) {
     if (S::NAUX > 0) {
       k_static_speed<R><<<148 * 4, 256, 0, st>>>(static_cast<const R*>(h->aux), h->L, h->ds);
@@ -360,6 +371,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     o.update = &update;
     o.to_soa = &to_soa;
     o.to_aos = &to_aos;
+    o.to_aos_aux = &to_aos_aux;
     o.static_speed = &static_speed;
     o.prepare = &prepare;
     o.static_speeds = S::STATIC_SPEEDS ? 1 : 0;

@@ -151,6 +151,17 @@ class DeviceGrid:
             return out
         return buf
 
+    def download_aux_ghosts(self, aux: np.ndarray) -> np.ndarray:
+        """Write the BC ghost frame of the uploaded aux into ``aux``'s ghost
+        frame in place (ws_download_aux_ghosts; reference fill_ghost of aux
+        in driver.py:211-212).  ``aux`` must be the handle's precision, F-order."""
+        shape = self.host_shape(self.desc.num_aux)
+        if aux.shape != shape or aux.dtype != self.dtype or not aux.flags.f_contiguous:
+            raise ValueError(f"aux ghosts need a Fortran-ordered {shape} "
+                             f"{np.dtype(self.dtype).name} array")
+        self._check(self.lib.ws_download_aux_ghosts(self.h, aux.ctypes.data, None))
+        return aux
+
     # -- stepping ---------------------------------------------------------------
     def step(self, ctl: _abi.WsCtl, stream=None):
         self._check(self.lib.ws_step(self.h, ctypes.byref(ctl), stream))

@@ -148,3 +148,23 @@ def test_order2_without_limiter_reduces_to_reference(W):
         O.step(oq, None, O.Spec(20, 17, 0.05, 0.05), O.make_solver("euler"),
                O.Controller(0.9), order=2, limiter="none")
     assert np.array_equal(st.data, oq)
+
+
+FILL = json.load(open(os.path.join(HERE, "golden", "fill_ghost_golden.json")))
+
+
+def _fill_case(c):
+    shape = (c["ncomp"], c["nx"] + 4, c["ny"] + 4)
+    before = np.array(c["before"]).reshape(shape, order="F")
+    after = np.array(c["after"]).reshape(shape, order="F")
+    return before, after
+
+
+@pytest.mark.parametrize("k", range(len(FILL["cases"])))
+def test_oracle_fill_ghost_matches_reference_golden(k):
+    # reference grid.py:179-193, both BCs, corners from the x-filled columns
+    c = FILL["cases"][k]
+    before, after = _fill_case(c)
+    a = np.asfortranarray(before.copy())
+    O.fill_ghost(a, c["bc_x"], c["bc_y"])
+    assert np.array_equal(a, after)
