@@ -130,7 +130,7 @@ def main():
         fp = num(upd, "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active")
         dur = num(upd, "gpu__time_duration.sum")
         u = dict(zip(hdr, units)).get("gpu__time_duration.sum", "ns")
-        dur_us = dur * (1e-3 if u == "ns" else 1)
+        dur_us = dur * {"ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}.get(u, 1.0)
         # FP64 warp-instr = pct x 0.5 warp-instr/clk/SMSP x 4 SMSP x 148 SM x active cycles
         cyc = num(upd, "sm__cycles_active.avg")
         per_cell = fp / 100 * 0.5 * 4 * 148 * cyc * 32 / a.cells if cyc else None
@@ -141,9 +141,11 @@ def main():
         js[a.config] = {
             "bytes_per_launch": int(b), "kernel": names[ks.index(upd)],
             "source": f"{a.raw} (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
-            "note": "1024^2 state (25 MB) is L2-resident: q_new stays in the 126 MB L2 "
-                    "during the launch; ncu flushes caches before the replay, so the reads "
-                    "come from DRAM",
+            "note": ("1024^2 state (25 MB) is L2-resident: q_new stays in the 126 MB L2 "
+                     "during the launch; ncu flushes caches before the replay, so the reads "
+                     "come from DRAM") if a.cells <= (1 << 21) else
+                    "state larger than L2: DRAM bytes vs the algorithmic 48 B/cell show the "
+                    "re-read overhead",
             "fp64_pipe_active_pct": fp,
             "issue_active_pct": num(upd, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "ncu_duration_us": dur_us,
