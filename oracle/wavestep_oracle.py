@@ -644,7 +644,11 @@ def _solve_band(q, aux, spec: Spec, solver: Solver, ja: int, jb: int, order: int
 
 
 def _update_band(q, spec: Spec, r: _BandResult, dt: float, order: int, limiter: str):
-    """Pass 2: donor-cell update (sweep.py:271-277) + correction flux."""
+    """Pass 2: donor-cell update (sweep.py:271-277) + correction flux.
+
+    Dimension by dimension: the reference's x term, then the x correction
+    flux difference, then the y term and the y correction.  order=1 is the
+    reference's update exactly (x term, then y term)."""
     g, nx = spec.g, spec.nx
     ja, jb = r.ja, r.jb
     nb = jb - ja
@@ -656,11 +660,13 @@ def _update_band(q, spec: Spec, r: _BandResult, dt: float, order: int, limiter: 
     xp = r.xp[:, ext:ext + nx + 1]
     ym = r.ym[:, :, ext:ext + nb + 1]
     yp = r.yp[:, :, ext:ext + nb + 1]
+    second = order == 2 and limiter != "none"
     cells -= dtdx * (xp[:, 0:nx] + xm[:, 1:nx + 1])
-    cells -= dtdy * (yp[:, :, 0:nb] + ym[:, :, 1:nb + 1])
-    if order == 2 and limiter != "none":
+    if second:
         fx = correction_flux(r.xw, r.xs, dtdx, limiter, axis=2)
         cells -= dtdx * (fx[:, 1:nx + 1] - fx[:, 0:nx])
+    cells -= dtdy * (yp[:, :, 0:nb] + ym[:, :, 1:nb + 1])
+    if second:
         fy = correction_flux(r.yw, r.ys, dtdy, limiter, axis=3)
         cells -= dtdy * (fy[:, :, 1:nb + 1] - fy[:, :, 0:nb])
 

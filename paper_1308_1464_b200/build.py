@@ -41,9 +41,20 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every translation unit (in parallel) and link libwavestep.so."""
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines: tuple = (),
+          out: Path | None = None) -> Path:
+    """Compile every translation unit (in parallel) and link libwavestep.so.
+
+    ``defines`` / ``out``: an experimental variant (e.g. WS_LB3=0) built into
+    its own directory; load it with WAVESTEP_LIB=<out>."""
+    global OUT
+    if out is not None:
+        saved, OUT = OUT, Path(out)
+        try:
+            return build(True, verbose, defines)
+        finally:
+            OUT = saved
+    if not force and not defines and up_to_date():
         return OUT
     from concurrent.futures import ThreadPoolExecutor
     OUT.parent.mkdir(parents=True, exist_ok=True)
@@ -53,7 +64,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: Path):
         obj = objdir / (src.stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-Xptxas", "-v", "-c", "-o", str(obj), str(src)]
+        cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-Xptxas", "-v", "-c",
+               "-o", str(obj), str(src)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, cmd, res
 
@@ -82,4 +94,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    # python -m paper_1308_1464_b200.build [--force] [--define X=1 ...] [--out path.so]
+    a = sys.argv[1:]
+    defs = tuple(a[i + 1] for i, x in enumerate(a) if x == "--define")
+    out = a[a.index("--out") + 1] if "--out" in a else None
+    build(force="--force" in a, verbose=True, defines=defs, out=out)

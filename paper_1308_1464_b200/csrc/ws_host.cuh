@@ -104,6 +104,7 @@ struct ws_handle {
   void* tmax = nullptr;         // [2][ntiles][4] R per-tile bound maxima
   bool pdl = true;              // programmatic dependent launch of the step kernels
   bool persist = true;          // persistent prefetching line kernel where it applies
+  bool persist3 = false;        // the same for 3-component fp64 (WS_PERSIST3=1)
   cudaError_t launch_err = cudaSuccess;  // first failed cudaLaunchKernelEx (reported once)
   void* peers_dev = nullptr;    // device table of the shards' DevState (device-side reduce)
   size_t border_bytes = 0;
@@ -259,13 +260,14 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     const int lsmem = (int)LineGeom<S>::template smem_bytes<R>();
     cudaFuncSetAttribute(kern_w<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
     cudaFuncSetAttribute(kern_w<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
-    if constexpr (PERSIST_W) {
+    if constexpr (PERSIST_W || PERSIST_3) {
       const int psmem = (int)LineGeom<S>::template smem_bytes<R>(true);
       cudaFuncSetAttribute(kern_w<true, false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
       cudaFuncSetAttribute(kern_w<false, false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
     }
     if constexpr (CAN_FUSE)
-      cudaFuncSetAttribute(kern_w<false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+      cudaFuncSetAttribute(kern_w<false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)LineGeom<S>::template smem_bytes<R>(false, true));
     const int smem = (int)G::template smem_bytes<R>();
     cudaFuncSetAttribute(kern<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(kern<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -286,26 +288,30 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   // 4-component systems stage 141 KB (fp64) -> 1 CTA/SM of 15 warps (97 %)
   static constexpr int LNW = (S::NEQ >= 4 && sizeof(R) == 8) ? 15 : 10;
   static constexpr bool CAN_FUSE = !S::STATIC_SPEEDS && S::NAUX == 0 && S::NPR <= S::NEQ;
+  // persistent form: one CTA of 15 warps per SM (29 lines / 15 ~ 97 %)
+  static constexpr int LNWP = 15;
   template <bool CHECKS, bool FUSED, bool PERSIST = false> static auto kern_w() {
-    return k_update_w<S, R, ORDER, LIM, LNW, CHECKS, FUSED, PERSIST>;
+    return k_update_w<S, R, ORDER, LIM, PERSIST ? LNWP : LNW, CHECKS, FUSED, PERSIST>;
   }
   // one CTA per SM (4-component fp64): persistent CTAs prefetch the next tile
   static constexpr bool PERSIST_W = S::NEQ >= 4 && sizeof(R) == 8;
+  // 3-component fp64: the persistent form is opt-in (WS_PERSIST3=1)
+  static constexpr bool PERSIST_3 = S::NEQ == 3 && sizeof(R) == 8;
   template <bool CHECKS, bool FUSED> static void update_w(ws_handle* h, const void* q, void* qn,
                                                           const StepArgs& a, cudaStream_t st) {
-    if constexpr (PERSIST_W && !FUSED) {
-      if (h->persist) {
+    if constexpr ((PERSIST_W || PERSIST_3) && !FUSED) {
+      if (PERSIST_W ? h->persist : h->persist3) {
         auto k = kern_w<CHECKS, false, true>();
         const size_t smem = LineGeom<S>::template smem_bytes<R>(true);
-        dim3 grid(persistent_grid(k, LNW * 32, smem, h->L.nx, h->L.ny, 29, 29));
-        launch(h, k, grid, dim3(LNW * 32), smem, st, static_cast<const R*>(q),
+        dim3 grid(persistent_grid(k, LNWP * 32, smem, h->L.nx, h->L.ny, 29, 29));
+        launch(h, k, grid, dim3(LNWP * 32), smem, st, static_cast<const R*>(q),
                static_cast<const R*>(h->aux), static_cast<R*>(qn), h->L, prm(h), a, h->ds);
         h->launches++;
         return;
       }
     }
     auto k = kern_w<CHECKS, FUSED>();
-    const size_t smem = LineGeom<S>::template smem_bytes<R>();
+    const size_t smem = LineGeom<S>::template smem_bytes<R>(false, FUSED);
     dim3 grid((h->L.nx + 28) / 29, (h->L.ny + 28) / 29);
     launch(h, k, grid, dim3(LNW * 32), smem, st, static_cast<const R*>(q),
            static_cast<const R*>(h->aux), static_cast<R*>(qn), h->L, prm(h), a, h->ds);

@@ -19,6 +19,10 @@
 
 #include "ws_solvers.cuh"
 
+#ifndef WS_LB3
+#define WS_LB3 1
+#endif
+
 namespace ws {
 
 // --------------------------------------------------------------------------
@@ -1262,7 +1266,7 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
         __syncthreads();
       }
 
-      R q1[KC][NEQ], dfx[KC][NEQ];
+      R q1[KC][NEQ];
 
       // one sweep direction: solve -> (limit) -> fluctuation/flux records in sE
       auto sweep = [&](auto ni_tag) {
@@ -1407,7 +1411,8 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
             R qc = sQ[m * HC + (lr + H) * HX + li + H];
             q1[kc][m] = qc - dtdx * (sE[(NEQ + m) * NIST + el] + sE[m * NIST + er]);
             if (ORDER == 2)
-              dfx[kc][m] = sE[(2 * NEQ + m) * NIST + er] - sE[(2 * NEQ + m) * NIST + el];
+              q1[kc][m] = q1[kc][m] - dtdx * (sE[(2 * NEQ + m) * NIST + er] -
+                                              sE[(2 * NEQ + m) * NIST + el]);
           }
         }
       }
@@ -1426,10 +1431,8 @@ k_update(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
 #pragma unroll
           for (int m = 0; m < NEQ; ++m) {
             R v = q1[kc][m] - dtdy * (sE[(NEQ + m) * NIST + el] + sE[m * NIST + eu]);
-            if (ORDER == 2) {
-              v = v - dtdx * dfx[kc][m];
+            if (ORDER == 2)
               v = v - dtdy * (sE[(2 * NEQ + m) * NIST + eu] - sE[(2 * NEQ + m) * NIST + el]);
-            }
             out[m] = v;
           }
           if (gi < L.nx && gj < L.ny) {
@@ -1716,14 +1719,16 @@ __device__ __forceinline__ void wait_arrivals(DevState* ds, unsigned long long n
 //   * the next edge's amdq / flux for the cell update is one more shuffle;
 //   * each sweep direction is ONE barrier-free pass (x: warps walk rows,
 //     y: warps walk columns), 3 barriers per tile in total.
-// The x pass leaves q1 = q - dtdx (apdq_i + amdq_{i+1}) and dFx per cell in
-// shared memory; the y pass adds the y term and both correction fluxes in
-// the reference order and writes q_new back to shared memory, from which
-// the tile is stored row-coalesced.
+// The x pass leaves q1 = (q - dtdx (apdq_i + amdq_{i+1})) - dtdx (F~_{i+1} - F~_i)
+// per cell in shared memory; the y pass subtracts the y term and then the y
+// correction (the oracle's dimension-by-dimension order) and writes q_new
+// back to shared memory, from which the tile is stored row-coalesced.
 template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUSED,
           bool PERSIST = false>
-__global__ void __launch_bounds__(NWARP * 32, (sizeof(R) == 4 && NWARP == 10 ? 3
+__global__ void __launch_bounds__(NWARP * 32, ((sizeof(R) == 4 || WS_LB3) && NWARP == 10 ? 3
                                                    : (20 / NWARP > 0 ? 20 / NWARP : 1)))
+// (10-warp CTAs: three per SM -- 30 warps, <= 64 registers, <= 75 KB of
+// shared memory each; WS_LB3=0 builds the two-per-SM form for comparison)
 k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
            const Layout L, const typename S::template Params<R> P, const StepArgs A,
            DevState* __restrict__ ds) {
@@ -1736,8 +1741,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   R* sQ = reinterpret_cast<R*>(smem_raw);
   R* sA = sQ + NEQ * HC;
   R* sP = sA + NAUX * HC;
-  R* sX = sP + NPR * HC;          // [2*NEQ][LW*LW]: q1 and dFx, later q_new
-  R* sR = sX + 2 * NEQ * LW * LW;  // PERSIST: raw q (+aux) of the next tile, cp.async
+  R* sX = sP + NPR * HC;          // [NEQ][LW*LW]: q1 after the x pass, later q_new
+                                  // (FUSED: [2*NEQ], the next state's prims after it)
+  R* sR = sX + (FUSED ? 2 : 1) * NEQ * LW * LW;  // PERSIST: raw q (+aux) of the next tile
   static_assert(!(PERSIST && FUSED), "persistent form has no fused epilogue");
 
   // warp index through a lane-0 broadcast: the compiler then treats it as
@@ -1853,6 +1859,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     if constexpr (HasTile<S>::value && !FUSED) {
       if (A.tmax && t_prev >= 0) finish_tile(t_prev);
     }
+    stage_ok = true;   // CHECKS: per tile
 #pragma unroll 4
     for (int idx = tid; idx < HC; idx += NT) {
       R qc[NEQ], ac[NA1], pc[NP1];
@@ -1958,8 +1965,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
           const R qc = sQ[m * HC + cr];
-          sX[m * (LW * LW) + r * LW + c] = qc - dtdx * (ap[m] + amn[m]);
-          if (ORDER == 2) sX[(NEQ + m) * (LW * LW) + r * LW + c] = fr[m] - fl[m];
+          R v = qc - dtdx * (ap[m] + amn[m]);
+          if (ORDER == 2) v = v - dtdx * (fr[m] - fl[m]);
+          sX[m * (LW * LW) + r * LW + c] = v;
         }
       }
     }
@@ -1989,10 +1997,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
           R v = sX[m * (LW * LW) + o] - dtdy * (ap[m] + amn[m]);
-          if (ORDER == 2) {
-            v = v - dtdx * sX[(NEQ + m) * (LW * LW) + o];
-            v = v - dtdy * (fr[m] - fl[m]);
-          }
+          if (ORDER == 2) v = v - dtdy * (fr[m] - fl[m]);
           sX[m * (LW * LW) + o] = v;
           qnew[m] = v;
         }
@@ -2189,8 +2194,10 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 
 template <class S> struct LineGeom {
   static constexpr int LW = 29, HC = 33 * 33;
-  template <class R> static constexpr size_t smem_bytes(bool persist = false) {
-    return sizeof(R) * (size_t)((S::NEQ + S::NAUX + S::NPR) * HC + 2 * S::NEQ * LW * LW +
+  template <class R> static constexpr size_t smem_bytes(bool persist = false,
+                                                        bool fused = false) {
+    return sizeof(R) * (size_t)((S::NEQ + S::NAUX + S::NPR) * HC +
+                                (fused ? 2 : 1) * S::NEQ * LW * LW +
                                 (persist ? (S::NEQ + S::NAUX) * HC : 0));
   }
 };

@@ -5,8 +5,8 @@ set -x
 nproc; free -g; nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 1500 python -m pytest tests -m gpu -q --durations=25 > gpurun_out/r2_pytest_gpu.log 2>&1; echo pytest_rc=$?
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1; echo smoke_rc=$?
-/usr/bin/time -v python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r2_bench_ref.json 2> gpurun_out/r2_bench_ref.err; echo ref_rc=$?
-/usr/bin/time -v python bench.py --steps 20 --warmup 5 > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err; echo bench_rc=$?
+python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r2_bench_ref.json 2> gpurun_out/r2_bench_ref.err; echo ref_rc=$?
+python bench.py --steps 20 --warmup 5 > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err; echo bench_rc=$?
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_c5.csv python bench.py --steps 20 --warmup 5 > gpurun_out/r2_ncu_launch.log 2>&1
 echo launch_rc=$?
 CMD="python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu"

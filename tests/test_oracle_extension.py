@@ -15,7 +15,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from helpers import oracle_run, random_state
+from helpers import PARAMS, oracle_run, random_state
 from oracle import exact_riemann as X
 from oracle import wavestep_oracle as O
 
@@ -196,3 +196,49 @@ def test_oracle_golden_regression():
         assert [r.dt for r in reps] == c["dts"], name
         h = hashlib.sha256((np.asfortranarray(oq) + 0.0).tobytes(order="F")).hexdigest()
         assert h == c["q_sha256"], name
+
+
+def test_oracle_matches_round1_fixture_dts():
+    """The update's association changed after round 1 (x term + x correction,
+    then y): every dt of the round-1 fixtures still agrees to 1e-12."""
+    old = json.load(open(os.path.join(HERE, "golden", "oracle_golden_r1.json")))["steps"]
+    new = json.load(open(os.path.join(HERE, "golden", "oracle_golden.json")))["steps"]
+    assert old.keys() == new.keys()
+    for name in old:
+        a, b = np.array(old[name]["dts"]), np.array(new[name]["dts"])
+        assert a.shape == b.shape
+        assert np.abs(b / a - 1.0).max() <= 1e-12, name
+
+
+@pytest.mark.parametrize("name,limiter", [("shallow-water-roe", "mc"),
+                                          ("euler-hlle", "minmod"),
+                                          ("euler", "superbee"),
+                                          ("acoustics-var", "mc"),
+                                          ("acoustics-const", "superbee")])
+def test_oracle_second_order_equals_clawpack_order(name, limiter):
+    """Independent anchor of the second-order update: the oracle
+    against a Clawpack-grouped restatement (tests/clawpack_order.py), 10
+    steps from the same state: relative state difference <= 1e-12 and every
+    dt within 1e-12 (north_star's fp64 tolerance)."""
+    import clawpack_order as CO
+    nx, ny = 48, 37
+    dx, dy = 1.0 / nx, 1.3 / ny
+    q, aux = random_state(name, nx, ny, 11)
+    solver = O.make_solver(name, **PARAMS[name])
+    spec = O.Spec(nx, ny, dx, dy)
+    oq = np.asfortranarray(q.copy())
+    oa = np.asfortranarray(aux.copy()) if aux is not None else None
+    cq = np.asfortranarray(q.copy())
+    ca = np.asfortranarray(aux.copy()) if aux is not None else None
+    for k in range(10):
+        r = O.step(oq, oa, spec, solver, O.Controller(0.9), bc_x="periodic", bc_y="periodic",
+                   order=2, limiter=limiter)
+        dt, msx, msy = CO.step(cq, ca, nx, ny, dx, dy, solver, 0.9, "periodic", limiter)
+        assert abs(r.dt / dt - 1.0) <= 1e-12, k
+        assert abs(r.max_speed_x / msx - 1.0) <= 1e-12
+    scale = np.abs(oq[:, 2:-2, 2:-2]).max(axis=(1, 2))
+    rel = (np.abs(oq[:, 2:-2, 2:-2] - cq[:, 2:-2, 2:-2]).max(axis=(1, 2)) /
+           np.where(scale > 0, scale, 1.0)).max()
+    assert rel <= 1e-12, rel
+    # and the two differ only by rounding, not identically (the check has teeth)
+    assert not np.array_equal(oq, cq) or name.startswith("acoustics-const")
