@@ -307,7 +307,6 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   }
   if (const char* v = std::getenv("WS_PDL")) h->pdl = std::atoi(v) != 0;
   if (const char* v = std::getenv("WS_PERSIST")) h->persist = std::atoi(v) != 0;
-  if (const char* v = std::getenv("WS_PERSIST3")) h->persist3 = std::atoi(v) != 0;
   {
     const char* v = std::getenv("WS_FUSE");
     const bool env_on = v && std::atoi(v) != 0, env_off = v && std::atoi(v) == 0;

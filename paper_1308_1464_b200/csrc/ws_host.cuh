@@ -104,7 +104,6 @@ struct ws_handle {
   void* tmax = nullptr;         // [2][ntiles][4] R per-tile bound maxima
   bool pdl = true;              // programmatic dependent launch of the step kernels
   bool persist = true;          // persistent prefetching line kernel where it applies
-  bool persist3 = false;        // the same for 3-component fp64 (WS_PERSIST3=1)
   cudaError_t launch_err = cudaSuccess;  // first failed cudaLaunchKernelEx (reported once)
   void* peers_dev = nullptr;    // device table of the shards' DevState (device-side reduce)
   size_t border_bytes = 0;
@@ -260,7 +259,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     const int lsmem = (int)LineGeom<S>::template smem_bytes<R>();
     cudaFuncSetAttribute(kern_w<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
     cudaFuncSetAttribute(kern_w<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
-    if constexpr (PERSIST_W || PERSIST_3) {
+    if constexpr (PERSIST_W) {
       const int psmem = (int)LineGeom<S>::template smem_bytes<R>(true);
       cudaFuncSetAttribute(kern_w<true, false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
       cudaFuncSetAttribute(kern_w<false, false, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
@@ -295,12 +294,11 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   }
   // one CTA per SM (4-component fp64): persistent CTAs prefetch the next tile
   static constexpr bool PERSIST_W = S::NEQ >= 4 && sizeof(R) == 8;
-  // 3-component fp64: the persistent form is opt-in (WS_PERSIST3=1)
-  static constexpr bool PERSIST_3 = S::NEQ == 3 && sizeof(R) == 8;
+
   template <bool CHECKS, bool FUSED> static void update_w(ws_handle* h, const void* q, void* qn,
                                                           const StepArgs& a, cudaStream_t st) {
-    if constexpr ((PERSIST_W || PERSIST_3) && !FUSED) {
-      if (PERSIST_W ? h->persist : h->persist3) {
+    if constexpr (PERSIST_W && !FUSED) {
+      if (h->persist) {
         auto k = kern_w<CHECKS, false, true>();
         const size_t smem = LineGeom<S>::template smem_bytes<R>(true);
         dim3 grid(persistent_grid(k, LNWP * 32, smem, h->L.nx, h->L.ny, 29, 29));

@@ -1728,7 +1728,9 @@ template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUS
 __global__ void __launch_bounds__(NWARP * 32, ((sizeof(R) == 4 || WS_LB3) && NWARP == 10 ? 3
                                                    : (20 / NWARP > 0 ? 20 / NWARP : 1)))
 // (10-warp CTAs: three per SM -- 30 warps, <= 64 registers, <= 75 KB of
-// shared memory each; WS_LB3=0 builds the two-per-SM form for comparison)
+// shared memory each; WS_LB3=0 builds the two-per-SM form for comparison.
+// Measured and dropped for 3-component fp64: the persistent prefetching
+// form at one 15-warp CTA per SM (-18 %) and at two (-19 % on C5))
 k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
            const Layout L, const typename S::template Params<R> P, const StepArgs A,
            DevState* __restrict__ ds) {
