@@ -20,7 +20,8 @@
  *   WS_OK (0), WS_ERR_KERNEL (1: inadmissible state, see ws_error_info),
  *   WS_ERR_CONFIG (2: bad descriptor / argument, message in ws_last_error),
  *   WS_ERR_CUDA (3), WS_ERR_STATIONARY (4: all wave speeds zero and no
- *   fixed_dt — reference driver.py:50-51 raises ValueError).
+ *   fixed_dt — reference driver.py:50-51 raises ValueError), WS_ERR_INTERNAL
+ *   (5: a device-side invariant check failed -- a bug, never the input).
  */
 #ifndef WAVESTEP_H
 #define WAVESTEP_H
@@ -34,7 +35,7 @@ extern "C" {
 #define WS_ABI_VERSION 1
 
 enum ws_status { WS_OK = 0, WS_ERR_KERNEL = 1, WS_ERR_CONFIG = 2, WS_ERR_CUDA = 3,
-                 WS_ERR_STATIONARY = 4 };
+                 WS_ERR_STATIONARY = 4, WS_ERR_INTERNAL = 5 };
 
 /* Riemann solvers: reference kernels.py:89-94 (DESCRIPTORS) plus the two
  * north-star solvers the reference lacks. */
@@ -153,6 +154,14 @@ int ws_download_aux_ghosts(ws_handle* h, void* aux_host, void* stream);
  * (the reference's step mutates them in place, driver.py:199-225). */
 int ws_pin_host(void* ptr, uint64_t bytes);
 int ws_unpin_host(void* ptr);
+
+/* Checked builds only (-DWS_CHECKED=1; the device analogue of the
+ * reference's WAVESWEEP_CHECKED write counts, sweep.py:32-33, 78-96): the
+ * bits of every device index check that failed since the last upload, and
+ * the minimum / maximum over the interior cells of the update kernel's
+ * write counts (each step writes every cell exactly once).  Other builds
+ * return WS_ERR_CONFIG. */
+int ws_checked_counts(ws_handle* h, uint32_t* flags, uint32_t* writes_min, uint32_t* writes_max);
 
 /* One step, enqueued only (no host sync): fill ghosts (implicit, by index
  * mapping) -> sweep -> choose_dt on device -> update.

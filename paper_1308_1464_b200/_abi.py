@@ -17,6 +17,7 @@ LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = LIB_DIR / "libwavestep.so"
 
 WS_OK, WS_ERR_KERNEL, WS_ERR_CONFIG, WS_ERR_CUDA, WS_ERR_STATIONARY = 0, 1, 2, 3, 4
+WS_ERR_INTERNAL = 5
 
 SOLVER_IDS = {
     "acoustics-const": 0,
@@ -83,6 +84,8 @@ SIGNATURES = [
     ("ws_download_aux_ghosts", C.c_int, [_P, _P, _P]),
     ("ws_pin_host", C.c_int, [_P, C.c_uint64]),
     ("ws_unpin_host", C.c_int, [_P]),
+    ("ws_checked_counts", C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                    C.POINTER(C.c_uint32)]),
     ("ws_phase_speeds", C.c_int, [_P, _P]),
     ("ws_phase_speeds_part", C.c_int, [_P, C.c_int32, _P]),
     ("ws_phase_update", C.c_int, [_P, C.POINTER(WsCtl), _P]),

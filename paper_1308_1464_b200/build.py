@@ -34,11 +34,28 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def up_to_date() -> bool:
-    if not OUT.exists():
+# the checked variant (-DWS_CHECKED=1): device index checks, per-cell write
+# counts and NaN canaries; the GPU tests load it with WAVESTEP_LIB
+CHECKED_OUT = HERE / "_lib" / "checked" / "libwavestep.so"
+
+
+def up_to_date(out: Path | None = None) -> bool:
+    out = OUT if out is None else out
+    if not out.exists():
         return False
-    t = OUT.stat().st_mtime
+    t = out.stat().st_mtime
     return all(p.stat().st_mtime <= t for p in DEPS)
+
+
+def build_all(force: bool = False, verbose: bool = False) -> Path:
+    """The product library and its checked variant (both in-tree, sm_100a)."""
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = [lambda: build(force, verbose)]
+    if force or not up_to_date(CHECKED_OUT):
+        jobs.append(lambda: build(True, verbose, ("WS_CHECKED=1",), CHECKED_OUT))
+    with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        outs = [f.result() for f in [ex.submit(j) for j in jobs]]
+    return outs[0]
 
 
 def build(force: bool = False, verbose: bool = False, defines: tuple = (),
@@ -47,15 +64,14 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (),
 
     ``defines`` / ``out``: an experimental variant (e.g. WS_LB3=0) built into
     its own directory; load it with WAVESTEP_LIB=<out>."""
-    global OUT
     if out is not None:
-        saved, OUT = OUT, Path(out)
-        try:
-            return build(True, verbose, defines)
-        finally:
-            OUT = saved
+        return _build(Path(out), verbose, defines)
     if not force and not defines and up_to_date():
         return OUT
+    return _build(OUT, verbose, defines)
+
+
+def _build(OUT: Path, verbose: bool, defines: tuple) -> Path:
     from concurrent.futures import ThreadPoolExecutor
     OUT.parent.mkdir(parents=True, exist_ok=True)
     objdir = OUT.parent / "obj"
@@ -98,4 +114,7 @@ if __name__ == "__main__":
     a = sys.argv[1:]
     defs = tuple(a[i + 1] for i, x in enumerate(a) if x == "--define")
     out = a[a.index("--out") + 1] if "--out" in a else None
-    build(force="--force" in a, verbose=True, defines=defs, out=out)
+    if defs or out:
+        build(force="--force" in a, verbose=True, defines=defs, out=out)
+    else:
+        build_all(force="--force" in a, verbose=True)

@@ -178,6 +178,7 @@ void compute_layout(ws_handle* h) {
   L.nx_glob = d.nx;
   L.trace = nullptr;
   L.trace_cap = 0;
+  L.chk = nullptr;
   L.peers = nullptr;
   L.npeers = 0;
   L.nq_lo[0] = L.nq_lo[1] = L.nq_hi[0] = L.nq_hi[1] = nullptr;
@@ -335,6 +336,15 @@ int ws_create(const ws_desc* d, ws_handle** out) {
     }
   }
   h->ops.prepare();
+  if (WS_CHECKED) {
+    const size_t cb = sizeof(unsigned) * (1 + (size_t)d->nx * d->ny);
+    if ((e = cudaMalloc(&h->chk, cb)) != cudaSuccess) {
+      ws_destroy(h);
+      return fail(nullptr, WS_ERR_CUDA, cudaGetErrorString(e));
+    }
+    cudaMemsetAsync(h->chk, 0, cb, h->stream);
+    h->L.chk = h->chk;
+  }
   if (const char* v = std::getenv("WS_TRACE")) {
     if (std::atoi(v) != 0) {
       // diagnostics: one {start, end, smid, block} record per CTA of the pre-pass
@@ -378,6 +388,7 @@ void ws_destroy(ws_handle* h) {
   if (h->borders) cudaFree(h->borders);
   if (h->tmax) cudaFree(h->tmax);
   if (h->trace) cudaFree(h->trace);
+  if (h->chk) cudaFree(h->chk);
   if (h->cstream) { cudaStreamSynchronize(h->cstream); cudaStreamDestroy(h->cstream); }
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -426,6 +437,10 @@ static int upload_impl(ws_handle* h, const void* qh, const void* ah, size_t hesz
     h->ops.to_soa(h, h->stage[b], h->aux, h->naux, st);
   }
   WS_CUDA(h, cudaEventRecord(h->ev_in[b], st));
+  if (WS_CHECKED && h->chk) {
+    WS_CUDA(h, cudaMemsetAsync(h->chk, 0, sizeof(unsigned) * (1 + (size_t)h->d.nx * h->d.ny), st));
+    h->ops.canary(h, st);
+  }
   WS_CUDA(h, cudaMemsetAsync(h->ds, 0, offsetof(DevState, rep), st));
   WS_CUDA(h, cudaMemsetAsync(h->borders, 0, h->border_bytes, st));
   h->need_prepass = true;
@@ -571,6 +586,19 @@ int ws_download_aux_ghosts(ws_handle* h, void* ah, void* s) {
   WS_CUDA(h, cudaMemcpy2DAsync(hd + hi, row, sd + hi, row, 2 * na * es, (size_t)h->d.ny,
                                cudaMemcpyDeviceToHost, st));
   WS_CUDA(h, cudaStreamSynchronize(st));
+  return WS_OK;
+}
+
+int ws_checked_counts(ws_handle* h, uint32_t* flags, uint32_t* wmin, uint32_t* wmax) {
+  if (!h || !flags || !wmin || !wmax) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (!WS_CHECKED || !h->chk) return fail(h, WS_ERR_CONFIG, "not a checked build (-DWS_CHECKED=1)");
+  cudaStream_t st = h->last_stream ? h->last_stream : h->stream;
+  WS_CUDA(h, cudaStreamSynchronize(st));
+  std::vector<unsigned> c(1 + (size_t)h->d.nx * h->d.ny);
+  WS_CUDA(h, cudaMemcpy(c.data(), h->chk, sizeof(unsigned) * c.size(), cudaMemcpyDeviceToHost));
+  unsigned lo = ~0u, hi = 0u;
+  for (size_t k = 1; k < c.size(); ++k) { lo = c[k] < lo ? c[k] : lo; hi = c[k] > hi ? c[k] : hi; }
+  *flags = c[0]; *wmin = lo; *wmax = hi;
   return WS_OK;
 }
 

@@ -14,7 +14,31 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef WS_CHECKED
+#define WS_CHECKED 0
+#endif
+
 namespace ws {
+
+// Checked builds (-DWS_CHECKED=1, _lib/checked/): the device analogue of the
+// reference's WAVESWEEP_CHECKED mode (sweep.py:32-33, 78-96, which counts
+// writes per interface slot and asserts exactly one).  Every kernel checks
+// its shared-memory and global indices against the layout, a broken check
+// sets a bit in Layout::chk[0], and the update kernel counts its writes per
+// interior cell in chk[1 + j*nx + i] (exactly one per step).  The upload
+// also fills every location no kernel may read (padding columns, the ghost
+// rows of physical boundaries) with NaN, so a stray read poisons the result
+// that the parity tests compare bit for bit.
+enum : unsigned {
+  CHK_STAGE_SMEM = 1u, CHK_STAGE_READ = 2u, CHK_EDGE_SMEM = 4u, CHK_X_SMEM = 8u,
+  CHK_STORE = 16u, CHK_PREPASS_READ = 32u, CHK_TILE_LIST = 64u
+};
+#define WS_CHK(L, cond, bit)                                                    \
+  do {                                                                          \
+    if (WS_CHECKED) {                                                           \
+      if (!(cond) && (L).chk != nullptr) atomicOr((L).chk, (unsigned)(bit));   \
+    }                                                                           \
+  } while (0)
 
 enum : int { BC_PERIODIC = 0, BC_EXTRAPOLATE = 1 };
 enum : int { ROWS_MEMORY = 0, ROWS_BC = 1 };
@@ -24,6 +48,7 @@ constexpr int REPCAP = 4096;          // device report ring (steps between polls
 constexpr int ERR_KERNEL = 1;
 constexpr int ERR_STATIONARY = 4;
 constexpr int ERR_WAIT_TIMEOUT = 3;   // a device-side wait gave up (reported as WS_ERR_CUDA)
+constexpr int ERR_INTERNAL = 5;       // a device-side invariant broke (reported as WS_ERR_CUDA)
 
 struct DevState;
 
@@ -49,7 +74,14 @@ struct Layout {
   struct DevState* nds_hi;
   int ny_lo;
   int hsides;                 // ghost-row sides this shard receives by push (0..2)
+  unsigned* chk;              // checked builds: {violation bits, write count per cell}
 };
+
+// a row a kernel may read after index mapping: memory ghost rows only on
+// sides whose ghost rows are in memory, else interior rows
+__device__ __forceinline__ bool row_readable(int j, const Layout& L) {
+  return j >= (L.lo == ROWS_MEMORY ? -2 : 0) && j < L.ny + (L.hi == ROWS_MEMORY ? 2 : 0);
+}
 
 // Programmatic dependent launch (sm_90+): a kernel launched with the
 // programmatic-serialization attribute may start before its predecessor in

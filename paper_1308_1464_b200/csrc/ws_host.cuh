@@ -39,6 +39,7 @@ struct Ops {
   void (*to_soa)(ws_handle*, const void* stage, void* dst, int ncomp, cudaStream_t);
   void (*to_aos)(ws_handle*, const void* cur, const void* gsrc, void* stage, cudaStream_t);
   void (*to_aos_aux)(ws_handle*, void* stage, cudaStream_t);   // aux + BC ghost frame
+  void (*canary)(ws_handle*, cudaStream_t);   // checked builds: NaN where nothing may read
   void (*static_speed)(ws_handle*, cudaStream_t);
   void (*prepare)();   // one-time kernel attributes (never inside a capture)
   int static_speeds;   // solver has q-independent speeds
@@ -64,6 +65,7 @@ struct ws_handle {
   int up_idx = 0;                        // staging buffer of the next upload
   void* stage_out = nullptr;     // download staging: a download and the next upload overlap
   size_t stage_out_bytes = 0;
+  unsigned* chk = nullptr;       // checked builds: {violation bits, per-cell write counts}
   void* stage_aux = nullptr;     // aux in the host layout with its BC ghost frame
   size_t stage_aux_bytes = 0;
   cudaStream_t stream = nullptr;
@@ -362,6 +364,17 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     h->launches++;
   }
 
+  static void canary(ws_handle* h, cudaStream_t st) {
+    for (int b = 0; b < 2; ++b) {
+      k_canary<R><<<148 * 4, 256, 0, st>>>(static_cast<R*>(h->q[b]), h->L, h->neq);
+      h->launches++;
+    }
+    if (h->naux > 0) {
+      k_canary<R><<<148 * 4, 256, 0, st>>>(static_cast<R*>(h->aux), h->L, h->naux);
+      h->launches++;
+    }
+  }
+
   static void static_speed(ws_handle* h, cudaStream_t st) {
     if (S::NAUX > 0) {
       k_static_speed<R><<<148 * 4, 256, 0, st>>>(static_cast<const R*>(h->aux), h->L, h->ds);
@@ -376,6 +389,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     o.to_soa = &to_soa;
     o.to_aos = &to_aos;
     o.to_aos_aux = &to_aos_aux;
+    o.canary = &canary;
     o.static_speed = &static_speed;
     o.prepare = &prepare;
     o.static_speeds = S::STATIC_SPEEDS ? 1 : 0;

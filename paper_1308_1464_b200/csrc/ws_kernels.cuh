@@ -765,7 +765,7 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
   constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   constexpr int LW = 29, NT = NWT * 32;
-  __shared__ int s_list[TILE_LIST];
+  __shared__ unsigned s_list[TILE_LIST];
   __shared__ int s_cnt, s_ok;
   __shared__ R s_t[2];
   const int tid = threadIdx.x, lane = tid & 31, wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
@@ -806,11 +806,23 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
       // cells, which no tile maxima here describe: always probed
       const int ty = t / ntx;
       if ((L.lo == ROWS_MEMORY && ty == 0) || (L.hi == ROWS_MEMORY && ty == nty - 1)) cy = true;
-      if (cx || cy)
-        s_list[atomicAdd(&s_cnt, 1)] = t | (part << 28) | (cx ? 1 << 30 : 0) | (cy ? 1 << 31 : 0);
+      if (cx || cy) {
+        // entry: tile (28 bits) | part (2 bits, SPL <= 4) | cx << 30 | cy << 31
+        const int slot = atomicAdd(&s_cnt, 1);
+        if (slot < TILE_LIST)
+          s_list[slot] = (unsigned)t | ((unsigned)part << 28) | (cx ? 1u << 30 : 0u) |
+                         (cy ? 1u << 31 : 0u);
+      }
     }
   }
   __syncthreads();
+  // the host sizes the grid so a CTA lists at most NT * SPL <= TILE_LIST
+  // tiles (ws_host.cuh); should that ever break, the step fails loudly
+  // instead of overrunning shared memory
+  if (s_cnt > TILE_LIST) {
+    if (tid == 0) { atomicCAS(&ds->err, 0, ERR_INTERNAL); WS_CHK(L, false, CHK_TILE_LIST); }
+    return;
+  }
   // an item is a run of TR consecutive edge rows of a listed tile; part s of
   // a tile takes the runs s, s + SPL, ...
   constexpr int TR = S::NEQ >= 4 ? 4 : 1;       // gas prims are dear: march runs
@@ -842,10 +854,10 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
   using NY = std::integral_constant<int, 2>;
 
   for (int item = wid; item < nitems; item += NWT) {
-    const int ent = s_list[item / ngs];
-    const int tile = ent & ((1 << 28) - 1);
-    const int run = ((ent >> 28) & 3) + SPL * (item % ngs);
-    const bool cx = (ent & (1 << 30)) != 0, cy = ent < 0;
+    const unsigned ent = s_list[item / ngs];
+    const int tile = (int)(ent & ((1u << 28) - 1u));
+    const int run = (int)((ent >> 28) & 3u) + SPL * (item % ngs);
+    const bool cx = (ent >> 30) & 1u, cy = (ent >> 31) & 1u;
     const int i0 = (tile % ntx) * LW, j0 = (tile / ntx) * LW;
     // edges owned: x-edges ei in [i0, iend) on rows [j0, min(j0+29, ny));
     // y-edges ci in [i0, min(i0+29, nx)) on rows [j0, rend)
@@ -868,6 +880,7 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
       if (k <= nr) {
         const int rr = rb - 1 + k;
         const int gj = map_j(rr < L.ny ? rr : L.ny, L);
+        WS_CHK(L, row_readable(gj, L) && gi >= 0 && gi < L.nx, CHK_PREPASS_READ);
         const R* src = q + row_off(gj, L) + gi;
 #pragma unroll
         for (int c = 0; c < NEQ; ++c) qb[k][c] = __ldcg(src + c * L.pitch);
@@ -1774,6 +1787,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       const int lx = idx % HW, ly = idx / HW;
       int gi = a - 2 + lx, gj = b - 2 + ly;
       if (!in) { gi = map_i(gi, L); gj = map_j(gj, L); }
+      WS_CHK(L, gi >= 0 && gi < L.nx && row_readable(gj, L), CHK_STAGE_READ);
       const R* src = q + row_off(gj, L) + gi;
 #pragma unroll
       for (int c = 0; c < NEQ; ++c) cp_async(&sR[c * HC + idx], src + c * L.pitch);
@@ -1894,6 +1908,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         const int lx = idx % HW, ly = idx / HW;
         int gi = i0 - 2 + lx, gj = j0 - 2 + ly;
         if (!inner) { gi = map_i(gi, L); gj = map_j(gj, L); }
+        WS_CHK(L, gi >= 0 && gi < L.nx && row_readable(gj, L), CHK_STAGE_READ);
         const R* src = q + row_off(gj, L) + gi;
 #pragma unroll
         for (int c = 0; c < NEQ; ++c) qs[k][c] = __ldcg(src + c * L.pitch);
@@ -1956,6 +1971,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     for (int r = warp; r < LW; r += NWARP) {
       if (j0 + r >= L.ny) break;
       const int cl = (r + 2) * HW + lane, cr = cl + 1;
+      WS_CHK(L, cl >= 0 && cr < HC, CHK_EDGE_SMEM);
       const int ei = i0 - 1 + lane;
       R ap[NEQ], amn[NEQ], fl[NEQ], fr[NEQ];
       line_edge<S, R, ORDER, LIM, CHECKS, 1, HC>(sQ, sA, sP, P, L, cl, cr, ei, j0 + r,
@@ -1969,6 +1985,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
           const R qc = sQ[m * HC + cr];
           R v = qc - dtdx * (ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdx * (fr[m] - fl[m]);
+          WS_CHK(L, r * LW + c < LW * LW, CHK_X_SMEM);
           sX[m * (LW * LW) + r * LW + c] = v;
         }
       }
@@ -1987,6 +2004,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     for (int c = warp; c < LW; c += NWARP) {
       if (i0 + c >= L.nx) break;
       const int cl = lane * HW + c + 2, cr = cl + HW;
+      WS_CHK(L, cl >= 0 && cr < HC, CHK_EDGE_SMEM);
       const int ej = j0 - 1 + lane;
       R ap[NEQ], amn[NEQ], fl[NEQ], fr[NEQ];
       line_edge<S, R, ORDER, LIM, CHECKS, 2, HC>(sQ, sA, sP, P, L, cl, cr, i0 + c, ej,
@@ -1995,6 +2013,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
                                                   dtdy, key, ap, amn, fl, fr);
       R qnew[NEQ];
       const int rr = lane - 1, o = rr * LW + c;
+      WS_CHK(L, !cell_lane || (o >= 0 && o < LW * LW), CHK_X_SMEM);
       if (cell_lane) {
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
@@ -2103,6 +2122,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         R* dst = qn + row_off(gj, L) + gi;
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = sX[m * (LW * LW) + idx];
+        WS_CHK(L, gi >= 0 && gj >= 0, CHK_STORE);
+        if (WS_CHECKED && L.chk) atomicAdd(&L.chk[1 + (long long)gj * L.nx + gi], 1u);
         if constexpr (HasTile<S>::value && !FUSED) {
           // tile-bound ingredients of the new cell for the next pre-pass
           // (k_speeds_t)
@@ -2191,6 +2212,23 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       commit_step<R>(ds, A, ctl, L);
     }
     if (L.trace) trace_cta(L, 1, t_start);
+  }
+}
+
+// checked builds: NaN into every location no kernel may read -- the padding
+// columns [nx, pitch) of each component row and the ghost rows of physical
+// boundary sides (those are produced by index mapping, never loaded)
+template <class R>
+__global__ void k_canary(R* __restrict__ buf, const Layout L, int ncomp) {
+  const long long per_row = (long long)ncomp * L.pitch;
+  const long long n = (long long)(L.ny + 4) * per_row;
+  const R nan = (R)NAN;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(t / per_row) - 2;
+    const int i = (int)((t % per_row) % L.pitch);
+    const bool bc_row = (j < 0 && L.lo == ROWS_BC) || (j >= L.ny && L.hi == ROWS_BC);
+    if (i >= L.nx || bc_row) buf[t] = nan;
   }
 }
 

@@ -218,6 +218,14 @@ class DeviceGrid:
         arr = (ctypes.c_void_p * max(1, len(state_ptrs)))(*state_ptrs)
         self._check(self.lib.ws_set_peers(self.h, len(state_ptrs), arr))
 
+    def checked_counts(self):
+        """Checked builds (WAVESTEP_LIB=_lib/checked/libwavestep.so): (violation
+        bits, min, max of the per-cell write counts) since the upload."""
+        f, lo, hi = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        self._check(self.lib.ws_checked_counts(self.h, ctypes.byref(f), ctypes.byref(lo),
+                                               ctypes.byref(hi)))
+        return f.value, lo.value, hi.value
+
     def launches(self) -> int:
         return int(self.lib.ws_launch_count(self.h))
 

@@ -1,0 +1,98 @@
+"""Parity cases run against the CHECKED build (-DWS_CHECKED=1; the device
+analogue of the reference's WAVESWEEP_CHECKED mode, sweep.py:32-33, 78-96).
+
+    WAVESTEP_LIB=paper_1308_1464_b200/_lib/checked/libwavestep.so \\
+        python tests/checked_cases.py
+
+Every case must (1) match the oracle bit for bit although every location no
+kernel may read holds NaN, (2) report no failed device index check, and (3)
+have written every interior cell exactly once per step.  Prints one JSON
+line per case; exit status 0 iff all pass.  Driven by test_gpu_checked.py.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+
+from helpers import PARAMS, device_grid, oracle_run, random_state  # noqa: E402
+
+
+def single(name, nx, ny, bc, order, limiter, steps, seed, use_run):
+    from paper_1308_1464_b200 import _abi
+    dx, dy = 1.0 / nx, 1.3 / ny
+    q, aux = random_state(name, nx, ny, seed)
+    oq, oreps = oracle_run(name, q, aux, nx, ny, dx, dy, steps=steps, order=order,
+                           limiter=limiter, bc_x=bc[0], bc_y=bc[1])
+    g = device_grid(name, nx, ny, dx, dy, order=order, limiter=limiter, bc_x=bc[0], bc_y=bc[1])
+    try:
+        g.upload(q, aux)
+        c = _abi.make_ctl(0.9)
+        if use_run:
+            g.run(steps, c)
+        else:
+            for _ in range(steps):
+                g.step(c)
+        res = g.poll()
+        out = g.download()
+        flags, wmin, wmax = g.checked_counts()
+    finally:
+        g.close()
+    ok = (res.error.code == 0 and res.steps_done == steps and np.array_equal(out, oq) and
+          [r[0] for r in res.reports] == [r.dt for r in oreps] and flags == 0 and
+          wmin == wmax == steps)
+    return {"case": f"{name} {nx}x{ny} {bc} o{order} {limiter}", "ok": bool(ok),
+            "flags": flags, "writes": [wmin, wmax], "steps": steps}
+
+
+def sharded(name, P, bc, dred, dhalo):
+    from test_gpu_multishard import fake_sharded
+    nx, ny, steps = 70, 61, 3
+    dx, dy = 1.0 / nx, 1.0 / ny
+    q, aux = random_state(name, nx, ny, 7)
+    oq, oreps = oracle_run(name, q, aux, nx, ny, dx, dy, steps=steps, order=2, limiter="mc",
+                           bc_x=bc, bc_y=bc)
+    seen = []
+    out, reps, errs, strips = fake_sharded(name, q, aux, nx, ny, dx, dy, P, steps, 2, "mc", bc,
+                                           device_reduce=dred, device_halo=dhalo,
+                                           inspect=lambda g: seen.append(g.checked_counts()))
+    full = np.concatenate(out, axis=2)
+    ok = (np.array_equal(full, oq[:, 2:-2, 2:-2]) and all(e.code == 0 for e in errs) and
+          all(r == [x.dt for x in oreps] for r in reps) and
+          all(f == 0 and lo == hi == steps for f, lo, hi in seen))
+    return {"case": f"{name} {P} shards {bc} reduce={dred} halo={dhalo}", "ok": bool(ok),
+            "shards": seen}
+
+
+def main():
+    results = []
+    solvers = ["advection", "acoustics-const", "acoustics-var", "euler", "euler-hlle",
+               "shallow-water-roe"]
+    bcs = [("extrapolate", "extrapolate"), ("periodic", "periodic"), ("periodic", "extrapolate")]
+    for name in solvers:
+        for bc in bcs:
+            results.append(single(name, 37, 29, bc, 2, "mc", 3, 1, False))
+        results.append(single(name, 131, 75, ("extrapolate", "extrapolate"), 2, "minmod", 5, 2, True))
+        results.append(single(name, 37, 29, ("periodic", "periodic"), 1, "none", 3, 3, False))
+    for nx, ny in ((1, 1), (2, 3), (5, 1), (33, 17), (610, 97)):
+        results.append(single("shallow-water-roe", nx, ny, ("extrapolate", "extrapolate"), 2,
+                              "mc", 3, 4, False))
+    for name, P, bc, dred, dhalo in (("shallow-water-roe", 2, "extrapolate", False, False),
+                                     ("shallow-water-roe", 3, "periodic", True, False),
+                                     ("euler-hlle", 3, "extrapolate", True, True),
+                                     ("acoustics-var", 2, "periodic", True, True)):
+        results.append(sharded(name, P, bc, dred, dhalo))
+    for r in results:
+        print(json.dumps(r))
+    return 0 if all(r["ok"] for r in results) else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

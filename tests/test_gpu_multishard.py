@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 
 def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
-                 device_reduce=False, device_halo=False):
+                 device_reduce=False, device_halo=False, inspect=None):
     import torch
 
     from paper_1308_1464_b200 import _abi
@@ -93,6 +93,8 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
         reps.append([r[0] for r in res.reports])
         errs.append(res.error)
         out.append(sh.grid.download()[:, 2:-2, 2:-2])
+        if inspect is not None:
+            inspect(sh.grid)
         sh.grid.close()
     return out, reps, errs, strips
 
