@@ -52,6 +52,28 @@ def single(name, nx, ny, bc, order, limiter, steps, seed, use_run):
             "flags": flags, "writes": [wmin, wmax], "steps": steps}
 
 
+def canaries_present():
+    """The check has teeth: after an upload the padding columns and the
+    physical-boundary ghost rows of the device state hold NaN."""
+    from cuda.bindings import runtime as rt
+    name, nx, ny = "shallow-water-roe", 37, 29
+    q, _ = random_state(name, nx, ny, 5)
+    g = device_grid(name, nx, ny, 1.0 / nx, 1.0 / ny, order=2, limiter="mc")
+    try:
+        g.upload(q)
+        g.sync()
+        ptr, pitch, row = g.state_ptr()
+        host = np.empty((ny + 4) * row, dtype=np.float64)
+        (rc,) = rt.cudaMemcpy(host.ctypes.data, ptr, host.nbytes,
+                              rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+        a = host.reshape(ny + 4, 3, pitch)
+        ok = (int(rc) == 0 and np.isnan(a[:, :, nx:]).all() and np.isnan(a[:2]).all() and
+              np.isnan(a[-2:]).all() and not np.isnan(a[2:-2, :, :nx]).any())
+    finally:
+        g.close()
+    return {"case": "canaries present (padding columns, BC ghost rows = NaN)", "ok": bool(ok)}
+
+
 def sharded(name, P, bc, dred, dhalo):
     from test_gpu_multishard import fake_sharded
     nx, ny, steps = 70, 61, 3
@@ -72,7 +94,7 @@ def sharded(name, P, bc, dred, dhalo):
 
 
 def main():
-    results = []
+    results = [canaries_present()]
     solvers = ["advection", "acoustics-const", "acoustics-var", "euler", "euler-hlle",
                "shallow-water-roe"]
     bcs = [("extrapolate", "extrapolate"), ("periodic", "periodic"), ("periodic", "extrapolate")]
