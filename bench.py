@@ -690,7 +690,9 @@ def e2e_leg(g, case, host_q, host_aux, ctl, stream, k):
 def gpu_arm_sharded(args, rank, world, local):
     from paper_1308_1464_b200 import parallel
     return parallel.bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate,
-                                  measured_peak_hbm, METRIC, UNIT)
+                                  measured_peak_hbm, METRIC, UNIT,
+                                  workload_config=workload_config,
+                                  cpu_baseline=cpu_baseline_block)
 
 
 def main():

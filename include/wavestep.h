@@ -182,6 +182,13 @@ int ws_phase_speeds(ws_handle* h, void* stream);
  * flight; part 2 = those y-edges, after they arrived.  part 0 = both. */
 int ws_phase_speeds_part(ws_handle* h, int32_t part, void* stream);
 int ws_phase_update(ws_handle* h, const ws_ctl* c, void* stream);
+/* ws_phase_update in two launches so a shard overlaps its halo exchange with
+ * the update: part 1 = the tile rows holding local rows 0, 1 and ny-2, ny-1
+ * (the rows the neighbours need as ghost rows of the next step), part 2 =
+ * the interior tile rows; the caller sends the new boundary rows after part
+ * 1 while part 2 runs.  Call part 1 then part 2 with the same control; the
+ * step counts as done after part 2.  part 0 == ws_phase_update. */
+int ws_phase_update_part(ws_handle* h, const ws_ctl* c, int32_t part, void* stream);
 /* device pointer of the current step's 3 x uint64 reduction slot */
 void* ws_slot_ptr(ws_handle* h);
 /* device pointers of the current state's halo rows (2 rows x all components,

@@ -672,6 +672,35 @@ int ws_phase_update(ws_handle* h, const ws_ctl* c, void* s) {
   return WS_OK;
 }
 
+int ws_phase_update_part(ws_handle* h, const ws_ctl* c, int32_t part, void* s) {
+  if (!h || !c) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (part == 0) return ws_phase_update(h, c, s);
+  if (part != 1 && part != 2) return fail(h, WS_ERR_CONFIG, "part must be 0, 1 or 2");
+  if (!h->line_kernel || h->fused || !h->multi)
+    return fail(h, WS_ERR_CONFIG, "a split update needs a row-strip shard on the warp-line kernel");
+  int rc = check_ctl(h, c);
+  if (rc) return rc;
+  cudaStream_t st = pick(h, s);
+  const int cur = (int)(h->enq & 1);
+  StepArgs a = make_args(h, c, cur);
+  // the tile rows holding local rows {0, 1} and {ny-2, ny-1}: what the
+  // neighbours read as ghost rows next step
+  const int nty = (h->d.ny + 28) / 29;
+  a.tr_lo = nty < 1 ? nty : 1;
+  a.tr_hi = (h->d.ny - 2) / 29;
+  if (a.tr_hi < a.tr_lo) a.tr_hi = a.tr_lo;
+  a.part = 1;
+  const int n1 = h->ops.update_ctas(h, a);
+  a.part = 2;
+  const int n2 = h->ops.update_ctas(h, a);
+  a.nblk_total = n1 + n2;
+  a.part = part;
+  h->ops.update(h, h->q[cur], h->q[cur ^ 1], a, st);
+  if (part == 2) h->enq++;
+  WS_CUDA(h, launch_status(h));
+  return WS_OK;
+}
+
 void* ws_slot_ptr(ws_handle* h) { return h ? (void*)&h->ds->slot[h->enq & 1][0] : nullptr; }
 
 int ws_halo_ptrs(ws_handle* h, void** slo, void** shi, void** rlo, void** rhi, uint64_t* bytes) {

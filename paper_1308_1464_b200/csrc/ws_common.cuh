@@ -157,6 +157,9 @@ struct StepArgs {
   int static_speeds;    // 1: max speeds come from DevState::static_bits
   int* borders;         // tile-border counters of the fused CFL epilogue
   void* tmax;           // per-tile bound maxima [2][ntiles][4] R for k_speeds_t, or null
+  int part;             // 0 whole step; 1 boundary tile rows; 2 interior tile rows
+  int tr_lo, tr_hi;     // part 1 = tile rows [0, tr_lo) + [tr_hi, nty), part 2 = [tr_lo, tr_hi)
+  int nblk_total;       // CTAs of the whole step over its parts (0: this grid)
 };
 
 __device__ __forceinline__ int map_i(int i, const Layout& L) {

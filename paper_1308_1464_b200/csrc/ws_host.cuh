@@ -40,6 +40,7 @@ struct Ops {
   void (*to_aos)(ws_handle*, const void* cur, const void* gsrc, void* stage, cudaStream_t);
   void (*to_aos_aux)(ws_handle*, void* stage, cudaStream_t);   // aux + BC ghost frame
   void (*canary)(ws_handle*, cudaStream_t);   // checked builds: NaN where nothing may read
+  int (*update_ctas)(ws_handle*, const StepArgs&);   // CTAs of a shard step part
   void (*static_speed)(ws_handle*, cudaStream_t);
   void (*prepare)();   // one-time kernel attributes (never inside a capture)
   int static_speeds;   // solver has q-independent speeds
@@ -297,13 +298,34 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   // one CTA per SM (4-component fp64): persistent CTAs prefetch the next tile
   static constexpr bool PERSIST_W = S::NEQ >= 4 && sizeof(R) == 8;
 
+  // tile rows of a step part (StepArgs::part; 0 = the whole step)
+  static int part_rows(const ws_handle* h, const StepArgs& a) {
+    const int nty = (h->L.ny + 28) / 29;
+    return a.part == 0 ? nty : a.part == 1 ? a.tr_lo + nty - a.tr_hi : a.tr_hi - a.tr_lo;
+  }
+  // CTAs the line kernel launches for a part of a shard's step (no checks,
+  // no fused epilogue: the shard form)
+  static int update_ctas(ws_handle* h, const StepArgs& a) {
+    const int rows = part_rows(h, a);
+    if (rows <= 0) return 0;
+    if constexpr (PERSIST_W) {
+      if (h->persist)
+        return persistent_grid(kern_w<false, false, true>(), LNWP * 32,
+                               LineGeom<S>::template smem_bytes<R>(true), h->L.nx, rows * 29,
+                               29, 29);
+    }
+    return ((h->L.nx + 28) / 29) * rows;
+  }
+
   template <bool CHECKS, bool FUSED> static void update_w(ws_handle* h, const void* q, void* qn,
                                                           const StepArgs& a, cudaStream_t st) {
+    const int rows = part_rows(h, a);
+    if (rows <= 0) return;    // an empty part (a strip of one or two tile rows)
     if constexpr (PERSIST_W && !FUSED) {
       if (h->persist) {
         auto k = kern_w<CHECKS, false, true>();
         const size_t smem = LineGeom<S>::template smem_bytes<R>(true);
-        dim3 grid(persistent_grid(k, LNWP * 32, smem, h->L.nx, h->L.ny, 29, 29));
+        dim3 grid(persistent_grid(k, LNWP * 32, smem, h->L.nx, rows * 29, 29, 29));
         launch(h, k, grid, dim3(LNWP * 32), smem, st, static_cast<const R*>(q),
                static_cast<const R*>(h->aux), static_cast<R*>(qn), h->L, prm(h), a, h->ds);
         h->launches++;
@@ -312,7 +334,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     }
     auto k = kern_w<CHECKS, FUSED>();
     const size_t smem = LineGeom<S>::template smem_bytes<R>(false, FUSED);
-    dim3 grid((h->L.nx + 28) / 29, (h->L.ny + 28) / 29);
+    dim3 grid((h->L.nx + 28) / 29, rows);
     launch(h, k, grid, dim3(LNW * 32), smem, st, static_cast<const R*>(q),
            static_cast<const R*>(h->aux), static_cast<R*>(qn), h->L, prm(h), a, h->ds);
     h->launches++;
@@ -390,6 +412,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     o.to_aos = &to_aos;
     o.to_aos_aux = &to_aos_aux;
     o.canary = &canary;
+    o.update_ctas = &update_ctas;
     o.static_speed = &static_speed;
     o.prepare = &prepare;
     o.static_speeds = S::STATIC_SPEEDS ? 1 : 0;

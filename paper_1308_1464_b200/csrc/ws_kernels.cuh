@@ -1775,8 +1775,22 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   // PERSIST (one CTA per SM, 4-component fp64): CTAs walk the tiles and
   // prefetch the next tile's raw state with cp.async while the current tile
   // computes; otherwise one tile per CTA (blockIdx)
-  const int ntx = (L.nx + LW - 1) / LW, ntiles = ntx * ((L.ny + LW - 1) / LW);
-  int t = PERSIST ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+  const int ntx = (L.nx + LW - 1) / LW, nty = (L.ny + LW - 1) / LW, ntiles = ntx * nty;
+  // row-strip overlap (ws_phase_update_part): part 1 = the boundary tile
+  // rows [0, tr_lo) and [tr_hi, nty) -- every cell a neighbour needs as a
+  // ghost row --, part 2 = the interior tile rows [tr_lo, tr_hi), launched
+  // while the new boundary rows travel; v indexes the tiles of the part
+  const int nvt = ntx * (A.part == 0 ? nty : A.part == 1 ? A.tr_lo + nty - A.tr_hi
+                                                         : A.tr_hi - A.tr_lo);
+  auto vtile = [&](int vv) {
+    int ty = vv / ntx;
+    const int tx = vv - ty * ntx;
+    if (A.part == 1) { if (ty >= A.tr_lo) ty += A.tr_hi - A.tr_lo; }
+    else if (A.part == 2) ty += A.tr_lo;
+    return ty * ntx + tx;
+  };
+  int v = PERSIST ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+  int t = vtile(v);
   auto tile_origin = [&](int tt, int& a, int& b) { a = (tt % ntx) * LW; b = (tt / ntx) * LW; };
   // raw tile + halo -> sR (BC by index mapping), one cp.async group
   auto prefetch = [&](int tt) {
@@ -1813,7 +1827,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   pdl_trigger();
   if (CHECKS) pdl_wait();
   if (PERSIST) {
-    if (t < ntiles) prefetch(t);
+    if (v < nvt) prefetch(t);
     if (tid == NT - 32) {
       if (!CHECKS) pdl_wait();
       if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (A.seq + 1));
@@ -1869,7 +1883,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   };
   for (;;) {
   if (PERSIST) {
-    if (t >= ntiles) break;
+    if (v >= nvt) break;
     cp_wait<0>();
     __syncthreads();   // raw tile landed for every thread; previous tile fully stored
     if constexpr (HasTile<S>::value && !FUSED) {
@@ -1891,7 +1905,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       if (CHECKS) stage_ok = stage_ok && S::cell_ok(qc, ac, pc, P);
     }
     __syncthreads();   // sR consumed: the next tile's copies may land
-    if (t + (int)gridDim.x < ntiles) prefetch(t + (int)gridDim.x);
+    if (v + (int)gridDim.x < nvt) prefetch(vtile(v + (int)gridDim.x));
   } else {
     // ---- stage tile + 2-cell halo (BC by index mapping), per-cell primitives
     const bool inner = i0 >= 2 && i0 + LW + 2 <= L.nx && j0 >= 2 && j0 + LW + 2 <= L.ny;
@@ -2181,7 +2195,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   }
   t_prev = t;
   if (!PERSIST) break;
-  t += gridDim.x;
+  v += gridDim.x;
+  t = vtile(v);
   tile_origin(t, i0, j0);
   }   // tile loop
   if (PERSIST) cp_wait<0>();   // no copy outstanding at exit
@@ -2199,7 +2214,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   __syncthreads();
   if (tid == 0) {
     if (CHECKS) __threadfence();
-    const int nblk = gridDim.x * gridDim.y;
+    // a split step (part 1 + part 2) counts the CTAs of both launches
+    const int nblk = A.nblk_total > 0 ? A.nblk_total : (int)(gridDim.x * gridDim.y);
     const int prev = atomicAdd(&ds->done, 1);
     if (prev == nblk - 1) {
       __threadfence();

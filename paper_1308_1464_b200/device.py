@@ -174,8 +174,14 @@ class DeviceGrid:
         (ws_phase_speeds_part), 0 = whole."""
         self._check(self.lib.ws_phase_speeds_part(self.h, int(part), stream))
 
-    def phase_update(self, ctl: _abi.WsCtl, stream=None):
-        self._check(self.lib.ws_phase_update(self.h, ctypes.byref(ctl), stream))
+    def phase_update(self, ctl: _abi.WsCtl, stream=None, part: int = 0):
+        """Update; part 1/2 = boundary / interior tile rows of a shard
+        (ws_phase_update_part), 0 = whole."""
+        if part == 0:
+            self._check(self.lib.ws_phase_update(self.h, ctypes.byref(ctl), stream))
+        else:
+            self._check(self.lib.ws_phase_update_part(self.h, ctypes.byref(ctl), int(part),
+                                                      stream))
 
     def slot_ptr(self) -> int:
         return self.lib.ws_slot_ptr(self.h)

@@ -1,28 +1,31 @@
 """Row-strip domain decomposition across GPUs (north_star subsystem 4).
 
 The reference has no domain decomposition (a non-goal); the
-north star asks for row strips along j with 2-cell halos.  Each rank owns
-global rows [j0, j1) (ny/P each, the remainder to the first ranks) and runs
-one C-ABI handle on its GPU.  Per time step:
+north star asks for row strips along j with 2-cell halos, the exchange
+overlapped with the interior tile computation.  Each rank owns global rows
+[j0, j1) (ny/P each, the remainder to the first ranks) and runs one C-ABI
+handle on its GPU.  Per time step (host collectives, NCCL):
 
-  1. halo exchange — the first/last two interior rows of every component go
-     to the neighbours' ghost rows (one contiguous block each way, the SoA
-     row layout makes 2 rows x all components contiguous); with periodic y
-     and P > 1 ranks 0 and P-1 are neighbours;
-  2. ws_phase_speeds — local CFL max + admissibility key into a 3 x u64 slot
-     (split around the exchange, below);
-  3. all_reduce(slot, MAX) — speeds are non-negative IEEE bit patterns and
+  1. ws_phase_speeds — local CFL max + admissibility key into a 3 x u64 slot
+     (the ghost rows of the current state are already in place);
+  2. all_reduce(slot, MAX) — speeds are non-negative IEEE bit patterns and
      the slot stores NKEY_MAX - key, so int64 MAX gives the global max speed
      and the globally first inadmissible interface (reference order);
-  4. ws_phase_update — every rank computes the identical dt and updates.
+  3. ws_phase_update_part 1 — every rank computes the identical dt and
+     updates the boundary tile rows (every row a neighbour needs);
+  4. halo exchange of the NEW state — its first/last two rows of every
+     component go to the neighbours' ghost rows (one contiguous block each
+     way: the SoA row layout makes 2 rows x all components contiguous), with
+     periodic y and P > 1 ranks 0 and P-1 are neighbours — while
+  5. ws_phase_update_part 2 updates the interior tile rows; the next step's
+     pre-pass waits for the received rows.
 
+The first step after an upload exchanges the current state's rows once.
 Because the max is order independent and the update is local, an N-rank run
 is bitwise identical to the 1-GPU run (the reference's serial-twin guard,
-bench.py:181-185, becomes the 1-vs-N test).
-
-The pre-pass is split so the halo transfer overlaps it: every edge that
-does not read the incoming ghost rows is probed while they are in flight
-(ws_phase_speeds_part 1), the y-edges of local row 0 after they land (part 2).
+bench.py:181-185, becomes the 1-vs-N test).  The opt-in device collectives
+(``--device-reduce`` / ``--device-halo``) move steps 2 and 4 into the
+kernels over peer memory.
 
 The orchestration is generic over a *shard executor*: ``CudaShard`` (the
 product: device buffers borrowed from torch, NCCL collectives) or any test
@@ -84,9 +87,10 @@ def shard_block(global_field: np.ndarray, j0: int, j1: int) -> np.ndarray:
     return np.asfortranarray(global_field[:, :, j0:j1 + 4])
 
 
-def exchange_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=None):
+def exchange_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=None,
+                   which: str = "current"):
     """Send the 2 boundary rows to each neighbour, receive its rows into ghosts."""
-    finish_halos(shard, post_halos(dist, shard, strips, rank, periodic, group))
+    finish_halos(shard, post_halos(dist, shard, strips, rank, periodic, group, which))
 
 
 def finish_halos(shard, reqs):
@@ -95,10 +99,13 @@ def finish_halos(shard, reqs):
     shard.halo_received()
 
 
-def post_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=None):
-    """Issue the halo sends/receives; returns the requests (finish_halos waits)."""
+def post_halos(dist, shard, strips: RowStrips, rank: int, periodic: bool, group=None,
+               which: str = "current"):
+    """Issue the halo sends/receives of the current state buffer, or of the
+    next one (the state the running update writes); returns the requests
+    (finish_halos waits)."""
     lo, hi = strips.neighbours(rank, periodic)
-    send_lo, send_hi, recv_lo, recv_hi = shard.halo_views()
+    send_lo, send_hi, recv_lo, recv_hi = shard.halo_views(which)
     # Fixed per-peer order (NCCL matches point-to-point ops to one peer in
     # issue order; with periodic P == 2 both neighbours are the same rank):
     # top rows go up first (tag 1, they land in the upper neighbour's recv_lo),
@@ -119,37 +126,44 @@ def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl,
                  device_reduce: bool = False, device_halo: bool = False):
     """One globally consistent time step.
 
-    The halo rows travel while the pre-pass runs on everything that does not
-    read them (all x-edges, y-edges of rows >= 1: part 1); the y-edges of row
-    0 follow once the low ghost rows are in (part 2), then the MAX all-reduce
-    of the slot and the update (which reads both ghost-row pairs).  With
+    Host collectives (the default): the ghost rows of the current state are
+    in place (the previous step sent them; the first step after an upload
+    exchanges them once), so the pre-pass runs whole, the 3-word slot is
+    MAX all-reduced, and the update runs in two launches: the boundary tile
+    rows first (every row a neighbour needs), then -- while their new rows
+    travel to the neighbours -- the interior tile rows.  Later work on the
+    stream waits for the received rows (finish_halos).  With
     ``device_reduce`` (shards set up with ``set_peers``) the all-reduce is
-    done by the kernels themselves over peer memory.
+    done by the kernels themselves over peer memory; with ``device_halo``
+    the update kernels push the halo rows into the neighbours' buffers.
     """
     ctx = getattr(shard, "stream_context", None)
     with ctx() if ctx is not None else contextlib.nullcontext():
-        if device_halo and not getattr(shard, "halos_primed", True):
+        if not getattr(shard, "halos_primed", True):
             # first step after an upload: the ghost rows come from the host
-            # exchange once; every later step's are pushed by the kernels
+            # exchange once; later steps' come with the previous step
             exchange_halos(dist, shard, strips, rank, periodic, group)
             shard.halos_primed = True
+        if device_halo:
+            # the neighbours' update kernels store our ghost rows; part 2 of
+            # the pre-pass waits for them on the device
             shard.phase_speeds_interior()
-        elif device_halo:
-            # the neighbours' update kernels already stored our ghost rows;
-            # part 2 of the pre-pass waits for them on the device
-            shard.phase_speeds_interior()
+            shard.phase_speeds_boundary()
         else:
-            reqs = post_halos(dist, shard, strips, rank, periodic, group)
-            shard.phase_speeds_interior()
-            finish_halos(shard, reqs)
-        shard.phase_speeds_boundary()
+            shard.phase_speeds()
         if not device_reduce:
             slot = shard.slot_view()
             dist.all_reduce(slot, op=dist.ReduceOp.MAX, group=group)
             shard.slot_reduced()
         # (device_reduce: the pre-pass pushed the slot into every shard's and
         # the update waits for all pushes on the device — no host collective)
-        shard.phase_update(ctl)
+        if device_halo:
+            shard.phase_update(ctl)
+            return
+        shard.phase_update_boundary(ctl)
+        reqs = post_halos(dist, shard, strips, rank, periodic, group, which="next")
+        shard.phase_update_interior(ctl)      # overlaps the halo transfer
+        finish_halos(shard, reqs)
 
 
 def decode_slot(slot_words) -> tuple[float, float, int | None]:
@@ -274,13 +288,17 @@ class CudaShard:
         ptrs = [int(hdl.buffer_ptrs[r]) for r in range(hdl.world_size)]
         self.set_peers(ptrs)
 
-    def _current(self):
+    def _current(self, which="current"):
         ptr, pitch, row = self.grid.state_ptr()
-        buf = self.bufs[0] if ptr == self.bufs[0].data_ptr() else self.bufs[1]
-        return buf, row * (8 if self.grid.precision == "f64" else 4)
+        k = 0 if ptr == self.bufs[0].data_ptr() else 1
+        if which == "next":
+            k ^= 1
+        return self.bufs[k], row * (8 if self.grid.precision == "f64" else 4)
 
-    def halo_views(self):
-        buf, rbytes = self._current()
+    def halo_views(self, which="current"):
+        """(send_lo, send_hi, recv_lo, recv_hi) byte views of the current state
+        buffer, or of the next one (the state the running update writes)."""
+        buf, rbytes = self._current(which)
         n = self.ny
         return (buf[2 * rbytes:4 * rbytes], buf[n * rbytes:(n + 2) * rbytes],
                 buf[0:2 * rbytes], buf[(n + 2) * rbytes:(n + 4) * rbytes])
@@ -309,11 +327,66 @@ class CudaShard:
     def phase_update(self, ctl):
         self.grid.phase_update(ctl, stream=self.stream)
 
+    def phase_update_boundary(self, ctl):
+        """Update part 1: the tile rows holding the rows the neighbours need."""
+        self.grid.phase_update(ctl, stream=self.stream, part=1)
+
+    def phase_update_interior(self, ctl):
+        """Update part 2: the interior tile rows (overlaps the halo transfer)."""
+        self.grid.phase_update(ctl, stream=self.stream, part=2)
+
 
 # ---------------------------------------------------------------------------
-# bench.py --gpus N (torchrun): weak scaling of the C2 workload
+# bench.py --gpus N (torchrun): weak (default) or strong scaling
 
-def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_fn, METRIC, UNIT):
+def rank_strip(args, rank, world, strong, build_case, dev):
+    """(case, strips, host q block, host aux block) of this rank.
+
+    C5 (the default): only this rank's rows of the global recipe are made
+    (weak: nx = 16384, ny = 16384 P with 64 P bumps; strong: the 16384^2
+    grid cut in P strips), on the GPU from the host's numpy factors; other
+    configs slice the 1-GPU case (weak: P stacked copies).  The ghost rows a
+    neighbour owns are primed by the first step's exchange; aux (never
+    exchanged) carries its neighbour rows here."""
+    from . import configs
+    size = getattr(args, "size", None)
+    prec = args.precision or "f64"
+    if args.config == "c5":
+        n = size or 16384
+        ny_g = n if strong else n * world
+        strips = RowStrips(ny_g, world)
+        j0, j1 = strips.bounds(rank)
+        case = configs.c5_bumps(n, ny=ny_g, rows=(j0, j1), dtype=prec, device=dev)
+        h = case.meta.pop("h_dev").t().contiguous().cpu().numpy()
+        q = configs._field(3, n, j1 - j0)
+        q[0, 2:-2, 2:-2] = h
+        case.name = "C5-shallow-water-scaling"
+        return case, strips, q, None
+    base = build_case(args.config, precision=args.precision, device=dev, size=size)
+    ny_g = base.ny if strong else base.ny * world
+    strips = RowStrips(ny_g, world)
+    j0, j1 = strips.bounds(rank)
+
+    def block(f):
+        if f is None:
+            return None
+        inner = f[:, :, 2:-2]
+        if strong:
+            g = f.copy(order="F")
+        else:   # P copies stacked along y
+            g = np.zeros((f.shape[0], base.nx + 4, ny_g + 4), order="F")
+            for r in range(world):
+                g[:, :, 2 + r * base.ny:2 + (r + 1) * base.ny] = inner
+        if periodic_rows(base.bc):
+            g[:, :, 0:2] = g[:, :, ny_g:ny_g + 2]
+            g[:, :, ny_g + 2:ny_g + 4] = g[:, :, 2:4]
+        return shard_block(g, j0, j1)
+
+    return base, strips, block(base.q), block(base.aux)
+
+
+def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_fn, METRIC, UNIT,
+                  workload_config=None, cpu_baseline=None):
     import torch
     import torch.distributed as dist
 
@@ -325,37 +398,12 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    base = build_case(args.config, precision=args.precision,
-                      device=torch.device("cuda", local), size=getattr(args, "size", None))
-    prec = base.dtype
     strong = bool(getattr(args, "strong", False))
-    # weak scaling: the per-GPU strip is the 1-GPU workload, strips stacked
-    # along y; strong scaling: the 1-GPU grid itself, cut into row strips
-    ny_g = base.ny if strong else base.ny * world
-    strips = RowStrips(ny_g, world)
+    case, strips, q_block, aux_block = rank_strip(args, rank, world, strong, build_case, dev)
+    prec = args.precision or case.dtype
+    ny_g = strips.ny
     j0, j1 = strips.bounds(rank)
-
-    def stack(f):
-        if f is None or strong:
-            return f
-        g = np.zeros((f.shape[0], base.nx + 4, ny_g + 4), order="F")
-        for r in range(world):
-            g[:, :, 2 + r * base.ny:2 + (r + 1) * base.ny] = f[:, :, 2:-2]
-        return g
-
-    glob, gaux = stack(base.q), stack(base.aux)
-    if strong:
-        glob = np.asfortranarray(glob.copy())
-        gaux = np.asfortranarray(gaux.copy()) if gaux is not None else None
-    if periodic_rows(base.bc):
-        # periodic y: the outermost strips' memory ghost rows wrap around
-        # (static aux rows are never exchanged, so they must be right here)
-        for g in (glob, gaux):
-            if g is not None:
-                g[:, :, 0:2] = g[:, :, ny_g:ny_g + 2]
-                g[:, :, ny_g + 2:ny_g + 4] = g[:, :, 2:4]
-    case = base
-    periodic = base.bc == "periodic"
+    periodic = case.bc == "periodic"
     dhalo = bool(getattr(args, "device_halo", False))
     dred = bool(getattr(args, "device_reduce", False)) or dhalo
     shard = CudaShard(case, strips, rank, dev, periodic, prec, symmetric=dred)
@@ -364,9 +412,9 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     if dhalo:
         shard.enable_device_halo(strips, rank, periodic)
     npdt = np.float64 if prec == "f64" else np.float32
-    host_q = np.asfortranarray(shard_block(glob, j0, j1), dtype=npdt)
-    host_aux = (np.asfortranarray(shard_block(gaux, j0, j1), dtype=npdt)
-                if gaux is not None else None)
+    host_q = np.asfortranarray(q_block, dtype=npdt)
+    host_aux = np.asfortranarray(aux_block, dtype=npdt) if aux_block is not None else None
+    del q_block, aux_block
     shard.upload(host_q, host_aux)
     if dred:
         torch.cuda.synchronize()
@@ -380,25 +428,42 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     res = shard.grid.poll()
     shard.grid.raise_for(res.error)
     k = args.steps
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(k)]
-    l0 = shard.grid.launches()
-    dist.barrier()
-    torch.cuda.synchronize()
-    with Clocks(local) as clk, shard.stream_context():
-        # queued GPU sleep: the host enqueues the whole loop (every op is
-        # asynchronous, NCCL included) so event gaps are device time; flush,
-        # events, kernels and collectives all on the shard's stream
-        torch.cuda._sleep(int(2e6 + 6e5 * k))
-        for i in range(k):
-            flush.zero_()
-            evs[i][0].record()
-            sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred,
-                     device_halo=dhalo)
-            evs[i][1].record()
+
+    def timed(split):
+        """k steps; split: events also around the update (parts 1 + 2)."""
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
+        dist.barrier()
         torch.cuda.synchronize()
-    dist.barrier()
-    ms = sum(a.elapsed_time(b) for a, b in evs)
+        with shard.stream_context():
+            # queued GPU sleep: the host enqueues the whole loop (every op is
+            # asynchronous, NCCL included) so event gaps are device time;
+            # flush, events, kernels and collectives on the shard's stream
+            torch.cuda._sleep(int(2e6 + 6e5 * k))
+            for i in range(k):
+                flush.zero_()
+                evs[i][0].record()
+                if split and not dhalo:
+                    shard.phase_speeds()
+                    if not dred:
+                        dist.all_reduce(shard.slot_view(), op=dist.ReduceOp.MAX)
+                    evs[i][1].record()
+                    shard.phase_update_boundary(ctl)
+                    reqs = post_halos(dist, shard, strips, rank, periodic, which="next")
+                    shard.phase_update_interior(ctl)
+                    evs[i][2].record()
+                    finish_halos(shard, reqs)
+                else:
+                    sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred,
+                                 device_halo=dhalo)
+                evs[i][3].record()
+            torch.cuda.synchronize()
+        dist.barrier()
+        return evs
+
+    l0 = shard.grid.launches()
+    with Clocks(local) as clk:
+        evs = timed(False)
+    ms = sum(e[0].elapsed_time(e[3]) for e in evs)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -407,6 +472,14 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     launches = shard.grid.launches() - l0
     cells = case.nx * ny_g
     value = cells * k / (ms_max / 1e3)
+    upd_ms = None
+    if not dhalo:
+        # the dominant kernel: the update (boundary + interior launches, the
+        # halo sends enqueued between them), event-timed in a second loop
+        evs = timed(True)
+        upd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+        res = shard.grid.poll()
+        shard.grid.raise_for(res.error)
     e2e = None
     if not getattr(args, "no_e2e", False):
         e2e = sharded_e2e(dist, shard, strips, rank, periodic, ctl, host_q, host_aux, k, cells,
@@ -414,26 +487,37 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     if rank == 0:
         peak, kind = peak_fn()
         bpc = configs.bytes_per_cell(case.kernel, prec)
-        achieved = cells / world * bpc / (ms_max / k / 1e3) / 1e9
+        local_cells = case.nx * (j1 - j0)
+        t_kernel = upd_ms if upd_ms else ms_max / k
+        achieved = local_cells * bpc / (t_kernel / 1e3) / 1e9
+        cfg = (workload_config(case, world, strong, ny_total=ny_g) if workload_config else
+               {"workload": case.name, "nx": case.nx, "ny": ny_g})
+        cpu = None
+        if world == 1 and cpu_baseline is not None and not getattr(args, "no_cpu", False):
+            cpu = cpu_baseline(args.config, args, precision=args.precision,
+                               size=getattr(args, "size", None))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k,
             "warmup": args.warmup, "ms_per_step": ms_max / k, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": prec,
             "data": "synthetic",
-            "config": {"workload": (f"{case.name} in {world} strips (strong)" if strong else
-                                    f"{case.name} x{world} strips (weak)"), "kernel": case.kernel,
-                       "nx": case.nx, "ny": ny_g, "limiter": case.limiter, "order": case.order,
-                       "cfl": case.cfl, "parallelism": f"row-strips{world}",
-                       "l2": "flushed between timed steps (512 MiB write)",
-                       "timed_step": ("CFL pre-pass + update with halo rows and the slot reduction "
-                           "done by the kernels over peer memory") if dhalo else
-                          ("halo exchange + CFL pre-pass + device-side slot reduction over "
-                           "peer memory + update") if dred else
-                          "halo exchange + CFL pre-pass + MAX all-reduce + update"},
+            "config": cfg,
+            "measurement": {
+                "parallelism": f"row-strips{world}",
+                "timed_step": ("CFL pre-pass + update with halo rows and the slot reduction "
+                               "done by the kernels over peer memory") if dhalo else
+                              ("CFL pre-pass + device-side slot reduction over peer memory + "
+                               "update (boundary tile rows, halo sends, interior tile rows)")
+                              if dred else
+                              "CFL pre-pass + MAX all-reduce + update (boundary tile rows, "
+                              "then the interior tile rows while the new halo rows travel)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "whole step",
-                         "peak_kind": kind},
-            "cpu_baseline": None,
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": ("k_update_w (boundary + interior launches), rank 0"
+                                    if upd_ms else "whole step"),
+                         "kernel_ms": t_kernel, "peak_kind": kind,
+                         "algorithmic_bytes_per_cell": bpc},
+            "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -74,7 +74,7 @@ def canaries_present():
     return {"case": "canaries present (padding columns, BC ghost rows = NaN)", "ok": bool(ok)}
 
 
-def sharded(name, P, bc, dred, dhalo):
+def sharded(name, P, bc, dred, dhalo, split=False):
     from test_gpu_multishard import fake_sharded
     nx, ny, steps = 70, 61, 3
     dx, dy = 1.0 / nx, 1.0 / ny
@@ -84,12 +84,14 @@ def sharded(name, P, bc, dred, dhalo):
     seen = []
     out, reps, errs, strips = fake_sharded(name, q, aux, nx, ny, dx, dy, P, steps, 2, "mc", bc,
                                            device_reduce=dred, device_halo=dhalo,
-                                           inspect=lambda g: seen.append(g.checked_counts()))
+                                           inspect=lambda g: seen.append(g.checked_counts()),
+                                           split_update=split)
     full = np.concatenate(out, axis=2)
     ok = (np.array_equal(full, oq[:, 2:-2, 2:-2]) and all(e.code == 0 for e in errs) and
           all(r == [x.dt for x in oreps] for r in reps) and
           all(f == 0 and lo == hi == steps for f, lo, hi in seen))
-    return {"case": f"{name} {P} shards {bc} reduce={dred} halo={dhalo}", "ok": bool(ok),
+    return {"case": f"{name} {P} shards {bc} reduce={dred} halo={dhalo} split={split}",
+            "ok": bool(ok),
             "shards": seen}
 
 
@@ -111,6 +113,9 @@ def main():
                                      ("euler-hlle", 3, "extrapolate", True, True),
                                      ("acoustics-var", 2, "periodic", True, True)):
         results.append(sharded(name, P, bc, dred, dhalo))
+    for name, P, bc in (("shallow-water-roe", 3, "periodic"), ("euler-hlle", 2, "extrapolate"),
+                        ("acoustics-var", 4, "periodic")):
+        results.append(sharded(name, P, bc, False, False, split=True))
     for r in results:
         print(json.dumps(r))
     return 0 if all(r["ok"] for r in results) else 1

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 
 def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
-                 device_reduce=False, device_halo=False, inspect=None):
+                 device_reduce=False, device_halo=False, inspect=None, split_update=False):
     import torch
 
     from paper_1308_1464_b200 import _abi
@@ -60,6 +60,38 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
                               None if hi is None else info(hi))
     ctl = _abi.make_ctl(0.9)
     torch.cuda.set_stream(stream)
+
+    def copy_halos(which):
+        views = [sh.halo_views(which) for sh in shards]
+        for r in range(P):
+            lo, hi = strips.neighbours(r, periodic)
+            if hi is not None:
+                views[hi][2].copy_(views[r][1])
+            if lo is not None:
+                views[lo][3].copy_(views[r][0])
+
+    def reduce_slots():
+        slot = shards[0].slot_view().clone()
+        for sh in shards[1:]:
+            slot = torch.maximum(slot, sh.slot_view())
+        for sh in shards:
+            sh.slot_view().copy_(slot)
+
+    if split_update:
+        # the product's sharded_step order: prime the current rows once; per
+        # step the whole pre-pass, the slot reduction, the boundary tile rows,
+        # the NEW state's rows to the neighbours, then the interior tile rows
+        copy_halos("current")
+        for it in range(steps):
+            for sh in shards:
+                sh.phase_speeds()
+            reduce_slots()
+            for sh in shards:
+                sh.phase_update_boundary(ctl)
+            copy_halos("next")
+            for sh in shards:
+                sh.phase_update_interior(ctl)
+        steps = 0
     for it in range(steps):
         # part 1 of the pre-pass runs BEFORE the halo rows are refreshed (the
         # ghost rows still hold the previous step's values): it must not read them
@@ -97,6 +129,29 @@ def fake_sharded(name, gq, gaux, nx, ny, dx, dy, P, steps, order, limiter, bc,
             inspect(sh.grid)
         sh.grid.close()
     return out, reps, errs, strips
+
+
+@pytest.mark.parametrize("name,P,bc", [("shallow-water-roe", 2, "extrapolate"),
+                                       ("shallow-water-roe", 3, "periodic"),
+                                       ("euler-hlle", 3, "periodic"),
+                                       ("acoustics-var", 4, "extrapolate"),
+                                       ("euler", 2, "periodic")])
+def test_split_update_overlap_order_bitwise(name, P, bc):
+    # boundary tile rows -> halo rows of the new state -> interior tile rows
+    # (the host-collective sharded_step): bitwise the single-domain oracle;
+    # the strips (ny = 100 over P) hold 1 to 4 tile rows, so part 2 is empty
+    # on some and the step's CTA count spans both launches
+    nx, ny, steps = 83, 100, 4
+    dx, dy = 1.0 / nx, 1.0 / ny
+    q, aux = random_state(name, nx, ny, 12)
+    oq, oreps = oracle_run(name, q, aux, nx, ny, dx, dy, steps=steps, order=2, limiter="mc",
+                           bc_x=bc, bc_y=bc)
+    out, reps, errs, strips = fake_sharded(name, q, aux, nx, ny, dx, dy, P, steps, 2, "mc", bc,
+                                           split_update=True)
+    assert all(e.code == 0 for e in errs)
+    for r in reps:
+        assert r == [x.dt for x in oreps]
+    assert np.array_equal(np.concatenate(out, axis=2), oq[:, 2:-2, 2:-2])
 
 
 @pytest.mark.parametrize("name,P,bc,order,limiter", [

@@ -45,8 +45,13 @@ class NumpyShard:
         self.solver = O.make_solver(name, **PARAMS[name])
         self.nx, self.order, self.limiter, self.bc = nx, order, limiter, bc
         self.reports, self.error = [], None
+        self.halos_primed = False       # the first step exchanges the current rows
+        self.calls = []
 
-    def halo_views(self):
+    def halo_views(self, which="current"):
+        # the double updates in place: after phase_update_boundary the next
+        # state is self.q itself
+        self.calls.append(f"halo_views:{which}")
         n = self.ny
         self._recv = (torch.zeros(self.q[:, :, 0:2].shape, dtype=torch.float64),
                       torch.zeros(self.q[:, :, 0:2].shape, dtype=torch.float64))
@@ -55,6 +60,7 @@ class NumpyShard:
                 self._recv[0], self._recv[1])
 
     def halo_received(self):
+        self.calls.append("halo_wait")
         n = self.ny
         if self.lo is not None:
             self.q[:, :, 0:2] = self._recv[0].numpy()
@@ -105,6 +111,13 @@ class NumpyShard:
 
     def slot_reduced(self):
         self.msx, self.msy, self.key = PL.decode_slot(self._slot.tolist())
+
+    def phase_update_boundary(self, ctl):
+        self.calls.append("update:boundary")
+        self.phase_update(ctl)           # the double updates everything here
+
+    def phase_update_interior(self, ctl):
+        self.calls.append("update:interior")
 
     def phase_update(self, ctl):
         if self.error is not None:
@@ -197,3 +210,31 @@ def test_inadmissible_cell_on_one_rank_stops_every_rank():
     k = keys.pop()
     d, i, j = k >> 62, (k >> 18) & 0x7FFFF, k & 0x3FFFF
     assert f"{'xy'[d]}-interface (i={i}, j={j})" == str(err).split(":")[0]
+
+
+def _order_worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nx, ny = 12, 10
+    q, aux = random_state("shallow-water-roe", nx, ny, 3)
+    strips = PL.RowStrips(ny, world)
+    sh = NumpyShard(q, aux, strips, rank, "shallow-water-roe", nx, 1 / nx, 1 / ny, 2, "mc",
+                    "extrapolate")
+    for _ in range(2):
+        PL.sharded_step(dist, sh, strips, rank, False, 0.9)
+    with open(os.path.join(outdir, f"o{rank}.pkl"), "wb") as f:
+        pickle.dump(sh.calls, f)
+    dist.destroy_process_group()
+
+
+def test_interior_update_is_issued_while_the_halo_travels():
+    """North-star overlap: after the boundary tile rows, the new rows are
+    posted, the interior update is issued, and only then does the rank wait
+    for the received rows; the first step primes the current state's rows."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_order_worker, args=(2, free_port(), d), nprocs=2, join=True)
+        calls = [pickle.load(open(os.path.join(d, f"o{r}.pkl"), "rb")) for r in range(2)]
+    for c in calls:
+        assert c == ["halo_views:current", "halo_wait",
+                     "update:boundary", "halo_views:next", "update:interior", "halo_wait",
+                     "update:boundary", "halo_views:next", "update:interior", "halo_wait"], c
