@@ -676,8 +676,8 @@ int ws_phase_update_part(ws_handle* h, const ws_ctl* c, int32_t part, void* s) {
   if (!h || !c) return fail(h, WS_ERR_CONFIG, "null argument");
   if (part == 0) return ws_phase_update(h, c, s);
   if (part != 1 && part != 2) return fail(h, WS_ERR_CONFIG, "part must be 0, 1 or 2");
-  if (!h->line_kernel || h->fused || !h->multi)
-    return fail(h, WS_ERR_CONFIG, "a split update needs a row-strip shard on the warp-line kernel");
+  if (!h->line_kernel || h->fused)
+    return fail(h, WS_ERR_CONFIG, "a split update needs the warp-line kernel without the fused epilogue");
   int rc = check_ctl(h, c);
   if (rc) return rc;
   cudaStream_t st = pick(h, s);
