@@ -145,7 +145,7 @@ def workload_config(case, world: int = 1, strong: bool = False, ny_total: int | 
     """The `config` object of the JSON line: identical in both arms."""
     ny = ny_total if ny_total is not None else case.meta.get("ny_full", case.ny)
     wl = case.name
-    if world > 1:
+    if world > 1 or strong:
         wl = f"{case.name} in {world} strips (strong)" if strong else \
              f"{case.name} x{world} strips (weak)"
     return {"workload": wl, "kernel": case.kernel, "nx": case.nx, "ny": ny,

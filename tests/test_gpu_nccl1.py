@@ -73,12 +73,14 @@ def test_bench_force_sharded_line():
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
                WORLD_SIZE="1", LOCAL_RANK="0")
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-sharded",
-                        "--steps", "4", "--warmup", "3"], env=env, capture_output=True,
-                       text=True, timeout=600)
+                        "--config", "c2", "--no-cpu", "--steps", "4", "--warmup", "3"], env=env,
+                       capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     line = json.loads(p.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 1 and line["value"] > 0
-    assert line["config"]["parallelism"] == "row-strips1"
+    assert line["measurement"]["parallelism"] == "row-strips1"
+    assert "interior tile rows" in line["measurement"]["timed_step"]
+    assert line["roofline"]["kernel_ms"] > 0
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
     assert line["gpu_launches"] > 0
 
@@ -103,9 +105,9 @@ def test_bench_force_sharded_device_collective_line(flag, text):
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
                WORLD_SIZE="1", LOCAL_RANK="0")
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-sharded",
-                        flag, "--steps", "4", "--warmup", "3"], env=env,
-                       capture_output=True, text=True, timeout=600)
+                        "--config", "c2", "--no-cpu", flag, "--steps", "4", "--warmup", "3"],
+                       env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     line = json.loads(p.stdout.strip().splitlines()[-1])
-    assert text in line["config"]["timed_step"]
+    assert text in line["measurement"]["timed_step"]
     assert line["value"] > 0 and line["e2e"]["value"] > 0
