@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--strong", action="store_true",
                     help="row-strip path: strong scaling (the 1-GPU grid cut into N strips) "
                          "instead of weak (an N-times taller grid, one 1-GPU strip per rank)")
+    ap.add_argument("--eager", action="store_true",
+                    help="row-strip path: issue every step from Python instead of replaying "
+                         "graphs (ws_run for device collectives, a captured two-step graph "
+                         "with the NCCL calls otherwise)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the row-strip (NCCL) path even with one rank (tests it on 1 GPU)")
     ap.add_argument("--size", type=int, default=None,

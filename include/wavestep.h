@@ -189,6 +189,17 @@ int ws_phase_update(ws_handle* h, const ws_ctl* c, void* stream);
  * 1 while part 2 runs.  Call part 1 then part 2 with the same control; the
  * step counts as done after part 2.  part 0 == ws_phase_update. */
 int ws_phase_update_part(ws_handle* h, const ws_ctl* c, int32_t part, void* stream);
+/* Caller-side graph capture of whole steps of phase calls (a torch CUDA
+ * graph that also holds the NCCL slot all-reduce and halo send/recv): call
+ * ws_capture_begin before capturing the phase calls and ws_capture_end after
+ * it; it returns the steps (must be even: the ping-pong parity repeats) and
+ * kernel launches the captured calls stand for, and rolls this handle's
+ * step and launch counts back, since nothing ran.  After each replay of the
+ * graph, ws_replayed(h, steps, launches) advances them as the calls would
+ * have.  Not a reference interface: the reference steps from Python. */
+int ws_capture_begin(ws_handle* h);
+int ws_capture_end(ws_handle* h, int64_t* steps, int64_t* launches);
+int ws_replayed(ws_handle* h, int64_t steps, int64_t launches);
 /* device pointer of the current step's 3 x uint64 reduction slot */
 void* ws_slot_ptr(ws_handle* h);
 /* device pointers of the current state's halo rows (2 rows x all components,

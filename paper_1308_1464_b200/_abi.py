@@ -90,6 +90,9 @@ SIGNATURES = [
     ("ws_phase_speeds_part", C.c_int, [_P, C.c_int32, _P]),
     ("ws_phase_update", C.c_int, [_P, C.POINTER(WsCtl), _P]),
     ("ws_phase_update_part", C.c_int, [_P, C.POINTER(WsCtl), C.c_int32, _P]),
+    ("ws_capture_begin", C.c_int, [_P]),
+    ("ws_capture_end", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("ws_replayed", C.c_int, [_P, C.c_int64, C.c_int64]),
     ("ws_slot_ptr", _P, [_P]),
     ("ws_halo_ptrs", C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
                                C.POINTER(_P), C.POINTER(C.c_uint64)]),

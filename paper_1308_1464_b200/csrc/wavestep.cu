@@ -200,7 +200,6 @@ StepArgs make_args(ws_handle* h, const ws_ctl* c, int cur) {
   a.has_t_final = !std::isnan(c->t_final); a.t_final = c->t_final;
   a.tol = a.has_t_final ? 1e-14 * std::fmax(1.0, c->t_final) : 0.0;   // driver.py:245
   a.cur = cur;
-  a.seq = h->enq;
   a.static_speeds = (h->ops.static_speeds && !h->multi) ? 1 : 0;
   a.borders = h->borders;
   a.tmax = h->tile_prepass ? h->tmax : nullptr;
@@ -308,6 +307,7 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   }
   if (const char* v = std::getenv("WS_PDL")) h->pdl = std::atoi(v) != 0;
   if (const char* v = std::getenv("WS_PERSIST")) h->persist = std::atoi(v) != 0;
+  if (const char* v = std::getenv("WS_RUN_SMALL")) h->run_small = std::atoi(v) != 0;
   {
     const char* v = std::getenv("WS_FUSE");
     const bool env_on = v && std::atoi(v) != 0, env_off = v && std::atoi(v) == 0;
@@ -701,6 +701,39 @@ int ws_phase_update_part(ws_handle* h, const ws_ctl* c, int32_t part, void* s) {
   return WS_OK;
 }
 
+int ws_capture_begin(ws_handle* h) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (!h->uploaded) return fail(h, WS_ERR_CONFIG, "no state uploaded");
+  if (h->cap_open) return fail(h, WS_ERR_CONFIG, "a capture is already open");
+  h->cap_open = true;
+  h->cap_enq = h->enq;
+  h->cap_launches = h->launches;
+  return WS_OK;
+}
+
+int ws_capture_end(ws_handle* h, int64_t* steps, int64_t* launches) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (!h->cap_open) return fail(h, WS_ERR_CONFIG, "no capture open");
+  h->cap_open = false;
+  const long long ds = h->enq - h->cap_enq, dl = h->launches - h->cap_launches;
+  h->enq = h->cap_enq;
+  h->launches = h->cap_launches;
+  if (ds % 2 != 0)
+    return fail(h, WS_ERR_CONFIG, "a captured graph must hold an even number of steps");
+  if (steps) *steps = ds;
+  if (launches) *launches = dl;
+  return WS_OK;
+}
+
+int ws_replayed(ws_handle* h, int64_t steps, int64_t launches) {
+  if (!h) return fail(h, WS_ERR_CONFIG, "null argument");
+  if (steps < 0 || steps % 2 != 0 || launches < 0)
+    return fail(h, WS_ERR_CONFIG, "replayed steps must be even and >= 0");
+  h->enq += steps;
+  h->launches += launches;
+  return WS_OK;
+}
+
 void* ws_slot_ptr(ws_handle* h) { return h ? (void*)&h->ds->slot[h->enq & 1][0] : nullptr; }
 
 int ws_halo_ptrs(ws_handle* h, void** slo, void** shi, void** rlo, void** rhi, uint64_t* bytes) {
@@ -733,15 +766,20 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
   cudaStream_t st = pick(h, s);
   if ((rc = tfinal_guard(h, c, st))) return rc;
   long long left = nsteps;
+  if (left >= 4) {
+    // small static-speed grid: every step in one cooperative launch
+    const StepArgs a = make_args(h, c, (int)(h->enq & 1));
+    if (a.static_speeds && h->ops.run_small(h, a, (int)left, st)) { h->enq += left; left = 0; }
+  }
   if (left > 0 && (h->enq & 1)) { enqueue_step(h, c, 1, st); h->enq++; left--; }
   if (left >= 4 && h->need_prepass && !h->ops.static_speeds) {
     // keep the one-off pre-pass out of the captured graph
     enqueue_step(h, c, 0, st); h->enq++; left--;
     enqueue_step(h, c, 1, st); h->enq++; left--;
   }
-  // shards with device collectives step without graphs (the arrival counts
-  // they wait for depend on the host's step sequence number)
-  if (left >= 4 && st != nullptr && !h->multi) {
+  // (shards with device collectives replay the same graph: the pushes their
+  // kernels await are counted from DevState::seq on the device)
+  if (left >= 4 && st != nullptr) {
     // two-step graph (parity 0 then 1), cached per (ctl, stream)
     if (!h->gexec || std::memcmp(&h->gctl, c, sizeof(ws_ctl)) != 0 || h->gstream != st) {
       if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }

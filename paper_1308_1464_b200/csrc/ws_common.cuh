@@ -136,6 +136,12 @@ struct DevState {
   long long nrep;                     // reports written (ring index)
   unsigned long long arrive;          // slot pushes received from the shards (device reduce)
   unsigned long long harrive;         // halo-row pushes received from the neighbours
+  unsigned long long mctr[2];         // k_run_small grid barrier per step parity:
+                                      // arrivals (low 32) | arrivals with an error (high 32)
+  long long seq;                      // update kernels committed since upload (skipped
+                                      // steps too): the pushes a shard awaits are
+                                      // counted from it on the device, so whole steps of
+                                      // device-collective shards replay from a graph
   int hsent[2];                       // this step's boundary tiles pushed (low / high side)
   // CFL filter hint (k_speeds_b): per direction, the edge where the previous
   // step's max |s| was found, packed (speed bits >> 29) << 29 | edge index;
@@ -150,7 +156,6 @@ struct DevState {
 
 struct StepArgs {
   double dx, dy;
-  long long seq;        // steps enqueued since upload (device reduce: arrivals to await)
   double cfl, dt_max, fixed_dt, remaining, t_final, tol;
   int has_dt_max, has_fixed, has_remaining, has_t_final;
   int cur;              // slot parity of this step

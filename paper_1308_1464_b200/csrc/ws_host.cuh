@@ -43,6 +43,9 @@ struct Ops {
   int (*update_ctas)(ws_handle*, const StepArgs&);   // CTAs of a shard step part
   void (*static_speed)(ws_handle*, cudaStream_t);
   void (*prepare)();   // one-time kernel attributes (never inside a capture)
+  // ws_run on a small static-speed grid: all steps in one cooperative launch
+  // (k_run_small); returns 0 when it does not apply (nothing launched)
+  int (*run_small)(ws_handle*, const StepArgs&, int nsteps, cudaStream_t);
   int static_speeds;   // solver has q-independent speeds
   int can_fuse_line;   // warp-line kernel has the fused next-step CFL epilogue
   int tile_prepass;    // solver has tile accumulators (S::HAS_TILE)
@@ -95,6 +98,10 @@ struct ws_handle {
   cudaStream_t gstream = nullptr;
   long long launches = 0;
   long long graph_launches = 0;  // kernels per replay of the 2-step graph
+  // ws_capture_begin / _end: the counts before a caller-side capture
+  bool cap_open = false;
+  long long cap_enq = 0, cap_launches = 0;
+  bool run_small = true;        // ws_run: multi-step k_run_small where it applies
   bool fused = false;           // next-step CFL maxima computed in the update epilogue
   bool need_prepass = true;     // fused mode: slot of the current state not yet filled
   int* borders = nullptr;       // tile-border counters of the fused epilogue
@@ -228,7 +235,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
         if (ctas > (long long)nt * spl) ctas = (long long)nt * spl;
         launch(h, k_speeds_t<S, R, NWT>, dim3((unsigned)ctas), dim3(NWT * 32), 0, st,
                static_cast<const R*>(q), static_cast<const R*>(h->aux),
-               static_cast<const int4*>(h->tmax), h->L, prm(h), cur, spl, (long long)h->enq,
+               static_cast<const int4*>(h->tmax), h->L, prm(h), cur, spl,
                h->ds);
       }
     } else if (HasBound<S>::value && !h->speeds_exact) {
@@ -239,7 +246,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
                   part == 2 ? 2 : (h->L.ny + 1 + KC * NW - 1) / (KC * NW));
         launch(h, k_speeds_b<S, R, KC, NW, MB, 6>, grid, dim3(NW * 32), 0, st,
                static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, part,
-               (long long)h->enq, h->ds);
+               h->ds);
       }
     } else {
       // register pre-pass: 8 edge rows per warp, 4 warps per CTA (the best of
@@ -249,7 +256,7 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
                 part == 2 ? 2 : (h->L.ny + 1 + KC * NW - 1) / (KC * NW));
       launch(h, k_speeds_w<S, R, KC, NW, 1, MB>, grid, dim3(NW * 32), 0, st,
              static_cast<const R*>(q), static_cast<const R*>(h->aux), h->L, prm(h), cur, part,
-             (long long)h->enq, h->ds);
+             h->ds);
     }
     h->launches++;
   }
@@ -259,6 +266,9 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
   }
 
   static void prepare() {
+    if constexpr (S::STATIC_SPEEDS)
+      cudaFuncSetAttribute(k_run_small<S, R, ORDER, LIM, NWR>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem());
     const int lsmem = (int)LineGeom<S>::template smem_bytes<R>();
     cudaFuncSetAttribute(kern_w<true, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
     cudaFuncSetAttribute(kern_w<false, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
@@ -404,8 +414,53 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
     }
   }
 
+  // k_run_small: one 30-warp CTA per tile, every tile resident at once
+  static constexpr int NWR = 30;
+  static constexpr size_t small_smem() {
+    return sizeof(R) * (size_t)((S::NEQ + S::NAUX + S::NPR) * 33 * 33 + S::NEQ * 29 * 29);
+  }
+  static int run_small(ws_handle* h, const StepArgs& a, int nsteps, cudaStream_t st) {
+    if constexpr (!S::STATIC_SPEEDS) {
+      return 0;
+    } else {
+      if (h->multi || !h->line_kernel || !h->run_small || (h->trace && !WS_RS_PROF)) return 0;
+      auto k = k_run_small<S, R, ORDER, LIM, NWR>;
+      static int per_sm = -1, sms = 0;
+      if (per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NWR * 32, small_smem()) !=
+            cudaSuccess) {
+          cudaGetLastError();
+          per_sm = 0;
+        }
+      }
+      const long long ntiles = (long long)((h->L.nx + 28) / 29) * ((h->L.ny + 28) / 29);
+      if (per_sm < 1 || ntiles > (long long)per_sm * sms) return 0;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)ntiles);
+      cfg.blockDim = dim3(NWR * 32);
+      cfg.dynamicSmemBytes = small_smem();
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;   // co-residency of every CTA
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t e = cudaLaunchKernelEx(&cfg, k, static_cast<R*>(h->q[0]),
+                                               static_cast<R*>(h->q[1]),
+                                               static_cast<const R*>(h->aux), h->L, prm(h), a,
+                                               nsteps, h->ds);
+      if (e != cudaSuccess && h->launch_err == cudaSuccess) h->launch_err = e;
+      h->launches++;
+      return 1;
+    }
+  }
+
   static Ops ops() {
     Ops o;
+    o.run_small = &run_small;
     o.speeds = &speeds;
     o.update = &update;
     o.to_soa = &to_soa;

@@ -213,7 +213,7 @@ template <class S, class R, int KC, int NWS, int UNR, int MINB>
 __global__ void __launch_bounds__(NWS * 32, MINB)
 k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
            const typename S::template Params<R> P, const int cur, const int part,
-           const long long seq, DevState* __restrict__ ds) {
+           DevState* __restrict__ ds) {
   constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   __shared__ unsigned long long sred[2][NWS];
@@ -228,7 +228,7 @@ k_speeds_w(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
     // device-side halos: the neighbours' updates pushed this step's ghost
     // rows; wait for all of them (the update launched after us stages ghost
     // rows too, so the trigger comes after this wait)
-    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * seq, ds);
+    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * (unsigned long long)__ldcg(&ds->seq), ds);
     __syncthreads();
   }
   pdl_trigger();
@@ -486,7 +486,7 @@ template <class S, class R, int KC, int NWS, int MINB, int RING>
 __global__ void __launch_bounds__(NWS * 32, MINB)
 k_speeds_b(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
            const typename S::template Params<R> P, const int cur, const int part,
-           const long long seq, DevState* __restrict__ ds) {
+           DevState* __restrict__ ds) {
   constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   const R MARGIN = (R)BoundMath::MARGIN;
@@ -496,7 +496,7 @@ k_speeds_b(const R* __restrict__ q, const R* __restrict__ aux, const Layout L,
   const unsigned long long t_start = L.trace ? gtimer() : 0ull;
   pdl_wait();
   if (L.hsides > 0 && part != 1) {
-    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * seq, ds);
+    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * (unsigned long long)__ldcg(&ds->seq), ds);
     __syncthreads();
   }
   pdl_trigger();
@@ -761,7 +761,7 @@ template <class S, class R, int NWT>
 __global__ void __launch_bounds__(NWT * 32, (S::NEQ >= 4 ? 2 : 4))
 k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __restrict__ tmax,
            const Layout L, const typename S::template Params<R> P, const int cur, const int SPL,
-           const long long seq, DevState* __restrict__ ds) {
+           DevState* __restrict__ ds) {
   constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   constexpr int LW = 29, NT = NWT * 32;
@@ -775,7 +775,7 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
     // device-side halos: the neighbours' updates pushed this step's ghost
     // rows; wait for them (the update launched after us stages ghost rows
     // too, so the trigger comes after this wait)
-    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * seq, ds);
+    if (tid == 0) wait_counter(&ds->harrive, (unsigned long long)L.hsides * (unsigned long long)__ldcg(&ds->seq), ds);
     __syncthreads();
   }
   pdl_trigger();
@@ -1014,6 +1014,15 @@ __device__ __forceinline__ void commit_step(DevState* ds, const StepArgs& A, con
   v->hint_acc[A.cur][0] = 0ull; v->hint_acc[A.cur][1] = 0ull;
   // this step's slot is consumed; it is the accumulator of the step after next
   v->slot[A.cur][0] = 0ull; v->slot[A.cur][1] = 0ull; v->slot[A.cur][2] = 0ull;
+  // a skipped step (t_final reached, error, stationary: the same decision on
+  // every shard) stored no rows, but still releases the neighbours once, so
+  // their halo-arrival counts stay hsides x seq
+  if (c.skip) {
+    __threadfence_system();
+    if (L.nds_lo) atomicAdd_system(&L.nds_lo->harrive, 1ull);
+    if (L.nds_hi) atomicAdd_system(&L.nds_hi->harrive, 1ull);
+  }
+  v->seq = v->seq + 1;
   __threadfence();
   v->done = 0;
 }
@@ -1830,7 +1839,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     if (v < nvt) prefetch(t);
     if (tid == NT - 32) {
       if (!CHECKS) pdl_wait();
-      if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (A.seq + 1));
+      if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (unsigned long long)(__ldcg(&ds->seq) + 1));
       const Ctl c0 = step_control<R>(A, ds, !CHECKS);
       s_ctl = c0;
       s_dtd[0] = (R)(c0.dt / A.dx);
@@ -1937,7 +1946,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     // the first warps) while its loads are in flight
     if (tid == NT - 32) {
       if (!CHECKS) pdl_wait();
-      if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (A.seq + 1));
+      if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (unsigned long long)(__ldcg(&ds->seq) + 1));
       const Ctl c0 = step_control<R>(A, ds, !CHECKS);
       s_ctl = c0;
       s_dtd[0] = (R)(c0.dt / A.dx);
@@ -2229,6 +2238,321 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
     if (L.trace) trace_cta(L, 1, t_start);
   }
+}
+
+// --------------------------------------------------------------------------
+// Multi-step form for small grids whose wave speeds are static (acoustics,
+// advection: no CFL pre-pass): ONE cooperative launch runs up to nsteps
+// steps, one CTA per tile (ntiles <= co-resident CTAs), so a step costs one
+// grid barrier instead of one kernel launch (BASELINE C1: 256^2, 81 tiles).
+// NWARP = 30: warps 0..28 own one line of the tile in each pass and stage /
+// store the tile; the last warp evaluates the step control and records the
+// previous step (report, t, counters) while the others work, so neither sits
+// on the critical path.  Every CTA derives the same controls from the same
+// values (static speeds, t advanced by the same fp64 additions as the
+// record), and learns whether an edge of the step was inadmissible from the
+// barrier word.  The arithmetic per cell is k_update_w's (line_edge, the
+// same update expressions): bitwise the same steps.
+//
+// Grid barrier: one 64-bit word per step parity, arrivals in the low half,
+// arrivals that found an inadmissible edge in the high half, added with one
+// release atomic per CTA; a CTA waits (acquire loads) until all arrivals of
+// the step are in.  The next use of a parity's word comes two steps later,
+// after a barrier every CTA must pass, so its high half is this step's.
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_add_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+// step_control with the static speeds, sticky error and t held by the caller
+__device__ __forceinline__ Ctl step_control_local(const StepArgs& A, double msx, double msy,
+                                                  double t, int err) {
+  Ctl c;
+  c.skip = 0; c.stationary = 0; c.finished = 0; c.dt = 0.0; c.msx = msx; c.msy = msy;
+  if (err) { c.skip = 1; c.msx = c.msy = 0.0; return c; }
+  double remaining = A.remaining;
+  int has_rem = A.has_remaining;
+  if (A.has_t_final) {
+    if (!(A.t_final - t > A.tol)) { c.skip = 1; c.finished = 1; return c; }
+    remaining = A.t_final - t;
+    has_rem = 1;
+  }
+  double dt;
+  if (A.has_fixed) {
+    dt = A.fixed_dt;
+  } else {
+    double rate = msx / A.dx + msy / A.dy;
+    if (rate == 0.0) { c.stationary = 1; c.skip = 1; return c; }
+    dt = A.cfl / rate;
+  }
+  if (A.has_dt_max) dt = (A.dt_max < dt) ? A.dt_max : dt;
+  if (has_rem) dt = (remaining < dt) ? remaining : dt;
+  c.dt = dt;
+  return c;
+}
+
+// the control thread's copy of the device counters (only it writes them)
+struct RunCtl {
+  double t, msx, msy;
+  long long steps, nrep, seq;
+  int err;
+  Ctl pend;          // CTA 0: the applied step still to be recorded
+  int pend_cur, have_pend;
+  unsigned a0[2], e0[2], uses[2];   // thread 0: barrier words at launch, uses per parity
+};
+
+#ifndef WS_RS_PROF
+#define WS_RS_PROF 0
+#endif
+
+template <class S, class R, int ORDER, int LIM, int NWARP>
+__global__ void __launch_bounds__(NWARP * 32, 1)
+k_run_small(R* __restrict__ q0, R* __restrict__ q1, const R* __restrict__ aux, const Layout L,
+            const typename S::template Params<R> P, const StepArgs A, const int nsteps,
+            DevState* __restrict__ ds) {
+  constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int LW = 29, HW = 33, HC = HW * HW, NTW = (NWARP - 1) * 32;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  static_assert(NWARP - 1 >= LW, "one line per working warp");
+  static_assert(S::STATIC_SPEEDS, "static wave speeds only (no CFL pre-pass)");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sQ = reinterpret_cast<R*>(smem_raw);
+  R* sA = sQ + NEQ * HC;
+  R* sP = sA + NAUX * HC;
+  R* sX = sP + NPR * HC;          // [NEQ][LW*LW]: q1 after the x pass, then q_new
+  __shared__ Ctl s_ctl;
+  __shared__ R s_dtd[2];
+  __shared__ int s_err;           // 1: an edge of the step was inadmissible; 2: barrier timeout
+  __shared__ RunCtl rc;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const bool ctl_warp = warp == NWARP - 1;
+  const bool ctl_thr = ctl_warp && lane == 0;
+  const bool rec = ctl_thr && blockIdx.x == 0;    // the thread that records the steps
+  const int ntx = (L.nx + LW - 1) / LW;
+  const int i0 = ((int)blockIdx.x % ntx) * LW, j0 = ((int)blockIdx.x / ntx) * LW;
+  const bool inner = i0 >= 2 && i0 + LW + 2 <= L.nx && j0 >= 2 && j0 + LW + 2 <= L.ny;
+  const bool cell_lane = lane >= 1 && lane <= LW;
+  const unsigned nblk = gridDim.x;
+#if WS_RS_PROF
+  const bool prof = L.trace && blockIdx.x == 0 && tid == 0;
+  auto stamp = [&](int st, int k) {
+    if (prof && st * 6 + k < 8 * L.trace_cap) L.trace[st * 6 + k] = gtimer();
+  };
+#else
+  auto stamp = [](int, int) {};
+#endif
+
+  if (ctl_thr) {
+    // values the previous kernel in the stream committed
+    rc.t = __ldcg(&ds->t);
+    rc.msx = (double)Bits<R>::from(__ldcg(&ds->static_bits[0]));
+    rc.msy = (double)Bits<R>::from(__ldcg(&ds->static_bits[1]));
+    rc.steps = __ldcg(&ds->steps);
+    rc.nrep = __ldcg(&ds->nrep);
+    rc.seq = __ldcg(&ds->seq);
+    rc.err = __ldcg(&ds->err);
+    rc.have_pend = 0;
+  }
+  if (tid == 0) {
+    for (int p = 0; p < 2; ++p) {
+      const unsigned long long w = __ldcg(&ds->mctr[p]);
+      rc.a0[p] = (unsigned)w; rc.e0[p] = (unsigned)(w >> 32); rc.uses[p] = 0u;
+    }
+  }
+  // commit_step for one step of this kernel (recording thread only)
+  auto record = [&](const Ctl& c, int cur, int errbit) {
+    if (rc.err == 0) {
+      if (c.finished) {
+        ds->finished = 1;
+      } else if (errbit) {
+        const unsigned long long nk = __ldcg(&ds->slot[cur][2]);
+        ds->err_key = NKEY_MAX - nk; ds->err_step = rc.steps; ds->err = ERR_KERNEL;
+        rc.err = ERR_KERNEL;
+      } else if (c.stationary) {
+        ds->err_step = rc.steps; ds->err = ERR_STATIONARY;
+        rc.err = ERR_STATIONARY;
+      } else {
+        Report r;
+        r.dt = c.dt;
+        r.cfl = c.dt * (c.msx / A.dx + c.msy / A.dy);   // cfl, driver.py:221
+        r.msx = c.msx; r.msy = c.msy;
+        ds->rep[rc.nrep % REPCAP] = r;
+        rc.nrep += 1; rc.steps += 1;
+        rc.t = rc.t + c.dt;
+        ds->nrep = rc.nrep; ds->steps = rc.steps; ds->t = rc.t;
+      }
+    }
+    ds->tmax_ok[cur ^ 1] = 0;
+    ds->slot[cur][0] = 0ull; ds->slot[cur][1] = 0ull; ds->slot[cur][2] = 0ull;
+    rc.seq += 1;
+    ds->seq = rc.seq;
+  };
+
+  for (int st = 0; st < nsteps; ++st) {
+    stamp(st, 0);
+    const int cur = (A.cur + st) & 1;
+    const R* __restrict__ q = cur ? q1 : q0;
+    R* __restrict__ qn = cur ? q0 : q1;
+    bool stage_ok = true;
+    if (ctl_warp) {
+      if (lane == 0) {
+        // this step's control first (the others need it at the next barrier),
+        // then the previous step's record; a pending step is an applied one
+        // (an error or a skip ends the loop), so t moves by its dt
+        const double t_now = (rec && rc.have_pend) ? rc.t + rc.pend.dt : rc.t;
+        const Ctl c0 = step_control_local(A, rc.msx, rc.msy, t_now, rc.err);
+        s_ctl = c0;
+        s_dtd[0] = (R)(c0.dt / A.dx);
+        s_dtd[1] = (R)(c0.dt / A.dy);
+        if (rec && rc.have_pend) { record(rc.pend, rc.pend_cur, 0); rc.have_pend = 0; }
+      }
+    } else {
+      constexpr int NSTG = (HC + NTW - 1) / NTW;
+      R qs[NSTG][NEQ], as[NSTG][NA1];
+#pragma unroll
+      for (int k = 0; k < NSTG; ++k) {
+        const int idx = tid + k * NTW;
+        if (idx < HC) {
+          const int lx = idx % HW, ly = idx / HW;
+          int gi = i0 - 2 + lx, gj = j0 - 2 + ly;
+          if (!inner) { gi = map_i(gi, L); gj = map_j(gj, L); }
+          WS_CHK(L, gi >= 0 && gi < L.nx && row_readable(gj, L), CHK_STAGE_READ);
+          const R* src = q + row_off(gj, L) + gi;
+#pragma unroll
+          for (int c = 0; c < NEQ; ++c) qs[k][c] = __ldcg(src + c * L.pitch);
+          if (NAUX > 0) {
+            const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
+#pragma unroll
+            for (int c = 0; c < NAUX; ++c) as[k][c] = __ldcg(asrc + c * L.pitch);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NSTG; ++k) {
+        const int idx = tid + k * NTW;
+        if (idx < HC) {
+#pragma unroll
+          for (int c = 0; c < NEQ; ++c) sQ[c * HC + idx] = qs[k][c];
+#pragma unroll
+          for (int c = 0; c < NAUX; ++c) sA[c * HC + idx] = as[k][c];
+          R pc[NP1];
+          if (NPR > 0) {
+            prims_fast<S>(qs[k], as[k], P, pc);
+#pragma unroll
+            for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
+          }
+          stage_ok = stage_ok && S::cell_ok(qs[k], as[k], pc, P);
+        }
+      }
+    }
+    const bool tile_clean = __syncthreads_and(stage_ok) != 0;
+    stamp(st, 1);
+    const Ctl ctl = s_ctl;
+    if (ctl.skip) {
+      if (rec) record(ctl, cur, 0);
+      break;
+    }
+    const R dtdx = s_dtd[0], dtdy = s_dtd[1];
+    unsigned long long key = ~0ull;
+    // ---- x pass: warp r walks row r; lane l = x-edge i0-1+l
+    if (!ctl_warp && warp < LW && j0 + warp < L.ny) {
+      const int r = warp;
+      const int cl = (r + 2) * HW + lane, cr = cl + 1;
+      WS_CHK(L, cl >= 0 && cr < HC, CHK_EDGE_SMEM);
+      const int ei = i0 - 1 + lane;
+      R ap[NEQ], amn[NEQ], fl[NEQ], fr[NEQ];
+      line_edge<S, R, ORDER, LIM, true, 1, HC>(sQ, sA, sP, P, L, cl, cr, ei, j0 + r,
+                                               !tile_clean && lane >= 1 && lane <= 30 &&
+                                                   ei <= L.nx,
+                                               dtdx, key, ap, amn, fl, fr);
+      if (cell_lane) {
+        const int c = lane - 1;
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) {
+          const R qc = sQ[m * HC + cr];
+          R v = qc - dtdx * (ap[m] + amn[m]);
+          if (ORDER == 2) v = v - dtdx * (fr[m] - fl[m]);
+          WS_CHK(L, r * LW + c < LW * LW, CHK_X_SMEM);
+          sX[m * (LW * LW) + r * LW + c] = v;
+        }
+      }
+    }
+    __syncthreads();
+    stamp(st, 2);
+    // ---- y pass: warp c walks column c; lane l = y-edge j0-1+l
+    if (!ctl_warp && warp < LW && i0 + warp < L.nx) {
+      const int c = warp;
+      const int cl = lane * HW + c + 2, cr = cl + HW;
+      WS_CHK(L, cl >= 0 && cr < HC, CHK_EDGE_SMEM);
+      const int ej = j0 - 1 + lane;
+      R ap[NEQ], amn[NEQ], fl[NEQ], fr[NEQ];
+      line_edge<S, R, ORDER, LIM, true, 2, HC>(sQ, sA, sP, P, L, cl, cr, i0 + c, ej,
+                                               !tile_clean && lane >= 1 && lane <= 30 &&
+                                                   ej < L.ny_edges_y,
+                                               dtdy, key, ap, amn, fl, fr);
+      const int rr = lane - 1, o = rr * LW + c;
+      WS_CHK(L, !cell_lane || (o >= 0 && o < LW * LW), CHK_X_SMEM);
+      if (cell_lane) {
+#pragma unroll
+        for (int m = 0; m < NEQ; ++m) {
+          R v = sX[m * (LW * LW) + o] - dtdy * (ap[m] + amn[m]);
+          if (ORDER == 2) v = v - dtdy * (fr[m] - fl[m]);
+          sX[m * (LW * LW) + o] = v;
+        }
+      }
+    }
+    __syncthreads();
+    stamp(st, 3);
+    // ---- row-coalesced store of the tile
+    if (!ctl_warp) {
+      for (int idx = tid; idx < LW * LW; idx += NTW) {
+        const int rr = idx / LW, c = idx % LW;
+        const int gi = i0 + c, gj = j0 + rr;
+        if (gi < L.nx && gj < L.ny) {
+          R* dst = qn + row_off(gj, L) + gi;
+#pragma unroll
+          for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = sX[m * (LW * LW) + idx];
+          WS_CHK(L, gi >= 0 && gj >= 0, CHK_STORE);
+          if (WS_CHECKED && L.chk) atomicAdd(&L.chk[1 + (long long)gj * L.nx + gi], 1u);
+        }
+      }
+      if (key != ~0ull) atomicMax(&ds->slot[cur][2], NKEY_MAX - key);
+    }
+    const bool bad = __syncthreads_or(key != ~0ull) != 0;
+    stamp(st, 4);
+    // ---- grid barrier (see above)
+    if (tid == 0) {
+      red_add_release_gpu(&ds->mctr[cur], 1ull + (bad ? (1ull << 32) : 0ull));
+      rc.uses[cur] += 1u;
+      const unsigned need = rc.a0[cur] + rc.uses[cur] * nblk;
+      unsigned long long w;
+      long long spins = 0;
+      int e = 0;
+      while ((int)((unsigned)(w = ld_acquire_gpu(&ds->mctr[cur])) - need) < 0) {
+        if (++spins > (1ll << 26)) { e = 2; break; }
+      }
+      s_err = e ? e : ((unsigned)(w >> 32) != rc.e0[cur] ? 1 : 0);
+    }
+    __syncthreads();
+    stamp(st, 5);
+    if (s_err) {
+      if (rec) {
+        if (s_err == 2) atomicCAS(&ds->err, 0, ERR_WAIT_TIMEOUT);
+        else record(ctl, cur, 1);
+      }
+      break;
+    }
+    if (ctl_thr) {
+      if (rec) { rc.pend = ctl; rc.pend_cur = cur; rc.have_pend = 1; }
+      else rc.t = rc.t + ctl.dt;     // every CTA keeps t in step with the record
+    }
+  }
+  if (rec && rc.have_pend) record(rc.pend, rc.pend_cur, 0);
 }
 
 // checked builds: NaN into every location no kernel may read -- the padding

@@ -183,6 +183,22 @@ class DeviceGrid:
             self._check(self.lib.ws_phase_update_part(self.h, ctypes.byref(ctl), int(part),
                                                       stream))
 
+    def capture_begin(self):
+        """Before the caller captures whole steps of phase calls into its own
+        CUDA graph (ws_capture_begin)."""
+        self._check(self.lib.ws_capture_begin(self.h))
+
+    def capture_end(self) -> tuple[int, int]:
+        """(steps, launches) the captured calls stand for; the handle's
+        counts roll back, nothing ran (ws_capture_end)."""
+        st, ln = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self.lib.ws_capture_end(self.h, ctypes.byref(st), ctypes.byref(ln)))
+        return int(st.value), int(ln.value)
+
+    def replayed(self, steps: int, launches: int):
+        """After each replay of such a graph (ws_replayed)."""
+        self._check(self.lib.ws_replayed(self.h, int(steps), int(launches)))
+
     def slot_ptr(self) -> int:
         return self.lib.ws_slot_ptr(self.h)
 

@@ -166,6 +166,46 @@ def sharded_step(dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl,
         finish_halos(shard, reqs)
 
 
+class StepGraph:
+    """Two whole sharded steps (host collectives: NCCL all-reduce of the slot
+    and the halo send/recv included) captured once into a torch CUDA graph
+    and replayed, so a rank issues one graph launch per two steps instead of
+    four library calls and three collectives per step.  The library's step
+    and launch counts follow the replays (ws_capture_begin / _end,
+    ws_replayed); two steps keep the ping-pong parity of every replay equal
+    to the captured one.  Shards with device collectives (``--device-halo``)
+    need no host call per step at all: they run whole steps through
+    ``DeviceGrid.run`` (ws_run's own two-step graph)."""
+
+    STEPS = 2
+
+    def __init__(self, dist, shard, strips: RowStrips, rank: int, periodic: bool, ctl,
+                 group=None, device_reduce: bool = False):
+        torch = shard.torch
+        self.shard = shard
+        if not getattr(shard, "halos_primed", True):
+            # the first step after an upload primes the ghost rows by a host
+            # exchange, which is not part of the repeated step
+            sharded_step(dist, shard, strips, rank, periodic, ctl, group,
+                         device_reduce=device_reduce)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        shard.grid.capture_begin()
+        try:
+            with torch.cuda.graph(self.graph, stream=shard.torch_stream):
+                for _ in range(self.STEPS):
+                    sharded_step(dist, shard, strips, rank, periodic, ctl, group,
+                                 device_reduce=device_reduce)
+        finally:
+            self.steps, self.launches = shard.grid.capture_end()
+
+    def replay(self):
+        """STEPS more steps, enqueued on the shard's stream."""
+        with self.shard.stream_context():
+            self.graph.replay()
+        self.shard.grid.replayed(self.steps, self.launches)
+
+
 def decode_slot(slot_words) -> tuple[float, float, int | None]:
     """(max_sx, max_sy, first error key or None) from the 3 reduced words."""
     bx, by, nk = (int(w) & ((1 << 64) - 1) for w in slot_words)
@@ -428,6 +468,43 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     res = shard.grid.poll()
     shard.grid.raise_for(res.error)
     k = args.steps
+    # the default issue path: whole steps from graphs (device collectives:
+    # ws_run's own; host collectives: a captured StepGraph of two steps with
+    # the NCCL calls inside); --eager issues every step from Python
+    # (a strip whose state fits twice in the 126 MB L2 steps eagerly: the L2
+    # is flushed between its timed steps, which a replayed graph would not do)
+    esz = 8 if prec == "f64" else 4
+    strip_bytes = host_q.shape[0] * case.nx * (j1 - j0) * esz
+    eager = bool(getattr(args, "eager", False)) or strip_bytes < (256 << 20)
+    whole = dhalo and dred
+    sgraph = None
+    if not eager and not whole:
+        sgraph = StepGraph(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
+
+    def graph_steps(n):
+        """n steps from graphs (one eager step when n is odd)."""
+        if whole:
+            shard.grid.run(n, ctl, stream=shard.stream)
+            return
+        for _ in range(n // 2):
+            sgraph.replay()
+        if n % 2:
+            sharded_step(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
+
+    def timed_graph():
+        """k steps from graphs, one event pair around them (device time)."""
+        e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        dist.barrier()
+        torch.cuda.synchronize()
+        with shard.stream_context():
+            torch.cuda._sleep(int(2e6))
+            flush.zero_()
+            e0.record()
+            graph_steps(k)
+            e1.record()
+            torch.cuda.synchronize()
+        dist.barrier()
+        return e0.elapsed_time(e1)
 
     def timed(split):
         """k steps; split: events also around the update (parts 1 + 2)."""
@@ -462,8 +539,11 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
 
     l0 = shard.grid.launches()
     with Clocks(local) as clk:
-        evs = timed(False)
-    ms = sum(e[0].elapsed_time(e[3]) for e in evs)
+        if eager:
+            evs = timed(False)
+            ms = sum(e[0].elapsed_time(e[3]) for e in evs)
+        else:
+            ms = timed_graph()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -504,6 +584,10 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
             "config": cfg,
             "measurement": {
                 "parallelism": f"row-strips{world}",
+                "issue": ("every step from Python (--eager)" if eager else
+                          "ws_run's two-step graph per rank (device collectives)" if whole else
+                          "a captured torch CUDA graph of two steps per rank (NCCL calls "
+                          "inside), replayed; the strip's state is larger than the L2"),
                 "timed_step": ("CFL pre-pass + update with halo rows and the slot reduction "
                                "done by the kernels over peer memory") if dhalo else
                               ("CFL pre-pass + device-side slot reduction over peer memory + "

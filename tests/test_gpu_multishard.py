@@ -300,3 +300,128 @@ def test_fake_shards_tile_prepass_skips_tiles(bc, dred, dhalo):
         assert errs[r].code == 0
         assert reps[r] == [o.dt for o in oreps]
         assert np.array_equal(out[r], ref[:, 2:-2, 2 + j0:2 + j1]), f"shard {r}"
+
+
+def device_collective_shards(name, gq, gaux, nx, ny, dx, dy, P, bc, halo, order=2, limiter="mc"):
+    """P shards on one GPU, each on its OWN stream, with device collectives
+    (slot reduction, and halo pushes when `halo`): whole steps need no host
+    collective, so ws_run replays its two-step graph per shard and the
+    shards' kernels wait on one another's counters while running
+    concurrently (tiny grids: every CTA of every shard is resident at once)."""
+    import torch
+
+    from paper_1308_1464_b200 import parallel as PL
+    dev = torch.device("cuda", 0)
+    case = SimpleNamespace(kernel=name, kernel_params=PARAMS[name], nx=nx, dx=dx, dy=dy,
+                           order=order, limiter=limiter, bc=bc)
+    periodic = bc == "periodic"
+    gq = np.asfortranarray(gq.copy())
+    O.fill_ghost(gq, bc, bc)
+    if gaux is not None:
+        gaux = np.asfortranarray(gaux.copy())
+        O.fill_ghost(gaux, bc, bc)
+    strips = PL.RowStrips(ny, P)
+    shards = [PL.CudaShard(case, strips, r, dev, periodic) for r in range(P)]
+    for r, sh in enumerate(shards):
+        j0, j1 = strips.bounds(r)
+        # the host block carries the neighbours' rows: ghost rows primed
+        sh.upload(PL.shard_block(gq, j0, j1),
+                  PL.shard_block(gaux, j0, j1) if gaux is not None else None)
+    ptrs = [sh.slots.data_ptr() for sh in shards]
+    for sh in shards:
+        sh.set_peers(ptrs)
+    if halo:
+        for r, sh in enumerate(shards):
+            lo, hi = strips.neighbours(r, periodic)
+            info = lambda k: (shards[k].bufs[0].data_ptr(), shards[k].bufs[1].data_ptr(),  # noqa: E731
+                              shards[k].slots.data_ptr())
+            sh.set_halo_peers(None if lo is None else info(lo) + (shards[lo].ny,),
+                              None if hi is None else info(hi))
+    torch.cuda.synchronize()
+    return shards, strips
+
+
+def collect(shards):
+    import torch
+    torch.cuda.synchronize()
+    out, reps, errs, ts = [], [], [], []
+    for sh in shards:
+        res = sh.grid.poll()
+        reps.append([r[0] for r in res.reports])
+        errs.append(res.error)
+        ts.append(res.t)
+        out.append(sh.grid.download()[:, 2:-2, 2:-2])
+    return out, reps, errs, ts
+
+
+@pytest.mark.parametrize("name,P,bc,halo", [("shallow-water-roe", 3, "periodic", True),
+                                            ("euler-hlle", 2, "extrapolate", True),
+                                            ("euler", 2, "periodic", True),
+                                            ("acoustics-var", 3, "periodic", True)])
+def test_device_collective_shards_run_from_graphs(name, P, bc, halo):
+    # ws_run on every shard (10 steps: the two-step graph replayed), the
+    # arrival counts awaited on the device taken from DevState::seq
+    nx, ny, steps = 45, 70, 10
+    dx, dy = 1 / nx, 1 / ny
+    gq, gaux = random_state(name, nx, ny, 41)
+    ref, oreps = oracle_run(name, gq, gaux, nx, ny, dx, dy, steps=steps, order=2,
+                            limiter="mc", bc_x=bc, bc_y=bc)
+    from paper_1308_1464_b200 import _abi
+    shards, strips = device_collective_shards(name, gq, gaux, nx, ny, dx, dy, P, bc, halo)
+    try:
+        for sh in shards:
+            sh.grid.run(steps, _abi.make_ctl(0.9), stream=sh.stream)
+        out, reps, errs, _ = collect(shards)
+        for r in range(P):
+            j0, j1 = strips.bounds(r)
+            assert errs[r].code == 0, errs[r]
+            assert reps[r] == [o.dt for o in oreps]
+            assert np.array_equal(out[r], ref[:, 2:-2, 2 + j0:2 + j1]), f"shard {r}"
+    finally:
+        for sh in shards:
+            sh.grid.close()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_device_collective_shards_t_final_then_more(P):
+    # a t_final run that stops mid-graph (the skipped steps still release the
+    # neighbours once each, keeping the halo-arrival count at hsides x seq),
+    # then -- after every shard synchronised -- a run to a later t_final
+    from paper_1308_1464_b200 import _abi
+    name, nx, ny, bc = "shallow-water-roe", 45, 70, "periodic"
+    dx, dy = 1 / nx, 1 / ny
+    gq, _ = random_state(name, nx, ny, 43)
+    solver = O.make_solver(name, **PARAMS[name])
+    spec = O.Spec(nx, ny, dx, dy)
+    kw = dict(bc_x=bc, bc_y=bc, order=2, limiter="mc")
+    oq = np.asfortranarray(gq.copy())
+    O.fill_ghost(oq, bc, bc)
+    probe = O.step(np.asfortranarray(oq.copy()), None, spec, solver, O.Controller(0.9), **kw)
+    t1, t2 = 5.41 * probe.dt, 9.83 * probe.dt
+    oreps = O.run(oq, None, spec, solver, O.Controller(0.9), t_final=t1, **kw)
+    n1 = len(oreps)
+    t = sum(r.dt for r in oreps)
+    while t2 - t > 1e-14 * max(1.0, t2):
+        r = O.step(oq, None, spec, solver, O.Controller(0.9), remaining=t2 - t, **kw)
+        oreps.append(r)
+        t += r.dt
+    shards, strips = device_collective_shards(name, gq, None, nx, ny, dx, dy, P, bc, True)
+    try:
+        for sh in shards:
+            sh.grid.run(12, _abi.make_ctl(0.9, t_final=t1), stream=sh.stream)
+        _, reps, errs, ts = collect(shards)
+        for r in range(P):
+            assert errs[r].code == 0, errs[r]
+            assert reps[r] == [o.dt for o in oreps[:n1]]
+        for sh in shards:
+            sh.grid.run(12, _abi.make_ctl(0.9, t_final=t2), stream=sh.stream)
+        out, reps, errs, ts = collect(shards)
+        for r in range(P):
+            j0, j1 = strips.bounds(r)
+            assert errs[r].code == 0, errs[r]
+            assert reps[r] == [o.dt for o in oreps[n1:]]
+            assert abs(ts[r] - t2) <= 1e-14 * max(1.0, t2)
+            assert np.array_equal(out[r], oq[:, 2:-2, 2 + j0:2 + j1]), f"shard {r}"
+    finally:
+        for sh in shards:
+            sh.grid.close()

@@ -111,3 +111,56 @@ def test_bench_force_sharded_device_collective_line(flag, text):
     line = json.loads(p.stdout.strip().splitlines()[-1])
     assert text in line["measurement"]["timed_step"]
     assert line["value"] > 0 and line["e2e"]["value"] > 0
+
+
+@pytest.mark.parametrize("name,bc,device_reduce", [("shallow-water-roe", "extrapolate", False),
+                                                   ("euler-hlle", "periodic", False),
+                                                   ("shallow-water-roe", "periodic", True)])
+def test_nccl_world1_step_graph_replays_bitwise(name, bc, device_reduce):
+    # StepGraph: two sharded steps (NCCL slot all-reduce inside) captured into
+    # a torch CUDA graph, replayed 3 times after 3 eager steps; the library's
+    # step count follows the replays (the state parity of later calls)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1308_1464_b200 import _abi
+    from paper_1308_1464_b200 import parallel as PL
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+                      WORLD_SIZE="1")
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", device_id=dev)
+    try:
+        nx, ny, steps = 53, 47, 10
+        gq, gaux = random_state(name, nx, ny, 33)
+        ref, oreps = oracle_run(name, gq, gaux, nx, ny, 1 / nx, 1 / ny, steps=steps, order=2,
+                                limiter="mc", bc_x=bc, bc_y=bc)
+        case = SimpleNamespace(kernel=name, kernel_params=PARAMS[name], nx=nx, dx=1 / nx,
+                               dy=1 / ny, order=2, limiter="mc", bc=bc)
+        strips = PL.RowStrips(ny, 1)
+        sh = PL.CudaShard(case, strips, 0, dev, bc == "periodic", symmetric=device_reduce)
+        if device_reduce:
+            sh.enable_device_reduce()
+        sh.upload(PL.shard_block(gq, 0, ny))
+        ctl = _abi.make_ctl(0.9)
+        for _ in range(3):                      # odd: the graph starts at parity 1
+            PL.sharded_step(dist, sh, strips, 0, bc == "periodic", ctl,
+                            device_reduce=device_reduce)
+        l0 = sh.grid.launches()
+        g = PL.StepGraph(dist, sh, strips, 0, bc == "periodic", ctl,
+                         device_reduce=device_reduce)
+        assert g.steps == 2 and g.launches >= 4
+        assert sh.grid.launches() == l0         # capture ran nothing
+        for _ in range(3):
+            g.replay()
+        PL.sharded_step(dist, sh, strips, 0, bc == "periodic", ctl, device_reduce=device_reduce)
+        torch.cuda.synchronize()
+        assert sh.grid.launches() == l0 + 3 * g.launches + g.launches // 2
+        res = sh.grid.poll()
+        assert res.error.code == 0
+        assert res.steps_done == steps
+        assert [r[0] for r in res.reports] == [o.dt for o in oreps]
+        out = sh.grid.download()
+        assert np.array_equal(out[:, 2:-2, 2:-2], ref[:, 2:-2, 2:-2])
+        sh.grid.close()
+    finally:
+        dist.destroy_process_group()
