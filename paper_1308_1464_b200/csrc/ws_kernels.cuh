@@ -22,6 +22,9 @@
 #ifndef WS_LB3
 #define WS_LB3 1
 #endif
+#ifndef WS_GAS2
+#define WS_GAS2 1   // 4-component fp64 on 10-warp CTAs, two per SM (0: 15 warps, one, persistent)
+#endif
 
 namespace ws {
 
@@ -1747,7 +1750,8 @@ __device__ __forceinline__ void wait_arrivals(DevState* ds, unsigned long long n
 // back to shared memory, from which the tile is stored row-coalesced.
 template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUSED,
           bool PERSIST = false>
-__global__ void __launch_bounds__(NWARP * 32, ((sizeof(R) == 4 || WS_LB3) && NWARP == 10 ? 3
+__global__ void __launch_bounds__(NWARP * 32, ((sizeof(R) == 4 || WS_LB3) && NWARP == 10
+                                                   ? (S::NEQ >= 4 && sizeof(R) == 8 ? 2 : 3)
                                                    : (20 / NWARP > 0 ? 20 / NWARP : 1)))
 // (10-warp CTAs: three per SM -- 30 warps, <= 64 registers, <= 75 KB of
 // shared memory each; WS_LB3=0 builds the two-per-SM form for comparison.

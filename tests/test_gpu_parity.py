@@ -343,8 +343,9 @@ def test_fp32_c5_recipe_within_stated_bound():
 
 @pytest.mark.parametrize("name,bc", [("euler-hlle", "periodic"), ("euler", "extrapolate")])
 def test_persistent_line_kernel_walks_tiles_bitwise(name, bc):
-    # 4-component fp64 systems run persistent CTAs (one per SM) that prefetch
-    # the next tile with cp.async: > 148 tiles so CTAs walk several tiles
+    # 4-component fp64 systems on 10-warp CTAs, two per SM: 264 tiles, more
+    # than one per SM (the WS_GAS2=0 build: persistent 15-warp CTAs that walk
+    # the tiles, prefetching the next with cp.async)
     _compare(name, 610, 331, 3, 2, "mc", (bc, bc), seed=23)
 
 
