@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--precision", default=None, choices=[None, "f64", "f32"])
+    ap.add_argument("--precision", default=None, choices=[None, "f64", "f32", "f32fast"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

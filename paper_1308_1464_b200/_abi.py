@@ -29,7 +29,7 @@ SOLVER_IDS = {
 }
 LIMITER_IDS = {"none": 0, "minmod": 1, "superbee": 2, "mc": 3}
 BC_IDS = {"periodic": 0, "extrapolate": 1}
-PRECISION_IDS = {"f64": 0, "f32": 1}
+PRECISION_IDS = {"f64": 0, "f32": 1, "f32fast": 2}
 ROWS_MEMORY, ROWS_BC = 0, 1
 
 

@@ -328,7 +328,7 @@ def main(argv=None) -> int:
     ap.add_argument("--cfl", type=float, default=0.9)
     ap.add_argument("--order", type=int, default=1)
     ap.add_argument("--limiter", default="none")
-    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32", "f32fast"])
     ap.add_argument("--out", default=None)
     ap.add_argument("--roofline-out", default=None,
                     help="sidecar CSV with bytes/cell, achieved GB/s and the HBM fraction")

@@ -3,6 +3,7 @@
 Flags that matter for parity: ``--fmad=false`` (no contraction of a*b+c into
 an FMA, so every product and sum rounds like numpy), ``-prec-div=true
 -prec-sqrt=true -ftz=false`` (IEEE division / square root, denormals kept).
+The fp32 throughput mode's units (``ws_inst_fast_*.cu``) use FAST_FLAGS.
 """
 
 from __future__ import annotations
@@ -25,6 +26,12 @@ NVCC_FLAGS = [
     "--fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
     "-Xcompiler", "-fPIC",
 ]
+
+# the fp32 throughput mode's units (ws_inst_fast_*.cu, WS_FP32_FAST): FMA
+# contraction and the approximate division / square root; their parity is a
+# stated bound against fp64, not bits
+FAST_FLAGS = [{"--fmad=false": "--fmad=true", "-prec-div=true": "-prec-div=false",
+               "-prec-sqrt=true": "-prec-sqrt=false"}.get(f, f) for f in NVCC_FLAGS]
 
 
 def nvcc() -> str:
@@ -80,7 +87,8 @@ def _build(OUT: Path, verbose: bool, defines: tuple) -> Path:
 
     def compile_one(src: Path):
         obj = objdir / (src.stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-Xptxas", "-v", "-c",
+        flags = FAST_FLAGS if src.name.startswith("ws_inst_fast_") else NVCC_FLAGS
+        cmd = [nvcc(), *flags, *(f"-D{d}" for d in defines), "-Xptxas", "-v", "-c",
                "-o", str(obj), str(src)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, cmd, res

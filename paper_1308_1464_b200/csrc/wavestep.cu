@@ -139,7 +139,7 @@ int validate(const ws_desc* d, std::string& m) {
   if ((d->bc_x != 0 && d->bc_x != 1) || (d->bc_y != 0 && d->bc_y != 1)) {
     m = "unknown boundary condition"; return WS_ERR_CONFIG;
   }
-  if (d->precision != WS_FP64 && d->precision != WS_FP32) {
+  if (d->precision != WS_FP64 && d->precision != WS_FP32 && d->precision != WS_FP32_FAST) {
     m = "unknown precision"; return WS_ERR_CONFIG;
   }
   // reference grid.py:165-169 (PERIODIC needs n >= num_ghost)
@@ -241,7 +241,7 @@ int ws_buffer_bytes(const ws_desc* d, uint64_t* q_bytes, uint64_t* aux_bytes,
   std::string m;
   int rc = validate(d, m);
   if (rc) return fail(nullptr, rc, m);
-  size_t esz = d->precision == WS_FP32 ? 4 : 8;
+  size_t esz = d->precision == WS_FP64 ? 8 : 4;
   int neq = (d->solver == WS_EULER_ROE || d->solver == WS_EULER_HLLE) ? 4
             : (d->solver == WS_ADVECTION ? 1 : 3);
   int naux = d->solver == WS_ACOUSTICS_VAR ? 2 : 0;
@@ -260,9 +260,9 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   if (rc) return fail(nullptr, rc, m);
   ws_handle* h = new ws_handle();
   h->d = *d;
-  h->esz = d->precision == WS_FP32 ? 4 : 8;
+  h->esz = d->precision == WS_FP64 ? 8 : 4;
   h->multi = d->rows_lo == WS_ROWS_MEMORY || d->rows_hi == WS_ROWS_MEMORY;
-  bool ok = d->precision == WS_FP32 ? bind<float>(h, m) : bind<double>(h, m);
+  bool ok = d->precision == WS_FP64 ? bind<double>(h, m) : bind<float>(h, m);
   if (!ok) { delete h; return fail(nullptr, WS_ERR_CONFIG, m); }
   compute_layout(h);
   cudaError_t e = cudaSetDevice(d->device);

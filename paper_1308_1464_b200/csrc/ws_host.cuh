@@ -495,6 +495,13 @@ Ops ops_euler_roe(int prec, int order, int lim);
 Ops ops_euler_hlle(int prec, int order, int lim);
 Ops ops_shallow_roe(int prec, int order, int lim);
 Ops ops_advection(int prec, int order, int lim);
+// WS_FP32_FAST: Fast<S> kernels from ws_inst_fast_*.cu (own compiler flags)
+Ops ops_fast_acoustics_const(int order, int lim);
+Ops ops_fast_acoustics_var(int order, int lim);
+Ops ops_fast_euler_roe(int order, int lim);
+Ops ops_fast_euler_hlle(int order, int lim);
+Ops ops_fast_shallow_roe(int order, int lim);
+Ops ops_fast_advection(int order, int lim);
 
 // batched pointwise plugin call (ws_riemann), fp64
 int riemann_acoustics_const(const double* p, int dir, long long n, const double* ql,

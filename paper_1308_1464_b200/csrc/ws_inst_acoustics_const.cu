@@ -8,6 +8,7 @@
 namespace wsh {
 
 Ops ops_acoustics_const(int prec, int order, int lim) {
+  if (prec == WS_FP32_FAST) return ops_fast_acoustics_const(order, lim);
   return prec == WS_FP32 ? pick_lim<AcousticsConst, float>(order, lim) : pick_lim<AcousticsConst, double>(order, lim);
 }
 

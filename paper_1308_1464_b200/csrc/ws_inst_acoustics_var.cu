@@ -8,6 +8,7 @@
 namespace wsh {
 
 Ops ops_acoustics_var(int prec, int order, int lim) {
+  if (prec == WS_FP32_FAST) return ops_fast_acoustics_var(order, lim);
   return prec == WS_FP32 ? pick_lim<AcousticsVar, float>(order, lim) : pick_lim<AcousticsVar, double>(order, lim);
 }
 

@@ -7,6 +7,7 @@
 namespace wsh {
 
 Ops ops_advection(int prec, int order, int lim) {
+  if (prec == WS_FP32_FAST) return ops_fast_advection(order, lim);
   return prec == WS_FP32 ? pick_lim<Advection, float>(order, lim)
                          : pick_lim<Advection, double>(order, lim);
 }

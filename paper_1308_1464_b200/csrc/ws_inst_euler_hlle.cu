@@ -8,6 +8,7 @@
 namespace wsh {
 
 Ops ops_euler_hlle(int prec, int order, int lim) {
+  if (prec == WS_FP32_FAST) return ops_fast_euler_hlle(order, lim);
   return prec == WS_FP32 ? pick_lim<EulerHLLE, float>(order, lim) : pick_lim<EulerHLLE, double>(order, lim);
 }
 

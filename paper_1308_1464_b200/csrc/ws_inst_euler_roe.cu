@@ -8,6 +8,7 @@
 namespace wsh {
 
 Ops ops_euler_roe(int prec, int order, int lim) {
+  if (prec == WS_FP32_FAST) return ops_fast_euler_roe(order, lim);
   return prec == WS_FP32 ? pick_lim<EulerRoe, float>(order, lim) : pick_lim<EulerRoe, double>(order, lim);
 }
 

@@ -1,0 +1,10 @@
+// ws_inst_fast_euler_hlle.cu — the fp32 throughput mode (WS_FP32_FAST) of the
+// EulerHLLE plugin: the same kernel templates instantiated for Fast<EulerHLLE>, compiled
+// with --fmad=true -prec-div=false -prec-sqrt=false (build.py FAST_FLAGS).
+#include "ws_host.cuh"
+
+namespace wsh {
+
+Ops ops_fast_euler_hlle(int order, int lim) { return pick_lim<Fast<EulerHLLE>, float>(order, lim); }
+
+}  // namespace wsh

@@ -8,6 +8,7 @@
 namespace wsh {
 
 Ops ops_shallow_roe(int prec, int order, int lim) {
+  if (prec == WS_FP32_FAST) return ops_fast_shallow_roe(order, lim);
   return prec == WS_FP32 ? pick_lim<ShallowRoe, float>(order, lim) : pick_lim<ShallowRoe, double>(order, lim);
 }
 

@@ -652,6 +652,13 @@ struct Advection {
 };
 
 // ---------------------------------------------------------------------------
+// the fp32 throughput mode (WS_FP32_FAST): the same plugin, a distinct type
+// so its kernels -- compiled in ws_inst_fast_*.cu with FMA contraction and
+// approximate division / square root -- never share a symbol with the
+// bitwise fp32 kernels
+template <class S> struct Fast : S {};
+
+// ---------------------------------------------------------------------------
 // wave limiters (oracle phi(); LeVeque 2002 §6.9)
 template <int LIM, class R> __device__ __forceinline__ R limiter_phi(R th) {
   if (LIM == LIM_MINMOD) return nmax((R)0, nmin((R)1, th));
