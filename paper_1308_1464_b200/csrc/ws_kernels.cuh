@@ -22,6 +22,9 @@
 #ifndef WS_LB3
 #define WS_LB3 1
 #endif
+#ifndef WS_F32_MINB
+#define WS_F32_MINB 4   // fp32 10-warp line-kernel CTAs per SM, 1-3 components (48 registers)
+#endif
 #ifndef WS_GAS2
 #define WS_GAS2 1   // 4-component fp64 on 10-warp CTAs, two per SM (0: 15 warps, one, persistent)
 #endif
@@ -1751,10 +1754,13 @@ __device__ __forceinline__ void wait_arrivals(DevState* ds, unsigned long long n
 template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUSED,
           bool PERSIST = false>
 __global__ void __launch_bounds__(NWARP * 32, ((sizeof(R) == 4 || WS_LB3) && NWARP == 10
-                                                   ? (S::NEQ >= 4 && sizeof(R) == 8 ? 2 : 3)
+                                                   ? (S::NEQ >= 4 ? (sizeof(R) == 8 ? 2 : 3)
+                                                      : sizeof(R) == 4 ? WS_F32_MINB : 3)
                                                    : (20 / NWARP > 0 ? 20 / NWARP : 1)))
 // (10-warp CTAs: three per SM -- 30 warps, <= 64 registers, <= 75 KB of
-// shared memory each; WS_LB3=0 builds the two-per-SM form for comparison.
+// shared memory each; four per SM for fp32 up to 3 components (48
+// registers, 36 KB); two for 4-component fp64 (111 KB); WS_LB3=0 builds the
+// two-per-SM form for comparison.
 // Measured and dropped for 3-component fp64: the persistent prefetching
 // form at one 15-warp CTA per SM (-18 %) and at two (-19 % on C5))
 k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ qn,
