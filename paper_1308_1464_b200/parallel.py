@@ -478,8 +478,19 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
     eager = bool(getattr(args, "eager", False)) or strip_bytes < (256 << 20)
     whole = dhalo and dred
     sgraph = None
+    graph_note = None
     if not eager and not whole:
-        sgraph = StepGraph(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
+        try:
+            sgraph = StepGraph(dist, shard, strips, rank, periodic, ctl, device_reduce=dred)
+        except Exception as e:  # noqa: BLE001 - capture of the NCCL P2P calls refused
+            # (verified at world size 1 only): every rank steps eagerly instead
+            graph_note = f"graph capture failed ({type(e).__name__}: {e}); eager"
+        ok = torch.tensor([0 if sgraph is None else 1], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            sgraph = None
+            eager = True
+            graph_note = graph_note or "graph capture failed on another rank; eager"
 
     def graph_steps(n):
         """n steps from graphs (one eager step when n is odd)."""
@@ -584,7 +595,8 @@ def bench_sharded(args, rank, world, local, build_case, Clocks, cpu_rate, peak_f
             "config": cfg,
             "measurement": {
                 "parallelism": f"row-strips{world}",
-                "issue": ("every step from Python (--eager)" if eager else
+                "issue": (graph_note if graph_note else
+                          "every step from Python (--eager)" if eager else
                           "ws_run's two-step graph per rank (device collectives)" if whole else
                           "a captured torch CUDA graph of two steps per rank (NCCL calls "
                           "inside), replayed; the strip's state is larger than the L2"),
