@@ -298,7 +298,8 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
 
   // warps per CTA of the warp-line kernel: 29 lines / 10 ~ 97 % at 2 CTAs/SM;
   // 4-component systems stage 141 KB (fp64) -> 1 CTA/SM of 15 warps (97 %)
-  static constexpr int LNW = (S::NEQ >= 4 && sizeof(R) == 8 && !WS_GAS2) ? 15 : 10;
+  static constexpr int LNW = (S::NEQ >= 4 && sizeof(R) == 8 && !WS_GAS2) ? 15
+                             : (S::NEQ <= 3 && sizeof(R) == 8) ? WS_LNW3 : 10;
   static constexpr bool CAN_FUSE = !S::STATIC_SPEEDS && S::NAUX == 0 && S::NPR <= S::NEQ;
   // persistent form: one CTA of 15 warps per SM (29 lines / 15 ~ 97 %)
   static constexpr int LNWP = 15;

@@ -22,6 +22,9 @@
 #ifndef WS_LB3
 #define WS_LB3 1
 #endif
+#ifndef WS_LNW3
+#define WS_LNW3 10   // warps per line-kernel CTA for 1-3 component systems
+#endif
 #ifndef WS_F32_MINB
 #define WS_F32_MINB 4   // fp32 10-warp line-kernel CTAs per SM, 1-3 components (48 registers)
 #endif
@@ -1756,6 +1759,7 @@ template <class S, class R, int ORDER, int LIM, int NWARP, bool CHECKS, bool FUS
 __global__ void __launch_bounds__(NWARP * 32, ((sizeof(R) == 4 || WS_LB3) && NWARP == 10
                                                    ? (S::NEQ >= 4 ? (sizeof(R) == 8 ? 2 : 3)
                                                       : sizeof(R) == 4 ? WS_F32_MINB : 3)
+                                                   : NWARP == 15 && S::NEQ <= 3 ? 2
                                                    : (20 / NWARP > 0 ? 20 / NWARP : 1)))
 // (10-warp CTAs: three per SM -- 30 warps, <= 64 registers, <= 75 KB of
 // shared memory each; four per SM for fp32 up to 3 components (48

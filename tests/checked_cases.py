@@ -52,6 +52,36 @@ def single(name, nx, ny, bc, order, limiter, steps, seed, use_run):
             "flags": flags, "writes": [wmin, wmax], "steps": steps}
 
 
+def single_fast(name, nx, ny, bc, steps, seed):
+    """The fp32 throughput mode (f32fast): no index violation, one write per
+    cell and step, and the stated bound (rel <= 1e-5) against fp64."""
+    from paper_1308_1464_b200 import DeviceGrid, _abi, make_kernel
+    dx, dy = 1.0 / nx, 1.3 / ny
+    q, aux = random_state(name, nx, ny, seed)
+    oq, oreps = oracle_run(name, q, aux, nx, ny, dx, dy, steps=steps, order=2, limiter="mc",
+                           bc_x=bc, bc_y=bc)
+    g = DeviceGrid(nx, ny, dx, dy, make_kernel(name, **PARAMS[name]), order=2, limiter="mc",
+                   bc_x=bc, bc_y=bc, precision="f32fast")
+    try:
+        g.upload(np.asfortranarray(q, dtype=np.float32),
+                 np.asfortranarray(aux, dtype=np.float32) if aux is not None else None)
+        g.run(steps, _abi.make_ctl(0.9))
+        res = g.poll()
+        out = g.download().astype(np.float64)
+        flags, wmin, wmax = g.checked_counts()
+    finally:
+        g.close()
+    a, b = out[:, 2:-2, 2:-2], oq[:, 2:-2, 2:-2]
+    rel = max(float(np.abs(a[c] - b[c]).max() / max(np.abs(b[c]).max(), 1e-300))
+              for c in range(b.shape[0]))
+    dts = np.array([r[0] for r in res.reports])
+    drel = float(np.abs(dts / np.array([r.dt for r in oreps]) - 1).max())
+    ok = (res.error.code == 0 and res.steps_done == steps and rel <= 1e-5 and drel <= 1e-5 and
+          flags == 0 and wmin == wmax == steps)
+    return {"case": f"f32fast {name} {nx}x{ny} {bc}", "ok": bool(ok), "flags": flags,
+            "writes": [wmin, wmax], "rel": rel, "dt_rel": drel}
+
+
 def canaries_present():
     """The check has teeth: after an upload the padding columns and the
     physical-boundary ghost rows of the device state hold NaN."""
@@ -108,6 +138,14 @@ def main():
     for nx, ny in ((1, 1), (2, 3), (5, 1), (33, 17), (610, 97)):
         results.append(single("shallow-water-roe", nx, ny, ("extrapolate", "extrapolate"), 2,
                               "mc", 3, 4, False))
+    # k_run_small (ws_run >= 4 steps on a static-speed grid): 81 tiles, one launch
+    results.append(single("acoustics-const", 256, 256, ("extrapolate", "extrapolate"), 2, "mc",
+                          12, 5, True))
+    results.append(single("acoustics-var", 100, 90, ("periodic", "periodic"), 2, "superbee",
+                          7, 6, True))
+    for name, bc in (("shallow-water-roe", "extrapolate"), ("euler-hlle", "periodic"),
+                     ("acoustics-var", "extrapolate")):
+        results.append(single_fast(name, 131, 75, bc, 6, 8))
     for name, P, bc, dred, dhalo in (("shallow-water-roe", 2, "extrapolate", False, False),
                                      ("shallow-water-roe", 3, "periodic", True, False),
                                      ("euler-hlle", 3, "extrapolate", True, True),
