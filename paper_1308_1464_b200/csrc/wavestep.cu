@@ -635,7 +635,11 @@ int ws_step(ws_handle* h, const ws_ctl* c, void* s) {
   if (rc) return rc;
   cudaStream_t st = pick(h, s);
   if ((rc = tfinal_guard(h, c, st))) return rc;
-  enqueue_step(h, c, (int)(h->enq & 1), st);
+  // a small static-speed grid: the step as one launch of k_run_small (one
+  // 30-warp CTA per tile: a line per warp instead of three)
+  const StepArgs a = make_args(h, c, (int)(h->enq & 1));
+  if (!(a.static_speeds && h->ops.run_small(h, a, 1, st)))
+    enqueue_step(h, c, (int)(h->enq & 1), st);
   h->enq++;
   WS_CUDA(h, launch_status(h));
   return WS_OK;
@@ -766,7 +770,7 @@ int ws_run(ws_handle* h, int32_t nsteps, const ws_ctl* c, void* s) {
   cudaStream_t st = pick(h, s);
   if ((rc = tfinal_guard(h, c, st))) return rc;
   long long left = nsteps;
-  if (left >= 4) {
+  if (left >= 1) {
     // small static-speed grid: every step in one cooperative launch
     const StepArgs a = make_args(h, c, (int)(h->enq & 1));
     if (a.static_speeds && h->ops.run_small(h, a, (int)left, st)) { h->enq += left; left = 0; }
