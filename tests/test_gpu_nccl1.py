@@ -164,3 +164,38 @@ def test_nccl_world1_step_graph_replays_bitwise(name, bc, device_reduce):
         sh.grid.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_capture_api_validation():
+    # ws_capture_end rolls the counts back and refuses an odd step count;
+    # ws_replayed refuses odd / negative counts
+    import torch
+    from helpers import device_grid
+    from paper_1308_1464_b200 import _abi
+    name = "shallow-water-roe"
+    q, _ = random_state(name, 40, 30, 3)
+    g = device_grid(name, 40, 30, 1 / 40, 1 / 30, order=2, limiter="mc")
+    try:
+        s = torch.cuda.Stream()
+        g.upload(q, stream=s.cuda_stream)     # every call of the handle on s
+        torch.cuda.synchronize()
+        with pytest.raises(ValueError, match="no capture open"):
+            g.capture_end()
+        ctl = _abi.make_ctl(0.9)
+        l0 = g.launches()
+        g.capture_begin()
+        with pytest.raises(ValueError, match="already open"):
+            g.capture_begin()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            g.phase_speeds(stream=s.cuda_stream)
+            g.phase_update(ctl, stream=s.cuda_stream)
+        with pytest.raises(ValueError, match="even number of steps"):
+            g.capture_end()
+        assert g.launches() == l0            # rolled back although refused
+        with pytest.raises(ValueError, match="even and >= 0"):
+            g.replayed(1, 2)
+        with pytest.raises(ValueError, match="even and >= 0"):
+            g.replayed(-2, 0)
+    finally:
+        g.close()
