@@ -18,7 +18,7 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 SOURCES = [CSRC / "wavestep.cu"] + sorted(CSRC.glob("ws_inst_*.cu"))
 OUT = HERE / "_lib" / "libwavestep.so"
-DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [HERE.parent / "include" / "wavestep.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [HERE.parent / "include" / "wavestep.h", Path(__file__).resolve()]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -28,10 +28,13 @@ NVCC_FLAGS = [
 ]
 
 # the fp32 throughput mode's units (ws_inst_fast_*.cu, WS_FP32_FAST): FMA
-# contraction and the approximate division / square root; their parity is a
-# stated bound against fp64, not bits
+# contraction, the approximate division / square root and denormals flushed
+# to zero (division = MUFU.RCP + FMUL with one range fix-up, square root and
+# reciprocal = one MUFU); their parity is a stated bound against fp64, not
+# bits
 FAST_FLAGS = [{"--fmad=false": "--fmad=true", "-prec-div=true": "-prec-div=false",
-               "-prec-sqrt=true": "-prec-sqrt=false"}.get(f, f) for f in NVCC_FLAGS]
+               "-prec-sqrt=true": "-prec-sqrt=false", "-ftz=false": "-ftz=true"}.get(f, f)
+              for f in NVCC_FLAGS]
 
 
 def nvcc() -> str:
