@@ -52,8 +52,8 @@ enum ws_bc { WS_BC_PERIODIC = 0, WS_BC_EXTRAPOLATE = 1 };  /* grid.py:12-16 */
  * FMA contraction, IEEE division / square root).  WS_FP32_FAST: the fp32
  * throughput mode -- FMA contraction, the approximate MUFU division /
  * square root, denormals flushed to zero; its parity is the stated bound
- * against fp64 (max relative
- * error <= 1e-5 on the state and on every dt after 20 steps), not bits. */
+ * against fp64 (max relative error <= 1e-5 on the state and on every dt
+ * after 20 steps), not bits. */
 enum ws_precision { WS_FP64 = 0, WS_FP32 = 1, WS_FP32_FAST = 2 };
 /* how the rows below j = 0 / above j = ny of THIS shard are obtained */
 enum ws_rowmode { WS_ROWS_MEMORY = 0,   /* ghost rows in memory (halo exchange) */
