@@ -453,7 +453,13 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
                                                static_cast<R*>(h->q[1]),
                                                static_cast<const R*>(h->aux), h->L, prm(h), a,
                                                nsteps, h->ds);
-      if (e != cudaSuccess && h->launch_err == cudaSuccess) h->launch_err = e;
+      if (e != cudaSuccess) {
+        // refused (e.g. the co-resident grid does not fit beside other work
+        // on the device): nothing was enqueued, the caller takes the
+        // per-step path
+        cudaGetLastError();
+        return 0;
+      }
       h->launches++;
       return 1;
     }
