@@ -325,8 +325,11 @@ int ws_create(const ws_desc* d, ws_handle** out) {
   // whole-tile CFL pre-pass (k_speeds_t): the update stores per-tile bound
   // maxima of the state it writes, the next pre-pass skips tiles that cannot
   // hold the step's maximum (WS_SPEEDS=exact|edge|smem select the others)
+  // (a static-speed solver needs it only as a row-strip shard: its single
+  // domain checks admissibility inside the update)
   h->tile_prepass = h->ops.tile_prepass && h->line_kernel && !h->fused &&
-                    !h->speeds_exact && !h->speeds_smem && !h->speeds_edge;
+                    !h->speeds_exact && !h->speeds_smem && !h->speeds_edge &&
+                    (!h->ops.static_speeds || h->multi);
   if (h->tile_prepass) {
     const size_t nt = (size_t)((d->nx + 28) / 29) * ((d->ny + 28) / 29);
     // [2][nt][nacc] int tile accumulators (S::tile_acc), one set per state buffer
@@ -655,8 +658,10 @@ int ws_phase_speeds_part(ws_handle* h, int32_t part, void* s) {
     // split pre-pass only exists for the dynamic-speed, unfused path (shards)
     return fail(h, WS_ERR_CONFIG, "split CFL pre-pass needs a dynamic-speed, unfused handle");
   }
-  // single-shard dynamic solvers probe the next state in the update epilogue
-  if (!h->fused || h->need_prepass)
+  // single-shard dynamic solvers probe the next state in the update epilogue;
+  // a static-speed single domain needs no pre-pass (speeds fixed at upload,
+  // admissibility checked by the update: the whole-step path)
+  if ((!h->fused || h->need_prepass) && !(h->ops.static_speeds && !h->multi))
     h->ops.speeds(h, h->q[h->enq & 1], (int)(h->enq & 1), part, st);
   if (part != 1) h->need_prepass = false;
   WS_CUDA(h, launch_status(h));

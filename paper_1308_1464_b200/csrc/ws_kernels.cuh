@@ -792,8 +792,17 @@ k_speeds_t(const R* __restrict__ q, const R* __restrict__ aux, const int4* __res
   if (tid == 0) {
     const int fl = __ldcg(&ds->err) | __ldcg(&ds->finished);
     const int ok = __ldcg(&ds->tmax_ok[cur]);
-    const R t0 = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][0])), Bits<R>::from(__ldcg(&ds->slot[cur][0])));
-    const R t1 = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][1])), Bits<R>::from(__ldcg(&ds->slot[cur][1])));
+    R t0, t1;
+    if constexpr (S::STATIC_SPEEDS) {
+      // a static-speed shard: its maxima are the upload's (the slot carries
+      // them to the reduction); only tiles holding a bad cell are probed
+      const unsigned long long b0 = __ldcg(&ds->static_bits[0]), b1 = __ldcg(&ds->static_bits[1]);
+      if (blockIdx.x == 0 && !fl) { atomicMax(&ds->slot[cur][0], b0); atomicMax(&ds->slot[cur][1], b1); }
+      t0 = Bits<R>::from(b0); t1 = Bits<R>::from(b1);
+    } else {
+      t0 = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][0])), Bits<R>::from(__ldcg(&ds->slot[cur][0])));
+      t1 = nmax(Bits<R>::from(__ldcg(&ds->tnext[cur][1])), Bits<R>::from(__ldcg(&ds->slot[cur][1])));
+    }
     s_ok = fl ? -1 : ok;
     s_t[0] = t0; s_t[1] = t1;
     s_cnt = 0;
@@ -1877,7 +1886,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       for (int w = 1; w < NWARP; ++w) v = mn ? min(v, s_acc[tid][w]) : max(v, s_acc[tid][w]);
       static_cast<int*>(A.tmax)[((long long)(A.cur ^ 1) * ntiles + tt) * NA + tid] = v;
     }
-    if (tid == 0 || tid == 32) {
+    // (static speeds: no hint edge, its probe would need aux)
+    if (!S::STATIC_SPEEDS && (tid == 0 || tid == 32)) {
       const int d = tid >> 5;
       const int o = s_hown[d] == tt ? s_hoff[d] : -1;
       if (o >= 0) {

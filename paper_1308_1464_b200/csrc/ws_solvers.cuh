@@ -58,6 +58,26 @@ template <class R> __device__ __forceinline__ bool bad_pos(R v) { return !(v > f
 struct AcousticsConst {
   static constexpr int NEQ = 3, NW = 2, NAUX = 0, NPR = 0;
   static constexpr bool STATIC_SPEEDS = true;
+  // Tile form for row-strip shards (k_speeds_t): the speeds are static, so a
+  // tile only needs probing if one of its new cells is inadmissible (then
+  // the checked probe finds the reference-order first interface); a[0] =
+  // "some cell is not finite" over the tile.  Aux is static: the first
+  // pre-pass after an upload probes every tile.
+  static constexpr bool HAS_TILE = true;
+  static constexpr int NACC = 4;
+  static constexpr unsigned ACC_MIN = 0x0u;
+  __device__ static __forceinline__ void acc_init(int (&a)[NACC]) {
+    a[0] = 0; a[1] = 0; a[2] = 0; a[3] = 0;
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_acc(const R* q, const P&, int (&a)[NACC]) {
+    a[0] = max(a[0], all_finite<R, NEQ>(q) ? 0 : 1);
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_bound(const int (&a)[NACC], const P&, R& bndx,
+                                                    R& bndy) {
+    bndx = bndy = a[0] ? (R)INFINITY : (R)0;
+  }
   // structurally zero wave components (skipped by the limiter; adding the
   // oracle's exact zeros would not change any value)
   template <int NI> __host__ __device__ static constexpr bool wzero(int, int m) { return m == 3 - NI; }
@@ -109,6 +129,26 @@ struct AcousticsConst {
 struct AcousticsVar {
   static constexpr int NEQ = 3, NW = 2, NAUX = 2, NPR = 1;  // pr[0] = Z = rho*c
   static constexpr bool STATIC_SPEEDS = true;
+  // Tile form for row-strip shards (k_speeds_t): the speeds are static, so a
+  // tile only needs probing if one of its new cells is inadmissible (then
+  // the checked probe finds the reference-order first interface); a[0] =
+  // "some cell is not finite" over the tile.  Aux is static: the first
+  // pre-pass after an upload probes every tile.
+  static constexpr bool HAS_TILE = true;
+  static constexpr int NACC = 4;
+  static constexpr unsigned ACC_MIN = 0x0u;
+  __device__ static __forceinline__ void acc_init(int (&a)[NACC]) {
+    a[0] = 0; a[1] = 0; a[2] = 0; a[3] = 0;
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_acc(const R* q, const P&, int (&a)[NACC]) {
+    a[0] = max(a[0], all_finite<R, NEQ>(q) ? 0 : 1);
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_bound(const int (&a)[NACC], const P&, R& bndx,
+                                                    R& bndy) {
+    bndx = bndy = a[0] ? (R)INFINITY : (R)0;
+  }
   template <int NI> __host__ __device__ static constexpr bool wzero(int, int m) { return m == 3 - NI; }
   template <class R> struct Params { R unused; };
 
@@ -611,6 +651,26 @@ struct ShallowRoe {
 struct Advection {
   static constexpr int NEQ = 1, NW = 1, NAUX = 0, NPR = 0;
   static constexpr bool STATIC_SPEEDS = true;
+  // Tile form for row-strip shards (k_speeds_t): the speeds are static, so a
+  // tile only needs probing if one of its new cells is inadmissible (then
+  // the checked probe finds the reference-order first interface); a[0] =
+  // "some cell is not finite" over the tile.  Aux is static: the first
+  // pre-pass after an upload probes every tile.
+  static constexpr bool HAS_TILE = true;
+  static constexpr int NACC = 4;
+  static constexpr unsigned ACC_MIN = 0x0u;
+  __device__ static __forceinline__ void acc_init(int (&a)[NACC]) {
+    a[0] = 0; a[1] = 0; a[2] = 0; a[3] = 0;
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_acc(const R* q, const P&, int (&a)[NACC]) {
+    a[0] = max(a[0], all_finite<R, NEQ>(q) ? 0 : 1);
+  }
+  template <class R, class P>
+  __device__ static __forceinline__ void tile_bound(const int (&a)[NACC], const P&, R& bndx,
+                                                    R& bndy) {
+    bndx = bndy = a[0] ? (R)INFINITY : (R)0;
+  }
   template <int NI> __host__ __device__ static constexpr bool wzero(int, int) { return false; }
   template <class R> struct Params { R u, v; };
 

@@ -425,3 +425,44 @@ def test_device_collective_shards_t_final_then_more(P):
     finally:
         for sh in shards:
             sh.grid.close()
+
+
+@pytest.mark.parametrize("name,dred", [("acoustics-const", False), ("acoustics-var", False),
+                                       ("acoustics-const", True)])
+def test_static_speed_shards_find_a_state_that_turns_inadmissible(name, dred):
+    # static-speed shards probe only tiles whose new cells include a
+    # non-finite one (tile pre-pass; speeds from the upload): a spike of
+    # +-1e308 is finite at step 1, overflows in its update, and step 2 must
+    # report the reference-order first interface, as the single domain does
+    from paper_1308_1464_b200 import _abi
+    nx, ny = 70, 90
+    gq, gaux = random_state(name, nx, ny, 23)
+    gq[0, 2 + 40, 2 + 61] = 1.5e308          # strip 2 of 3
+    gq[0, 2 + 41, 2 + 61] = -1.5e308
+    with pytest.raises(O.OracleError) as oe:
+        oracle_run(name, gq, gaux, nx, ny, 1 / nx, 1 / ny, steps=4, order=2, limiter="mc")
+    ref, oreps = None, None
+    out, reps, errs, _ = fake_sharded(name, gq, gaux, nx, ny, 1 / nx, 1 / ny, 3, 4, 2, "mc",
+                                      "extrapolate", device_reduce=dred)
+    for e, r in zip(errs, reps):
+        assert e.code == _abi.WS_ERR_KERNEL
+        assert e.step >= 1                     # not the first step: the overflow comes later
+        assert f"{'xy'[e.direction]}-interface (i={e.i}, j={e.j})" == str(oe.value).split(":")[0]
+        assert len(r) == e.step
+
+
+@pytest.mark.parametrize("name", ["acoustics-const", "acoustics-var"])
+def test_static_speed_shards_skip_clean_tiles_bitwise(name):
+    # the tile pre-pass of static-speed shards on a larger grid (most tiles
+    # skipped after the first step) is bitwise the single-domain oracle
+    nx, ny, steps, P = 200, 300, 6, 3
+    gq, gaux = random_state(name, nx, ny, 24)
+    ref, oreps = oracle_run(name, gq, gaux, nx, ny, 1 / nx, 1 / ny, steps=steps, order=2,
+                            limiter="mc", bc_x="periodic", bc_y="periodic")
+    out, reps, errs, strips = fake_sharded(name, gq, gaux, nx, ny, 1 / nx, 1 / ny, P, steps, 2,
+                                           "mc", "periodic")
+    for r in range(P):
+        j0, j1 = strips.bounds(r)
+        assert errs[r].code == 0
+        assert reps[r] == [o.dt for o in oreps]
+        assert np.array_equal(out[r], ref[:, 2:-2, 2 + j0:2 + j1])
