@@ -1783,6 +1783,9 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   constexpr int LW = 29, HW = 33, HC = HW * HW, NT = NWARP * 32;
   constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
   constexpr unsigned FULL = 0xffffffffu;
+  // per-tile accumulators for the next tile pre-pass (S::tile_acc): not in
+  // the checked (static-speed single-domain) and fused forms, which have none
+  constexpr bool TILES = HasTile<S>::value && !FUSED && !CHECKS;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* sQ = reinterpret_cast<R*>(smem_raw);
@@ -1875,7 +1878,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   // bound).  Runs after a barrier that follows the tile's store loop.
   int t_prev = -1;
   auto finish_tile = [&](int tt) {
-    if constexpr (HasTile<S>::value) {
+    if constexpr (TILES) {
     constexpr int NA = NAcc<S>::value;
     constexpr unsigned MINS = AccMin<S>::value;
     if (tid < NA) {
@@ -1919,7 +1922,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     if (v >= nvt) break;
     cp_wait<0>();
     __syncthreads();   // raw tile landed for every thread; previous tile fully stored
-    if constexpr (HasTile<S>::value && !FUSED) {
+    if constexpr (TILES) {
       if (A.tmax && t_prev >= 0) finish_tile(t_prev);
     }
     stage_ok = true;   // CHECKS: per tile
@@ -2011,7 +2014,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     // has completed: the step-control thread waited for it before the
     // barrier above)
     unsigned long long hk0 = 0ull;
-    const bool hwarp = HasTile<S>::value && !FUSED && A.tmax != nullptr && t_prev < 0 &&
+    const bool hwarp = TILES && A.tmax != nullptr && t_prev < 0 &&
                        warp == NWARP - 1 && lane < 2;
     if (hwarp) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
     // ---- x pass: warps walk rows; lane l = x-edge i0-1+l
@@ -2157,7 +2160,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
 
     int tb[NAcc<S>::value];   // TMAX: this thread's S::tile_acc accumulator
-    if constexpr (HasTile<S>::value) S::acc_init(tb);
+    if constexpr (TILES) S::acc_init(tb);
     // ---- row-coalesced store of the tile; the strip's two first / last rows
     // also go straight into the low / high neighbour's ghost rows (P2P
     // stores into its buffer of the same parity) when halos are pushed
@@ -2171,7 +2174,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = sX[m * (LW * LW) + idx];
         WS_CHK(L, gi >= 0 && gj >= 0, CHK_STORE);
         if (WS_CHECKED && L.chk) atomicAdd(&L.chk[1 + (long long)gj * L.nx + gi], 1u);
-        if constexpr (HasTile<S>::value && !FUSED) {
+        if constexpr (TILES) {
           // tile-bound ingredients of the new cell for the next pre-pass
           // (k_speeds_t)
           if (A.tmax) {
@@ -2193,7 +2196,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         }
       }
     }
-    if constexpr (HasTile<S>::value && !FUSED) {
+    if constexpr (TILES) {
       if (A.tmax) {
         constexpr unsigned MINS = AccMin<S>::value;
 #pragma unroll
@@ -2235,7 +2238,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   if (PERSIST) cp_wait<0>();   // no copy outstanding at exit
   __syncthreads();
   ctl = s_ctl;
-  if constexpr (HasTile<S>::value && !FUSED) {
+  if constexpr (TILES) {
     if (A.tmax && !ctl.skip && t_prev >= 0) finish_tile(t_prev);
   }
 
