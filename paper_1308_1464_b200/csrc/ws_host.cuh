@@ -439,6 +439,13 @@ template <class S, class R, int ORDER, int LIM> struct Impl {
       }
       const long long ntiles = (long long)((h->L.nx + 28) / 29) * ((h->L.ny + 28) / 29);
       if (per_sm < 1 || ntiles > (long long)per_sm * sms) return 0;
+      // inside a caller's stream capture: the per-step kernels (a refused
+      // cooperative launch would invalidate the capture)
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return 0;
+      }
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)ntiles);
       cfg.blockDim = dim3(NWR * 32);

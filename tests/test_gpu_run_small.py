@@ -146,3 +146,42 @@ def test_run_small_back_to_back_runs_and_steps():
         assert np.array_equal(g.download(), ref)
     finally:
         g.close()
+
+
+def test_step_inside_a_caller_capture_uses_the_per_step_kernels():
+    # ws_step on a small static-speed grid is one k_run_small launch, except
+    # inside a caller's stream capture (a cooperative launch there could
+    # invalidate it): the captured graph replays bitwise
+    import torch
+    from paper_1308_1464_b200 import DeviceGrid, _abi, make_kernel
+    name, nx, ny = "acoustics-const", 64, 48
+    q, aux = random_state(name, nx, ny, 56)
+    ref, oreps = oracle_run(name, q, aux, nx, ny, 1 / nx, 1 / ny, steps=8, order=2,
+                            limiter="mc", bc_x="periodic", bc_y="periodic")
+    g = DeviceGrid(nx, ny, 1 / nx, 1 / ny, make_kernel(name, **PARAMS[name]), order=2,
+                   limiter="mc", bc_x="periodic", bc_y="periodic")
+    try:
+        s = torch.cuda.Stream()
+        g.upload(q, aux, stream=s.cuda_stream)
+        ctl = _abi.make_ctl(0.9)
+        g.step(ctl, stream=s.cuda_stream)
+        g.step(ctl, stream=s.cuda_stream)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        g.capture_begin()
+        with torch.cuda.graph(graph, stream=s):
+            g.step(ctl, stream=s.cuda_stream)
+            g.step(ctl, stream=s.cuda_stream)
+        steps, launches = g.capture_end()
+        assert steps == 2 and launches == 2          # the per-step update kernels
+        for _ in range(3):
+            with torch.cuda.stream(s):
+                graph.replay()
+            g.replayed(steps, launches)
+        torch.cuda.synchronize()
+        res = g.poll()
+        assert res.error.code == 0 and res.steps_done == 8
+        assert [r[0] for r in res.reports] == [o.dt for o in oreps]
+        assert np.array_equal(g.download(stream=s.cuda_stream), ref)
+    finally:
+        g.close()
