@@ -521,6 +521,19 @@ def gpu_arm(args):
                                             "capture x cells / event-timed update kernel, "
                                             "against the measured DFMA peak",
                                     "peak_source": pr.get("fp64_peak_source")}
+            if pr.get("instr_per_cell"):
+                # the first binding resource: issue (one warp instruction per
+                # clock and scheduler)
+                ic = pr["instr_per_cell"] * cells / (upd_ms / 1e3)
+                roofline["issue"] = {"instr_per_cell": pr["instr_per_cell"],
+                                     "achieved_instr_per_s": ic,
+                                     "peak_instr_per_s": pr["issue_peak_instr_per_s"],
+                                     "frac": ic / pr["issue_peak_instr_per_s"],
+                                     "issue_active_frac_ncu": pr["issue_active_pct"] / 100.0,
+                                     "note": "warp-lane instructions per cell from the ncu "
+                                             "capture x cells / event-timed update kernel, "
+                                             "against 148 SMs x 4 schedulers x 32 lanes x "
+                                             "1965 MHz"}
         except Exception:
             pass
 

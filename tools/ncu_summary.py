@@ -84,8 +84,11 @@ def main():
     ap.add_argument("raw")
     ap.add_argument("--json", default=None)
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--cells", type=float, default=1024 * 1024)
+    ap.add_argument("--cells", type=float, default=None,
+                    help="cells per launch (default: the --config's grid)")
     a = ap.parse_args()
+    if a.cells is None:
+        a.cells = float({"c1": 256, "c2": 1024, "c3": 4096, "c4": 8192, "c5": 16384}[a.config] ** 2)
     table, _ = launches(a.launches)
     print("## Launch list (cold-cache, serialised; shares)\n")
     print(table)
@@ -150,6 +153,8 @@ def main():
             "issue_active_pct": num(upd, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "ncu_duration_us": dur_us,
             "fp64_instr_per_cell_approx": round(per_cell) if per_cell else None,
+            "instr_per_cell": round(num(upd, "smsp__inst_executed.sum") * 32 / a.cells),
+            "issue_peak_instr_per_s": 148 * 4 * 32 * 1.965e9,
             "fp64_peak_instr_per_s": 18.05e12,
             "fp64_peak_source": "profiles/r1_fp64_peak.json"}
         with open(a.json, "w") as f:
