@@ -505,9 +505,10 @@ def gpu_arm(args):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                pr = json.load(f).get(args.config, {})
+                # entries per config, and per config + precision for fp32
+                pr = json.load(f).get(args.config if prec == "f64" else f"{args.config}_{prec}", {})
             roofline["traffic"] = pr.get("bytes_per_launch")
-            if pr.get("fp64_pipe_active_pct") is not None:
+            if pr.get("fp64_instr_per_cell_approx"):
                 # the binding resource: FP64 pipe, from the ncu capture
                 ipc = pr.get("fp64_instr_per_cell_approx")
                 pk = pr.get("fp64_peak_instr_per_s")

@@ -84,6 +84,8 @@ def main():
     ap.add_argument("raw")
     ap.add_argument("--json", default=None)
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--key", default=None,
+                    help="entry name in the --json file (default: --config; e.g. c5_f32)")
     ap.add_argument("--cells", type=float, default=None,
                     help="cells per launch (default: the --config's grid)")
     a = ap.parse_args()
@@ -141,7 +143,7 @@ def main():
             js = json.load(open(a.json))
         except Exception:
             js = {}
-        js[a.config] = {
+        js[a.key or a.config] = {
             "bytes_per_launch": int(b), "kernel": names[ks.index(upd)],
             "source": f"{a.raw} (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
             "note": ("1024^2 state (25 MB) is L2-resident: q_new stays in the 126 MB L2 "
@@ -152,7 +154,7 @@ def main():
             "fp64_pipe_active_pct": fp,
             "issue_active_pct": num(upd, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "ncu_duration_us": dur_us,
-            "fp64_instr_per_cell_approx": round(per_cell) if per_cell else None,
+            "fp64_instr_per_cell_approx": round(per_cell) if per_cell and fp > 1.0 else None,
             "instr_per_cell": round(num(upd, "smsp__inst_executed.sum") * 32 / a.cells),
             "issue_peak_instr_per_s": 148 * 4 * 32 * 1.965e9,
             "fp64_peak_instr_per_s": 18.05e12,
