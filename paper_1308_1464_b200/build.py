@@ -91,7 +91,8 @@ def _build(OUT: Path, verbose: bool, defines: tuple) -> Path:
     def compile_one(src: Path):
         obj = objdir / (src.stem + ".o")
         flags = FAST_FLAGS if src.name.startswith("ws_inst_fast_") else NVCC_FLAGS
-        cmd = [nvcc(), *flags, *(f"-D{d}" for d in defines), "-Xptxas", "-v", "-c",
+        extra = os.environ.get("WS_NVCC_EXTRA", "").split()   # experiments only
+        cmd = [nvcc(), *flags, *extra, *(f"-D{d}" for d in defines), "-Xptxas", "-v", "-c",
                "-o", str(obj), str(src)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, cmd, res
