@@ -28,11 +28,43 @@
 #ifndef WS_F32_MINB
 #define WS_F32_MINB 4   // fp32 10-warp line-kernel CTAs per SM, 1-3 components (48 registers)
 #endif
+// Line-kernel variants chosen per solver and precision from A/B runs on one
+// B200 (profiles/r2_s5_ab.md); -1 = that policy, 0 / 1 force a form for
+// experiments.  The update kernel sits at its register cap (64 at three
+// CTAs per SM), where fewer instructions do not always mean a faster kernel.
+#ifndef WS_ROWSTAGE
+#define WS_ROWSTAGE -1  // halo tile staged a row per warp (uniform row addressing)
+#endif
+#ifndef WS_ROWSTORE
+#define WS_ROWSTORE -1  // tile stored a row per warp
+#endif
+#ifndef WS_LIMSEL
+#define WS_LIMSEL -1    // limiter ratio: one select on phi instead of guarded operands
+#endif
+#ifndef WS_STGB
+#define WS_STGB -1      // staged cells per thread and batch of loads (0: all at once)
+#endif
 #ifndef WS_GAS2
 #define WS_GAS2 1   // 4-component fp64 on 10-warp CTAs, two per SM (0: 15 warps, one, persistent)
 #endif
 
 namespace ws {
+
+template <class S, class R> struct LinePolicy {
+  static constexpr bool F64 = sizeof(R) == 8;
+  // C4 +3.7 %, C3 +1.7 % (two-wave solvers); three-wave fp64 -4 %, fp32 -1.5 %
+  static constexpr bool LIMSEL = WS_LIMSEL < 0 ? (F64 && S::NW == 2) : (WS_LIMSEL != 0);
+  // C3 (two CTAs per SM, 96 registers) +1.3 % / +1.6 %, all three +3.1 %;
+  // three-component fp64 at 64 registers: -10 % (C5), -2 % (C4)
+  static constexpr bool ROWSTAGE = WS_ROWSTAGE < 0 ? (F64 && S::NEQ >= 4) : (WS_ROWSTAGE != 0);
+  static constexpr bool ROWSTORE = WS_ROWSTORE < 0 ? (F64 && S::NEQ >= 4) : (WS_ROWSTORE != 0);
+  // loads of one batch in flight per thread: (NEQ + NAUX) * batch values.
+  // Five fp64 values per cell (C4) times four cells spill at 64 registers
+  // (batches of 2: no spills, same speed); C3 +3.2 % on top of ROWSTAGE, fp32
+  // +0.7 % (C5) / +1.6 % (C4); three-component fp64 (C5, C2) -1 %
+  static constexpr int STGB = WS_STGB < 0 ? ((!F64 || S::NEQ >= 4 || S::NEQ + S::NAUX >= 5) ? 2 : 0)
+                                          : WS_STGB;
+};
 
 // --------------------------------------------------------------------------
 // block reductions
@@ -1705,11 +1737,29 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
     // the NW limiter ratios as independent FastMath divisions, one fallback
     R thw[NW];
     bool okt = true;
+    // LIMSEL: theta = dup / dow, 0 where dow == 0.  dup == +-0 gives theta =
+    // +-0 (dow is a sum of squares: positive, and NaN only together with
+    // dup), and every limiter maps +-0 to +0: so phi = +0 whenever dup == 0
+    // or dow == 0, the quotient is unguarded and its range test only counts
+    // otherwise
+    constexpr bool LIMSEL = LinePolicy<S, R>::LIMSEL;
+    bool spw[NW];
+    if constexpr (LIMSEL) {
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const bool nz = doww[w] != (R)0;
-      const R q = FastMath::div(nz ? dupw[w] : (R)0, nz ? doww[w] : (R)1, okt);
-      thw[w] = nz ? q : (R)0;
+      for (int w = 0; w < NW; ++w) {
+        bool okc;
+        thw[w] = FastMath::div_core(dupw[w], doww[w], okc);
+        spw[w] = (doww[w] == (R)0) || (dupw[w] == (R)0);
+        okt = okt && (spw[w] || okc);
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const bool nz = doww[w] != (R)0;
+        const R q = FastMath::div(nz ? dupw[w] : (R)0, nz ? doww[w] : (R)1, okt);
+        thw[w] = nz ? q : (R)0;
+        spw[w] = false;
+      }
     }
     if (!okt) {
 #pragma unroll
@@ -1719,6 +1769,7 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
     for (int w = 0; w < NW; ++w) {
       R th = thw[w];
       R ph = limiter_phi<LIM>(th);
+      if (LIMSEL && LIM != LIM_NONE) ph = spw[w] ? (R)0 : ph;
       R a = fabs(s[w]);
       R coef = a * ((R)1 - dtdn * a);
       R cph = coef * ph;
@@ -1949,29 +2000,52 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     // primitives: the loads' latency is paid once per tile, not per cell.
     // L2 loads (ld.global.cg): this grid may have launched before the
     // pre-pass finished, so nothing is taken from a possibly stale L1 line
-    constexpr int NSTG = (HC + NT - 1) / NT;
-    R qs[NSTG][NEQ], as[NSTG][NA1];
+    // ROWSTAGE: a halo row per warp and slot (lane = column 0..31: the
+    // row's address is warp-uniform, the shared-memory index row * HW +
+    // lane); column 32 of rows 0..31 in the free last slot of warp NWARP-2.
+    // The halo's four 2 x 2 corners feed no edge, so the one cell left over
+    // (32, 32) is not staged at all.
+    constexpr bool ROWSTAGE = LinePolicy<S, R>::ROWSTAGE;
+    constexpr int NSTG = ROWSTAGE ? (HW + NWARP - 1) / NWARP : (HC + NT - 1) / NT;
+    static_assert(!ROWSTAGE || (NWARP >= 2 && (NWARP - 2) + (NSTG - 1) * NWARP >= HW),
+                  "no free slot for column 32");
+    auto slot_cell = [&](int k, int& lx, int& ly) {
+      if constexpr (ROWSTAGE) {
+        lx = lane; ly = warp + k * NWARP;
+        if (k == NSTG - 1 && warp == NWARP - 2) { lx = HW - 1; ly = lane; }
+        return ly < HW;
+      } else {
+        const int idx = tid + k * NT;
+        lx = idx % HW; ly = idx / HW;
+        return idx < HC;
+      }
+    };
+    // loads in batches of SB cells per thread (LinePolicy::STGB)
+    constexpr int SB = LinePolicy<S, R>::STGB > 0 && LinePolicy<S, R>::STGB < NSTG
+                           ? LinePolicy<S, R>::STGB : NSTG;
 #pragma unroll
-    for (int k = 0; k < NSTG; ++k) {
-      const int idx = tid + k * NT;
-      if (idx < HC) {
-        const int lx = idx % HW, ly = idx / HW;
+    for (int k0 = 0; k0 < NSTG; k0 += SB) {
+    R qs[SB][NEQ], as[SB][NA1];
+#pragma unroll
+    for (int kk = 0; kk < SB; ++kk) {
+      int lx, ly;
+      if (k0 + kk < NSTG && slot_cell(k0 + kk, lx, ly)) {
         int gi = i0 - 2 + lx, gj = j0 - 2 + ly;
         if (!inner) { gi = map_i(gi, L); gj = map_j(gj, L); }
         WS_CHK(L, gi >= 0 && gi < L.nx && row_readable(gj, L), CHK_STAGE_READ);
         const R* src = q + row_off(gj, L) + gi;
 #pragma unroll
-        for (int c = 0; c < NEQ; ++c) qs[k][c] = __ldcg(src + c * L.pitch);
+        for (int c = 0; c < NEQ; ++c) qs[kk][c] = __ldcg(src + c * L.pitch);
         if (NAUX > 0) {
           const R* asrc = aux + (long long)(gj + 2) * L.astride + gi;
 #pragma unroll
-          for (int c = 0; c < NAUX; ++c) as[k][c] = __ldcg(asrc + c * L.pitch);
+          for (int c = 0; c < NAUX; ++c) as[kk][c] = __ldcg(asrc + c * L.pitch);
         }
       }
     }
     // step control by lane 0 of the last warp (one staged cell fewer than
     // the first warps) while its loads are in flight
-    if (tid == NT - 32) {
+    if (k0 == 0 && tid == NT - 32) {
       if (!CHECKS) pdl_wait();
       if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (unsigned long long)(__ldcg(&ds->seq) + 1));
       const Ctl c0 = step_control<R>(A, ds, !CHECKS);
@@ -1980,22 +2054,24 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       s_dtd[1] = (R)(c0.dt / A.dy);
     }
 #pragma unroll
-    for (int k = 0; k < NSTG; ++k) {
-      const int idx = tid + k * NT;
-      if (idx < HC) {
+    for (int kk = 0; kk < SB; ++kk) {
+      int lx, ly;
+      if (k0 + kk < NSTG && slot_cell(k0 + kk, lx, ly)) {
+        const int idx = ly * HW + lx;
 #pragma unroll
-        for (int c = 0; c < NEQ; ++c) sQ[c * HC + idx] = qs[k][c];
+        for (int c = 0; c < NEQ; ++c) sQ[c * HC + idx] = qs[kk][c];
 #pragma unroll
-        for (int c = 0; c < NAUX; ++c) sA[c * HC + idx] = as[k][c];
+        for (int c = 0; c < NAUX; ++c) sA[c * HC + idx] = as[kk][c];
         R pc[NP1];
         if (NPR > 0) {
-          prims_fast<S>(qs[k], as[k], P, pc);
+          prims_fast<S>(qs[kk], as[kk], P, pc);
 #pragma unroll
           for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
         }
-        if (CHECKS) stage_ok = stage_ok && S::cell_ok(qs[k], as[k], pc, P);
+        if (CHECKS) stage_ok = stage_ok && S::cell_ok(qs[kk], as[kk], pc, P);
       }
     }
+    }   // batches
   }
   // CHECKS (static speeds, no pre-pass): a tile whose staged cells are all
   // admissible cannot report an error, so its edges skip the checked probe
@@ -2165,10 +2241,15 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     // also go straight into the low / high neighbour's ghost rows (P2P
     // stores into its buffer of the same parity) when halos are pushed
     const int par = A.cur ^ 1;
-    for (int idx = tid; idx < LW * LW; idx += NT) {
-      const int rr = idx / LW, c = idx % LW;
+    // ROWSTORE: a tile row per warp (lane = column), so the row address and
+    // the halo-push tests are warp-uniform; else threads walk the tile's
+    // cells linearly
+    constexpr bool ROWSTORE = LinePolicy<S, R>::ROWSTORE;
+    for (int it = ROWSTORE ? warp : tid; it < (ROWSTORE ? LW : LW * LW); it += ROWSTORE ? NWARP : NT) {
+      const int rr = ROWSTORE ? it : it / LW, c = ROWSTORE ? lane : it % LW;
+      const int idx = ROWSTORE ? rr * LW + (lane < LW ? lane : 0) : it;
       const int gi = i0 + c, gj = j0 + rr;
-      if (gi < L.nx && gj < L.ny) {
+      if (c < LW && gi < L.nx && gj < L.ny) {
         R* dst = qn + row_off(gj, L) + gi;
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) dst[m * L.pitch] = sX[m * (LW * LW) + idx];
