@@ -44,6 +44,15 @@
 #ifndef WS_STGB
 #define WS_STGB -1      // staged cells per thread and batch of loads (0: all at once)
 #endif
+// L2 prefetch of a later tile's rows (one cp.async.bulk.prefetch.L2 per halo
+// row and component, issued while this tile's own loads are in flight): the
+// tile WS_PFD CTAs ahead, about the number of co-resident CTAs (148 SMs x 3)
+#ifndef WS_L2PF
+#define WS_L2PF 1
+#endif
+#ifndef WS_PFD
+#define WS_PFD 444
+#endif
 #ifndef WS_GAS2
 #define WS_GAS2 1   // 4-component fp64 on 10-warp CTAs, two per SM (0: 15 warps, one, persistent)
 #endif
@@ -65,6 +74,39 @@ template <class S, class R> struct LinePolicy {
   static constexpr int STGB = WS_STGB < 0 ? ((!F64 || S::NEQ >= 4 || S::NEQ + S::NAUX >= 5) ? 2 : 0)
                                           : WS_STGB;
 };
+
+// bytes [p, p + n) towards L2, no register or shared-memory destination
+// (p 16-byte aligned, n a multiple of 16)
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, unsigned n) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(n) : "memory");
+}
+
+// Band prefetch for the line kernel: the CTAs of one tile row share out the
+// halo band (HW rows x components, first row jb) of a tile row further down
+// -- about WS_PFD CTAs ahead, the co-resident count -- as whole row
+// segments, one cp.async.bulk.prefetch.L2 each.  A hint: nothing waits for
+// it.  Not inlined: the update kernel sits at its register cap and its
+// allocation must not depend on this code.
+template <class R, int NEQ, int NAUX, int HW>
+__device__ __noinline__ void band_prefetch(const R* q, const R* aux, int nx, int ny,
+                                           long long pitch, long long rstride, long long astride,
+                                           int ntx, int txv, int jb) {
+  constexpr int NC = NEQ + NAUX, NRC = HW * NC;
+  const int nseg = ntx >= NRC ? ntx / NRC : 1;
+  for (int it = txv; it < NRC * nseg; it += ntx) {
+    const int sg = it / NRC, rc = it - sg * NRC;
+    const int ly = rc / NC, c = rc - ly * NC;
+    const int gj = jb + ly;
+    if (gj < 0 || gj >= ny) continue;
+    const int g0 = (int)((long long)nx * sg / nseg);
+    const int g1 = (int)((long long)nx * (sg + 1) / nseg);
+    const R* rowp = c < NEQ ? q + (long long)(gj + 2) * rstride + c * pitch
+                            : aux + (long long)(gj + 2) * astride + (c - NEQ) * pitch;
+    const unsigned long long lo = (unsigned long long)(rowp + g0) & ~15ull;
+    const unsigned long long hi = (unsigned long long)(rowp + g1) & ~15ull;
+    if (hi > lo) l2_prefetch_bulk((const void*)lo, (unsigned)(hi - lo));
+  }
+}
 
 // --------------------------------------------------------------------------
 // block reductions
@@ -1875,8 +1917,13 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     else if (A.part == 2) ty += A.tr_lo;
     return ty * ntx + tx;
   };
+  // part row -> tile row (vtile's row mapping)
+  auto vrow = [&](int ty) {
+    if (A.part == 1) { if (ty >= A.tr_lo) ty += A.tr_hi - A.tr_lo; }
+    else if (A.part == 2) ty += A.tr_lo;
+    return ty;
+  };
   int v = PERSIST ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
-  int t = vtile(v);
   auto tile_origin = [&](int tt, int& a, int& b) { a = (tt % ntx) * LW; b = (tt / ntx) * LW; };
   // raw tile + halo -> sR (BC by index mapping), one cp.async group
   auto prefetch = [&](int tt) {
@@ -1899,8 +1946,18 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
     cp_commit();
   };
-  int i0, j0;
-  tile_origin(t, i0, j0);
+  // one tile per CTA: the grid is (ntx, part rows), so the tile's column and
+  // part row are the block indices themselves (no division by ntx)
+  int t, i0, j0;
+  if (PERSIST) {
+    t = vtile(v);
+    tile_origin(t, i0, j0);
+  } else {
+    const int ty = vrow((int)blockIdx.y);
+    t = ty * ntx + (int)blockIdx.x;
+    i0 = (int)blockIdx.x * LW;
+    j0 = ty * LW;
+  }
   Ctl ctl;
   bool stage_ok = true;   // CHECKS: every staged cell admissible (per thread)
   const unsigned long long t_start = L.trace ? gtimer() : 0ull;
@@ -2020,6 +2077,17 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
         return idx < HC;
       }
     };
+    if constexpr (WS_L2PF != 0) {
+      // Band prefetch (band_prefetch above), by one thread before the tile's
+      // own loads
+      if (tid == 32) {
+        const int tyv = (int)blockIdx.y, txv = (int)blockIdx.x;
+        const int ka = (WS_PFD + ntx - 1) / ntx;
+        if (tyv + ka < (int)gridDim.y)
+          band_prefetch<R, NEQ, NAUX, HW>(q, aux, L.nx, L.ny, L.pitch, L.rstride, L.astride, ntx,
+                                          txv, vrow(tyv + ka) * LW - 2);
+      }
+    }
     // loads in batches of SB cells per thread (LinePolicy::STGB)
     constexpr int SB = LinePolicy<S, R>::STGB > 0 && LinePolicy<S, R>::STGB < NSTG
                            ? LinePolicy<S, R>::STGB : NSTG;
