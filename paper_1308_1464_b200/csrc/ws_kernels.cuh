@@ -53,6 +53,22 @@
 #ifndef WS_PFD
 #define WS_PFD 444
 #endif
+// Interior tiles staged by a non-inlined row-per-warp helper (stage_inner)
+// on NWARP - 1 warps while the last warp evaluates the step control
+#ifndef WS_FASTSTAGE
+#define WS_FASTSTAGE -1
+#endif
+// experiments on the three-wave fp64 kernel's register allocation (all off:
+// profiles/r2_s6_ab.md)
+#ifndef WS_ULOOP
+#define WS_ULOOP 0      // pass loops counted by a uniform trip index (line = warp + k * NWARP)
+#endif
+#ifndef WS_HINTLATE
+#define WS_HINTLATE 0   // hint keys loaded after the x pass instead of before it
+#endif
+#ifndef WS_EARLYSUM
+#define WS_EARLYSUM 0   // apdq_i + amdq_{i+1} formed right after the solve (before the limiter section)
+#endif
 #ifndef WS_GAS2
 #define WS_GAS2 1   // 4-component fp64 on 10-warp CTAs, two per SM (0: 15 warps, one, persistent)
 #endif
@@ -71,6 +87,11 @@ template <class S, class R> struct LinePolicy {
   // Five fp64 values per cell (C4) times four cells spill at 64 registers
   // (batches of 2: no spills, same speed); C3 +3.2 % on top of ROWSTAGE, fp32
   // +0.7 % (C5) / +1.6 % (C4); three-component fp64 (C5, C2) -1 %
+  // interior tiles through stage_inner: C4 +2.2 %, fp32 +1.6 % (C4, C5); the
+  // three-wave fp64 kernel loses its register allocation (C5 -2.7 %, C2 -2.7 %),
+  // four-component fp64 (row staging already) +-0
+  static constexpr bool FASTSTAGE =
+      WS_FASTSTAGE < 0 ? (!F64 || (S::NW == 2 && S::NEQ <= 3)) : (WS_FASTSTAGE != 0);
   static constexpr int STGB = WS_STGB < 0 ? ((!F64 || S::NEQ >= 4 || S::NEQ + S::NAUX >= 5) ? 2 : 0)
                                           : WS_STGB;
 };
@@ -1753,6 +1774,15 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
       key = kk < key ? kk : key;
     }
   }
+#if WS_EARLYSUM
+  // the cell's first-order term needs only apdq of this edge and amdq of the
+  // next: summed here, am / apl are dead through the limiter section
+#pragma unroll
+  for (int m = 0; m < NEQ; ++m) {
+    amn[m] = __shfl_down_sync(FULL, am[m], 1);
+    ap[m] = apl[m] + amn[m];
+  }
+#endif
   R f[NEQ];
   bool fz[NEQ];
 #pragma unroll
@@ -1828,11 +1858,76 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
   }
 #pragma unroll
   for (int m = 0; m < NEQ; ++m) {
+#if !WS_EARLYSUM
     ap[m] = apl[m];
     amn[m] = __shfl_down_sync(FULL, am[m], 1);
+#endif
     fr[m] = __shfl_down_sync(FULL, f[m], 1);
     fl[m] = f[m];
   }
+}
+
+// Staging of an INTERIOR tile (no boundary mapping) for the line kernel, a
+// halo row per warp and slot: lane = column 0..31, so a row's address is one
+// warp-uniform base plus the lane; column 32 of rows 0..31 goes into the free
+// last slot of the last staging warp (cell (32, 32) is one of the halo's
+// 2 x 2 corners, which feed no edge).  All of a thread's loads are issued
+// before the first is used.  Returns "every staged cell admissible" (CHECKS).
+// Not inlined, like band_prefetch: its registers are its own.
+template <class S, class R, int NSW, bool CHECKS>
+__device__ __noinline__ int stage_inner(const R* __restrict__ q, const R* __restrict__ aux,
+                                        R* __restrict__ sQ, long long pitch, long long rstride,
+                                        long long astride, int i0, int j0,
+                                        const typename S::template Params<R> P) {
+  constexpr int NEQ = S::NEQ, NAUX = S::NAUX, NPR = S::NPR;
+  constexpr int NA1 = NAUX > 0 ? NAUX : 1, NP1 = NPR > 0 ? NPR : 1;
+  constexpr int HW = 33, HC = HW * HW;
+  constexpr int NSTG = (HW + NSW - 1) / NSW;
+  static_assert(NSW >= 1 && (NSW - 1) + (NSTG - 1) * NSW >= HW, "no free slot for column 32");
+  R* sA = sQ + NEQ * HC;
+  R* sP = sA + NAUX * HC;
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  auto slot_cell = [&](int k, int& lx, int& ly) {
+    lx = lane; ly = warp + k * NSW;
+    if (k == NSTG - 1 && warp == NSW - 1) { lx = HW - 1; ly = lane; }
+    return ly < HW;
+  };
+  R qs[NSTG][NEQ], as[NSTG][NA1];
+#pragma unroll
+  for (int k = 0; k < NSTG; ++k) {
+    int lx, ly;
+    if (slot_cell(k, lx, ly)) {
+      const R* src = q + (long long)(j0 + ly) * rstride + (i0 - 2 + lx);
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) qs[k][c] = __ldcg(src + c * pitch);
+      if (NAUX > 0) {
+        const R* asrc = aux + (long long)(j0 + ly) * astride + (i0 - 2 + lx);
+#pragma unroll
+        for (int c = 0; c < NAUX; ++c) as[k][c] = __ldcg(asrc + c * pitch);
+      }
+    }
+  }
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < NSTG; ++k) {
+    int lx, ly;
+    if (slot_cell(k, lx, ly)) {
+      const int idx = ly * HW + lx;
+#pragma unroll
+      for (int c = 0; c < NEQ; ++c) sQ[c * HC + idx] = qs[k][c];
+#pragma unroll
+      for (int c = 0; c < NAUX; ++c) sA[c * HC + idx] = as[k][c];
+      R pc[NP1];
+      if (NPR > 0) {
+        prims_fast<S>(qs[k], as[k], P, pc);
+#pragma unroll
+        for (int c = 0; c < NPR; ++c) sP[c * HC + idx] = pc[c];
+      }
+      if (CHECKS) ok = ok && S::cell_ok(qs[k], as[k], pc, P);
+    }
+  }
+  return ok ? 1 : 0;
 }
 
 // device-side reduction across shards: wait until every shard pushed its
@@ -2053,6 +2148,35 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
   } else {
     // ---- stage tile + 2-cell halo (BC by index mapping), per-cell primitives
     const bool inner = i0 >= 2 && i0 + LW + 2 <= L.nx && j0 >= 2 && j0 + LW + 2 <= L.ny;
+    // step control by lane 0 of the last warp
+    auto do_ctl = [&]() {
+      if (!CHECKS) pdl_wait();
+      if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (unsigned long long)(__ldcg(&ds->seq) + 1));
+      const Ctl c0 = step_control<R>(A, ds, !CHECKS);
+      s_ctl = c0;
+      s_dtd[0] = (R)(c0.dt / A.dx);
+      s_dtd[1] = (R)(c0.dt / A.dy);
+    };
+    constexpr bool FASTSTAGE = LinePolicy<S, R>::FASTSTAGE && NWARP >= 4 && !WS_CHECKED;
+    if (FASTSTAGE && inner) {
+      // interior tile: warps 0 .. NWARP-2 stage it (stage_inner), the last
+      // warp prefetches the band further down and evaluates the step control
+      if (warp == NWARP - 1) {
+        if constexpr (WS_L2PF != 0) {
+          if (lane == 1) {
+            const int tyv = (int)blockIdx.y, txv = (int)blockIdx.x;
+            const int ka = (WS_PFD + ntx - 1) / ntx;
+            if (tyv + ka < (int)gridDim.y)
+              band_prefetch<R, NEQ, NAUX, HW>(q, aux, L.nx, L.ny, L.pitch, L.rstride, L.astride,
+                                              ntx, txv, vrow(tyv + ka) * LW - 2);
+          }
+        }
+        if (lane == 0) do_ctl();
+      } else {
+        stage_ok = stage_inner<S, R, NWARP - 1, CHECKS>(q, aux, sQ, L.pitch, L.rstride, L.astride,
+                                                        i0, j0, P) != 0;
+      }
+    } else {
     // all of this thread's loads first (NSTG cells in flight), then the
     // primitives: the loads' latency is paid once per tile, not per cell.
     // L2 loads (ld.global.cg): this grid may have launched before the
@@ -2113,14 +2237,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
     // step control by lane 0 of the last warp (one staged cell fewer than
     // the first warps) while its loads are in flight
-    if (k0 == 0 && tid == NT - 32) {
-      if (!CHECKS) pdl_wait();
-      if (!CHECKS && L.npeers > 0) wait_arrivals(ds, (unsigned long long)L.npeers * (unsigned long long)(__ldcg(&ds->seq) + 1));
-      const Ctl c0 = step_control<R>(A, ds, !CHECKS);
-      s_ctl = c0;
-      s_dtd[0] = (R)(c0.dt / A.dx);
-      s_dtd[1] = (R)(c0.dt / A.dy);
-    }
+    if (k0 == 0 && tid == NT - 32) do_ctl();
 #pragma unroll
     for (int kk = 0; kk < SB; ++kk) {
       int lx, ly;
@@ -2140,6 +2257,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       }
     }
     }   // batches
+    }   // boundary-mapped staging
   }
   // CHECKS (static speeds, no pre-pass): a tile whose staged cells are all
   // admissible cannot report an error, so its edges skip the checked probe
@@ -2160,10 +2278,18 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     unsigned long long hk0 = 0ull;
     const bool hwarp = TILES && A.tmax != nullptr && t_prev < 0 &&
                        warp == NWARP - 1 && lane < 2;
-    if (hwarp) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
+    if (!WS_HINTLATE && hwarp) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
     // ---- x pass: warps walk rows; lane l = x-edge i0-1+l
+#if WS_ULOOP
+    constexpr int NTRIP = (LW + NWARP - 1) / NWARP;
+#pragma unroll 1
+    for (int k = 0; k < NTRIP; ++k) {
+      const int r = warp + k * NWARP;
+      if (r >= LW || j0 + r >= L.ny) break;
+#else
     for (int r = warp; r < LW; r += NWARP) {
       if (j0 + r >= L.ny) break;
+#endif
       const int cl = (r + 2) * HW + lane, cr = cl + 1;
       WS_CHK(L, cl >= 0 && cr < HC, CHK_EDGE_SMEM);
       const int ei = i0 - 1 + lane;
@@ -2177,7 +2303,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
           const R qc = sQ[m * HC + cr];
-          R v = qc - dtdx * (ap[m] + amn[m]);
+          R v = qc - dtdx * (WS_EARLYSUM ? ap[m] : ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdx * (fr[m] - fl[m]);
           WS_CHK(L, r * LW + c < LW * LW, CHK_X_SMEM);
           sX[m * (LW * LW) + r * LW + c] = v;
@@ -2186,6 +2312,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
     if (hwarp) {
       int own, off;
+      if (WS_HINTLATE) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
       hint_owner(hk0, L, lane, own, off);
       s_hown[lane] = own; s_hoff[lane] = off;
     }
@@ -2195,8 +2322,15 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     const int nxv = min(LW, L.nx - i0), nyv = min(LW, L.ny - j0);
     R nmx = (R)0, nmy = (R)0;             // FUSED: next state's max |s|
     unsigned long long nkey = ~0ull;      // FUSED: next state's first bad edge
+#if WS_ULOOP
+#pragma unroll 1
+    for (int k = 0; k < NTRIP; ++k) {
+      const int c = warp + k * NWARP;
+      if (c >= LW || i0 + c >= L.nx) break;
+#else
     for (int c = warp; c < LW; c += NWARP) {
       if (i0 + c >= L.nx) break;
+#endif
       const int cl = lane * HW + c + 2, cr = cl + HW;
       WS_CHK(L, cl >= 0 && cr < HC, CHK_EDGE_SMEM);
       const int ej = j0 - 1 + lane;
@@ -2211,7 +2345,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       if (cell_lane) {
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
-          R v = sX[m * (LW * LW) + o] - dtdy * (ap[m] + amn[m]);
+          R v = sX[m * (LW * LW) + o] - dtdy * (WS_EARLYSUM ? ap[m] : ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdy * (fr[m] - fl[m]);
           sX[m * (LW * LW) + o] = v;
           qnew[m] = v;
@@ -2651,7 +2785,7 @@ k_run_small(R* __restrict__ q0, R* __restrict__ q1, const R* __restrict__ aux, c
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
           const R qc = sQ[m * HC + cr];
-          R v = qc - dtdx * (ap[m] + amn[m]);
+          R v = qc - dtdx * (WS_EARLYSUM ? ap[m] : ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdx * (fr[m] - fl[m]);
           WS_CHK(L, r * LW + c < LW * LW, CHK_X_SMEM);
           sX[m * (LW * LW) + r * LW + c] = v;
@@ -2676,7 +2810,7 @@ k_run_small(R* __restrict__ q0, R* __restrict__ q1, const R* __restrict__ aux, c
       if (cell_lane) {
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
-          R v = sX[m * (LW * LW) + o] - dtdy * (ap[m] + amn[m]);
+          R v = sX[m * (LW * LW) + o] - dtdy * (WS_EARLYSUM ? ap[m] : ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdy * (fr[m] - fl[m]);
           sX[m * (LW * LW) + o] = v;
         }
