@@ -58,17 +58,6 @@
 #ifndef WS_FASTSTAGE
 #define WS_FASTSTAGE -1
 #endif
-// experiments on the three-wave fp64 kernel's register allocation (all off:
-// profiles/r2_s6_ab.md)
-#ifndef WS_ULOOP
-#define WS_ULOOP 0      // pass loops counted by a uniform trip index (line = warp + k * NWARP)
-#endif
-#ifndef WS_HINTLATE
-#define WS_HINTLATE 0   // hint keys loaded after the x pass instead of before it
-#endif
-#ifndef WS_EARLYSUM
-#define WS_EARLYSUM 0   // apdq_i + amdq_{i+1} formed right after the solve (before the limiter section)
-#endif
 #ifndef WS_GAS2
 #define WS_GAS2 1   // 4-component fp64 on 10-warp CTAs, two per SM (0: 15 warps, one, persistent)
 #endif
@@ -1774,15 +1763,6 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
       key = kk < key ? kk : key;
     }
   }
-#if WS_EARLYSUM
-  // the cell's first-order term needs only apdq of this edge and amdq of the
-  // next: summed here, am / apl are dead through the limiter section
-#pragma unroll
-  for (int m = 0; m < NEQ; ++m) {
-    amn[m] = __shfl_down_sync(FULL, am[m], 1);
-    ap[m] = apl[m] + amn[m];
-  }
-#endif
   R f[NEQ];
   bool fz[NEQ];
 #pragma unroll
@@ -1858,10 +1838,8 @@ __device__ __forceinline__ void line_edge(const R* sQ, const R* sA, const R* sP,
   }
 #pragma unroll
   for (int m = 0; m < NEQ; ++m) {
-#if !WS_EARLYSUM
     ap[m] = apl[m];
     amn[m] = __shfl_down_sync(FULL, am[m], 1);
-#endif
     fr[m] = __shfl_down_sync(FULL, f[m], 1);
     fl[m] = f[m];
   }
@@ -2278,18 +2256,10 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     unsigned long long hk0 = 0ull;
     const bool hwarp = TILES && A.tmax != nullptr && t_prev < 0 &&
                        warp == NWARP - 1 && lane < 2;
-    if (!WS_HINTLATE && hwarp) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
+    if (hwarp) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
     // ---- x pass: warps walk rows; lane l = x-edge i0-1+l
-#if WS_ULOOP
-    constexpr int NTRIP = (LW + NWARP - 1) / NWARP;
-#pragma unroll 1
-    for (int k = 0; k < NTRIP; ++k) {
-      const int r = warp + k * NWARP;
-      if (r >= LW || j0 + r >= L.ny) break;
-#else
     for (int r = warp; r < LW; r += NWARP) {
       if (j0 + r >= L.ny) break;
-#endif
       const int cl = (r + 2) * HW + lane, cr = cl + 1;
       WS_CHK(L, cl >= 0 && cr < HC, CHK_EDGE_SMEM);
       const int ei = i0 - 1 + lane;
@@ -2303,7 +2273,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
           const R qc = sQ[m * HC + cr];
-          R v = qc - dtdx * (WS_EARLYSUM ? ap[m] : ap[m] + amn[m]);
+          R v = qc - dtdx * (ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdx * (fr[m] - fl[m]);
           WS_CHK(L, r * LW + c < LW * LW, CHK_X_SMEM);
           sX[m * (LW * LW) + r * LW + c] = v;
@@ -2312,7 +2282,6 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     }
     if (hwarp) {
       int own, off;
-      if (WS_HINTLATE) hk0 = __ldcg(&ds->hint_acc[A.cur][lane]);
       hint_owner(hk0, L, lane, own, off);
       s_hown[lane] = own; s_hoff[lane] = off;
     }
@@ -2322,15 +2291,8 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
     const int nxv = min(LW, L.nx - i0), nyv = min(LW, L.ny - j0);
     R nmx = (R)0, nmy = (R)0;             // FUSED: next state's max |s|
     unsigned long long nkey = ~0ull;      // FUSED: next state's first bad edge
-#if WS_ULOOP
-#pragma unroll 1
-    for (int k = 0; k < NTRIP; ++k) {
-      const int c = warp + k * NWARP;
-      if (c >= LW || i0 + c >= L.nx) break;
-#else
     for (int c = warp; c < LW; c += NWARP) {
       if (i0 + c >= L.nx) break;
-#endif
       const int cl = lane * HW + c + 2, cr = cl + HW;
       WS_CHK(L, cl >= 0 && cr < HC, CHK_EDGE_SMEM);
       const int ej = j0 - 1 + lane;
@@ -2345,7 +2307,7 @@ k_update_w(const R* __restrict__ q, const R* __restrict__ aux, R* __restrict__ q
       if (cell_lane) {
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
-          R v = sX[m * (LW * LW) + o] - dtdy * (WS_EARLYSUM ? ap[m] : ap[m] + amn[m]);
+          R v = sX[m * (LW * LW) + o] - dtdy * (ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdy * (fr[m] - fl[m]);
           sX[m * (LW * LW) + o] = v;
           qnew[m] = v;
@@ -2785,7 +2747,7 @@ k_run_small(R* __restrict__ q0, R* __restrict__ q1, const R* __restrict__ aux, c
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
           const R qc = sQ[m * HC + cr];
-          R v = qc - dtdx * (WS_EARLYSUM ? ap[m] : ap[m] + amn[m]);
+          R v = qc - dtdx * (ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdx * (fr[m] - fl[m]);
           WS_CHK(L, r * LW + c < LW * LW, CHK_X_SMEM);
           sX[m * (LW * LW) + r * LW + c] = v;
@@ -2810,7 +2772,7 @@ k_run_small(R* __restrict__ q0, R* __restrict__ q1, const R* __restrict__ aux, c
       if (cell_lane) {
 #pragma unroll
         for (int m = 0; m < NEQ; ++m) {
-          R v = sX[m * (LW * LW) + o] - dtdy * (WS_EARLYSUM ? ap[m] : ap[m] + amn[m]);
+          R v = sX[m * (LW * LW) + o] - dtdy * (ap[m] + amn[m]);
           if (ORDER == 2) v = v - dtdy * (fr[m] - fl[m]);
           sX[m * (LW * LW) + o] = v;
         }
