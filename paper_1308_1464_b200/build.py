@@ -37,6 +37,12 @@ FAST_FLAGS = [{"--fmad=false": "--fmad=true", "-prec-div=true": "-prec-div=false
               for f in NVCC_FLAGS]
 
 
+# per-unit additions (measured per kernel, profiles/r2_s6_ab.md): ptxas'
+# register-usage level 2 (default 5) for the three-wave fp64 shallow-water
+# kernels only
+UNIT_FLAGS = {"ws_inst_shallow_roe.cu": ["-Xptxas", "--register-usage-level=2"]}
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
         if cand and os.path.exists(cand):
@@ -92,7 +98,8 @@ def _build(OUT: Path, verbose: bool, defines: tuple) -> Path:
         obj = objdir / (src.stem + ".o")
         flags = FAST_FLAGS if src.name.startswith("ws_inst_fast_") else NVCC_FLAGS
         extra = os.environ.get("WS_NVCC_EXTRA", "").split()   # experiments only
-        cmd = [nvcc(), *flags, *extra, *(f"-D{d}" for d in defines), "-Xptxas", "-v", "-c",
+        cmd = [nvcc(), *flags, *UNIT_FLAGS.get(src.name, []), *extra, *(f"-D{d}" for d in defines),
+               "-Xptxas", "-v", "-c",
                "-o", str(obj), str(src)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, cmd, res

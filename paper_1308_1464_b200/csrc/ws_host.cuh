@@ -508,6 +508,7 @@ Ops ops_acoustics_var(int prec, int order, int lim);
 Ops ops_euler_roe(int prec, int order, int lim);
 Ops ops_euler_hlle(int prec, int order, int lim);
 Ops ops_shallow_roe(int prec, int order, int lim);
+Ops ops_f32_shallow_roe(int order, int lim);   // ws_inst_f32_shallow_roe.cu
 Ops ops_advection(int prec, int order, int lim);
 // WS_FP32_FAST: Fast<S> kernels from ws_inst_fast_*.cu (own compiler flags)
 Ops ops_fast_acoustics_const(int order, int lim);
