@@ -129,3 +129,17 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     with pytest.raises(_abi.NativeUnavailable):
         _abi.lib()
     monkeypatch.setattr(_abi, "_LIB", None)
+
+
+def test_per_unit_build_flags_name_real_units():
+    """build.py UNIT_FLAGS (ptxas options measured per kernel) must name
+    translation units that exist, and every unit is compiled exactly once."""
+    from paper_1308_1464_b200 import build
+    names = [p.name for p in build.SOURCES]
+    assert len(names) == len(set(names))
+    for unit, flags in build.UNIT_FLAGS.items():
+        assert unit in names, unit
+        assert flags and all(isinstance(f, str) for f in flags)
+    # the fp32 shallow-water kernels live in their own unit (default ptxas level)
+    assert "ws_inst_f32_shallow_roe.cu" in names
+    assert "ws_inst_f32_shallow_roe.cu" not in build.UNIT_FLAGS
