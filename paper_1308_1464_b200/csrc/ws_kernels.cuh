@@ -29,7 +29,7 @@
 #define WS_F32_MINB 4   // fp32 10-warp line-kernel CTAs per SM, 1-3 components (48 registers)
 #endif
 // Line-kernel variants chosen per solver and precision from A/B runs on one
-// B200 (profiles/r2_s5_ab.md); -1 = that policy, 0 / 1 force a form for
+// B200 (profiles/r2_s5_ab.md, profiles/r2_s6_ab.md); -1 = that policy, 0 / 1 force a form for
 // experiments.  The update kernel sits at its register cap (64 at three
 // CTAs per SM), where fewer instructions do not always mean a faster kernel.
 #ifndef WS_ROWSTAGE
@@ -44,9 +44,10 @@
 #ifndef WS_STGB
 #define WS_STGB -1      // staged cells per thread and batch of loads (0: all at once)
 #endif
-// L2 prefetch of a later tile's rows (one cp.async.bulk.prefetch.L2 per halo
-// row and component, issued while this tile's own loads are in flight): the
-// tile WS_PFD CTAs ahead, about the number of co-resident CTAs (148 SMs x 3)
+// L2 band prefetch (band_prefetch): the CTAs of a tile row share out the halo
+// band of the tile row ~WS_PFD CTAs ahead -- about the number of co-resident
+// CTAs (148 SMs x 3) -- one cp.async.bulk.prefetch.L2 per row segment, so the
+// staging loads hit L2 instead of HBM
 #ifndef WS_L2PF
 #define WS_L2PF 1
 #endif
